@@ -1,0 +1,313 @@
+/*
+ * fcdp.h - C ABI of the B200-native FCDP parameter-movement hot path.
+ *
+ * The reference (arxiv 2602.06499, `shardsim`, /root/reference/proj) is a
+ * C++20 library with no FFI of its own: its public surface is the set of free
+ * functions and value types in proj/include/shardsim/*.hpp.  This header is
+ * the C boundary a maintainer binds (ctypes / cgo / JNI) to reach
+ *
+ *   (1) that control plane, re-implemented from scratch behind the same C++
+ *       headers (include/shardsim/*.hpp), flattened to plain C types, and
+ *   (2) the data plane the reference only describes (PAPER.md:431-549,
+ *       SPEC.md:315-376): an HBM shard store with a pinned host-cache tier,
+ *       NVLink gathers fused with PEFT expansion, a throttled host-staged NIC
+ *       emulator between emulated nodes, FCDP-Cache D2H/H2D, and a gradient
+ *       reduce-scatter fused with fp32 accumulation, cast and 1/G scaling.
+ *
+ * Conventions
+ *   - Every function returns int: FCDP_OK (0) or a negative FCDP_ERR_* code.
+ *     fcdp_last_error() returns a thread-local message for the last failure.
+ *     No C++ exception crosses this boundary.  Reference ConfigError maps to
+ *     FCDP_ERR_CONFIG and ProtocolError to FCDP_ERR_PROTOCOL (error.hpp:10-20).
+ *   - Device pointers are plain `void*`; streams are `void*` (a cudaStream_t).
+ *   - Nothing here falls back to the CPU: data-plane entry points fail with
+ *     FCDP_ERR_CUDA when no device is present.
+ */
+#ifndef FCDP_H_
+#define FCDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library builds with -fvisibility=hidden */
+#endif
+
+/* ------------------------------------------------------------------ status */
+#define FCDP_OK 0
+#define FCDP_ERR_CONFIG (-1)   /* shardsim::ConfigError */
+#define FCDP_ERR_PROTOCOL (-2) /* shardsim::ProtocolError, freshness violations */
+#define FCDP_ERR_CUDA (-3)     /* CUDA runtime / driver failure, no device */
+#define FCDP_ERR_OOM (-4)      /* device or pinned-host allocation failed */
+#define FCDP_ERR_INTERNAL (-5)
+#define FCDP_ERR_TIMEOUT (-6)  /* a cross-rank wait exceeded its deadline */
+
+const char* fcdp_last_error(void);
+const char* fcdp_version(void);
+
+/* ============================================================ control plane
+ * Flattened shardsim API.  Enum integer values follow declaration order in
+ * the reference headers.
+ */
+
+/* shardsim::StrategyKind (strategy.hpp:11) */
+enum { FCDP_ZERO2 = 0, FCDP_ZERO3 = 1, FCDP_MICS = 2, FCDP_ZEROPP = 3, FCDP_FCDP = 4, FCDP_FCDP_COMM = 5 };
+/* shardsim::EventKind (schedule.hpp:14-25) */
+enum {
+  FCDP_EV_AG_INTER = 0, FCDP_EV_AG_INTRA = 1, FCDP_EV_H2D = 2, FCDP_EV_D2H = 3,
+  FCDP_EV_COMPUTE_FWD = 4, FCDP_EV_COMPUTE_BWD = 5, FCDP_EV_REDUCE_SCATTER = 6,
+  FCDP_EV_OPTIMIZER_STEP = 7, FCDP_EV_MASK_DIRTY = 8, FCDP_EV_BROADCAST = 9
+};
+/* shardsim::ParamSet (schedule.hpp:27) */
+enum { FCDP_SET_ALL = 0, FCDP_SET_TRAINABLE = 1, FCDP_SET_FROZEN = 2 };
+
+/* shardsim::LinkClass / ClusterTopology (topology.hpp:16-36); index 0 = IntraGpu,
+ * 1 = HostGpu, 2 = InterNode (LinkKind order). duplex: 0 full, 1 half. */
+typedef struct fcdp_topology {
+  int32_t num_nodes;
+  int32_t gpus_per_node;
+  double bandwidth_bytes_per_s[3];
+  double latency_s[3];
+  int32_t duplex[3];
+} fcdp_topology;
+
+/* shardsim::StrategyPlan (strategy.hpp:16-34) */
+typedef struct fcdp_plan {
+  int32_t kind;
+  int32_t subgroup_size;
+  double tau;
+  int32_t host_cache_enabled;
+} fcdp_plan;
+
+/* shardsim::CommVolume (costmodel.hpp:14-26) */
+typedef struct fcdp_comm_volume {
+  uint64_t fwd_ag_inter, bwd_ag_inter, reduce_scatter_inter, param_sync_inter;
+  uint64_t intra_node_total, h2d_total, d2h_total;
+} fcdp_comm_volume;
+
+/* shardsim::MemoryFootprint (strategy.hpp:37-49) */
+typedef struct fcdp_memory_footprint {
+  uint64_t gpu_param_shard_bytes, gpu_gradient_bytes, gpu_optimizer_bytes, gpu_persistent_bytes;
+  uint64_t gpu_cache_bytes, gpu_transient_peak_bytes, host_cache_bytes_per_node;
+} fcdp_memory_footprint;
+
+/* shardsim::ParamState (schedule.hpp:43-50); host_cached_version < 0 = nullopt */
+typedef struct fcdp_param_state {
+  int32_t layer;
+  int32_t frozen;
+  uint64_t version;
+  int32_t dirty;
+  int64_t host_cached_version;
+  int32_t gpu_cached;
+} fcdp_param_state;
+
+/* shardsim::Event (schedule.hpp:31-38) without its deps vector */
+typedef struct fcdp_event {
+  uint32_t id;
+  int32_t kind;
+  int32_t layer;
+  int32_t param_set;
+  uint64_t bytes_total;
+  uint32_t num_deps;
+} fcdp_event;
+
+typedef struct fcdp_model fcdp_model;       /* shardsim::ModelSpec */
+typedef struct fcdp_states fcdp_states;     /* std::vector<shardsim::ParamState> */
+typedef struct fcdp_program fcdp_program;   /* shardsim::EventProgram */
+
+/* collective.hpp:19-33 */
+uint64_t fcdp_ag_inter_bytes(uint64_t payload, int32_t scope_nodes);
+uint64_t fcdp_ring_intra_bytes(uint64_t payload, int32_t ring_gpus);
+
+/* topology.hpp:44-58 -> link_preset / make_topology / transfer_time */
+int fcdp_link_preset(const char* name, int32_t* kind, double* bandwidth_bytes_per_s);
+int fcdp_make_topology(int32_t num_nodes, int32_t gpus_per_node, const char* intra_preset,
+                       const char* host_preset, const char* inter_preset, fcdp_topology* out);
+int fcdp_transfer_time(uint64_t size_bytes, int32_t link_kind, const fcdp_topology* topo, double* out);
+
+/* workload.hpp:13-54 -> ModelSpec construction, model_preset, apply_lora_mask */
+int fcdp_model_create(int32_t num_layers, const int64_t* param_counts, const double* trainable_fraction,
+                      int32_t param_bytes_per_element, double optimizer_state_multiplier,
+                      int32_t batch_per_gpu, const double* fwd_compute_s_per_sample,
+                      const double* bwd_compute_s_per_sample,
+                      const int64_t* activation_bytes_per_sample, fcdp_model** out);
+int fcdp_model_preset(const char* name, fcdp_model** out);
+int fcdp_model_apply_lora_mask(const fcdp_model* model, double trainable_fraction, fcdp_model** out);
+int fcdp_model_info(const fcdp_model* model, int32_t* num_layers, int64_t* total_params,
+                    int64_t* trainable_params, int32_t* param_bytes_per_element);
+int fcdp_model_layer_bytes(const fcdp_model* model, int32_t layer, uint64_t* all, uint64_t* trainable,
+                           uint64_t* frozen);
+void fcdp_model_destroy(fcdp_model* model);
+
+/* strategy.hpp:51-65 */
+int fcdp_strategy_from_string(const char* s, int32_t* kind);
+int fcdp_memory_footprint_of(const fcdp_plan* plan, const fcdp_model* model, const fcdp_topology* topo,
+                             fcdp_memory_footprint* out);
+int fcdp_max_feasible_batch(const fcdp_plan* plan, const fcdp_model* model, const fcdp_topology* topo,
+                            uint64_t gpu_capacity_bytes, int32_t* max_batch, int32_t* oom_at_batch_1);
+
+/* costmodel.hpp:31-38 */
+int fcdp_comm_volume_of(const fcdp_plan* plan, const fcdp_model* model, const fcdp_topology* topo,
+                        uint64_t iteration, fcdp_comm_volume* out);
+int fcdp_iteration_time_estimate(const fcdp_plan* plan, const fcdp_model* model,
+                                 const fcdp_topology* topo, double* out);
+
+/* schedule.hpp:72-92 */
+int fcdp_states_init(const fcdp_model* model, fcdp_states** out);
+int fcdp_states_create(int32_t count, fcdp_states** out); /* default-initialised list */
+int fcdp_states_count(const fcdp_states* states, int32_t* count);
+int fcdp_states_get(const fcdp_states* states, int32_t index, fcdp_param_state* out);
+int fcdp_states_set(fcdp_states* states, int32_t index, const fcdp_param_state* in);
+void fcdp_states_destroy(fcdp_states* states);
+int fcdp_build_iteration(const fcdp_plan* plan, const fcdp_model* model, const fcdp_topology* topo,
+                         const fcdp_states* states, uint64_t iteration_index, int32_t prefetch,
+                         uint64_t gpu_capacity_bytes, fcdp_program** out);
+int fcdp_step_state(fcdp_states* states, const fcdp_program* program); /* in place */
+int fcdp_program_num_events(const fcdp_program* program, uint32_t* count);
+int fcdp_program_event(const fcdp_program* program, uint32_t index, fcdp_event* out, uint32_t* deps,
+                       uint32_t deps_capacity);
+/* per-layer flags: bit0 retained, bit1 clean path, bit2 dirty path */
+int fcdp_program_layer_flags(const fcdp_program* program, uint8_t* out, int32_t capacity);
+/* serialize_program (schedule.hpp:83-85); *len receives the full length (incl. when truncated) */
+int fcdp_program_serialize(const fcdp_program* program, char* buf, size_t capacity, size_t* len);
+void fcdp_program_destroy(fcdp_program* program);
+
+/* ============================================================== data plane
+ * Layer layout.  A layer is a flat natural-order buffer of E elements of
+ * `elem_bytes` (2: bf16, 4: fp32), seen as C = E*elem/16 16-byte chunks.  The
+ * PEFT trainable mask is chunk-granular (one flag per 16 B).  Trainable and
+ * frozen chunks form two portion vectors (mask-order compaction), each padded
+ * to a multiple of G chunks and split G ways: global shard r = j*N + n lives
+ * on the GPU (node n, local j); intra slice j = shards j*N .. j*N+N-1 is
+ * contiguous.  (shardsim ParamState portions, schedule.hpp:43-50.)
+ */
+typedef struct fcdp_layout fcdp_layout;
+
+/* chunk_mask: host array of num_chunks bytes (non-zero = trainable). */
+int fcdp_layout_create(int64_t num_chunks, const uint8_t* chunk_mask, int32_t elem_bytes,
+                       int32_t num_nodes, int32_t gpus_per_node, fcdp_layout** out);
+/* portion chunk counts and padded shard/slice sizes (in chunks) */
+int fcdp_layout_info(const fcdp_layout* layout, int64_t* trainable_chunks, int64_t* frozen_chunks,
+                     int64_t* shard_t, int64_t* shard_f, int64_t* slice_t, int64_t* slice_f);
+void fcdp_layout_destroy(fcdp_layout* layout);
+
+/* Stateless kernels (device pointers; `stream` is a cudaStream_t). ----------
+ * fcdp_partition:  natural -> (trainable portion, frozen portion); warp-ballot
+ *                  compaction by the chunk mask.  t / f hold >= padded sizes.
+ * fcdp_expand:     (g slice pointers per portion, each possibly a peer GPU's
+ *                  memory) -> natural layer; only portions in `param_set`
+ *                  are written.  This is the intra-node all-gather fused with
+ *                  the PEFT expansion (Alg. 1 lines 14-15).
+ * fcdp_rs_slice:   intra-node reduce-scatter of the trainable gradient: reads
+ *                  slice j's trainable chunks from g natural-layout gradient
+ *                  buffers (peer pointers), fp32 sum in fixed order 0..g-1,
+ *                  compacts.  Chunks of shard (j*N + n) go to own_out as fp32
+ *                  (times `scale` when `final_scale` != 0); the other shards
+ *                  go to wire_out in the parameter dtype (RNE) for the
+ *                  inter-node hop.
+ * fcdp_rs_finalize: out[i] = scale * sum_{m=0..N-1} part_m[i] in fixed order,
+ *                  part_n = own (fp32), part_m = wire[m] (parameter dtype).
+ * fcdp_adam_step:  AdamW on fp32 master/m/v with an fp32 grad; writes the
+ *                  parameter shard in its dtype.  Bit-exact vs oracle.
+ * fcdp_init_portion_shard: deterministic counter-based init of one shard.
+ */
+int fcdp_partition(const fcdp_layout* layout, const void* natural, void* trainable, void* frozen,
+                   void* stream);
+int fcdp_expand(const fcdp_layout* layout, const void* const* t_slices, const void* const* f_slices,
+                void* natural, int32_t param_set, void* stream);
+int fcdp_rs_slice(const fcdp_layout* layout, const void* const* grads, int32_t local_rank,
+                  int32_t node, float scale, int32_t final_scale, float* own_out, void* wire_out,
+                  void* stream);
+int fcdp_rs_finalize(int64_t n_elems, int32_t num_nodes, int32_t node, int32_t elem_bytes,
+                     const float* own, const void* wire, int64_t wire_stride_elems, float scale,
+                     float* out, void* stream);
+
+typedef struct fcdp_adam_config {
+  float lr, beta1, beta2, eps, weight_decay;
+  int32_t step; /* 1-based step for bias correction */
+} fcdp_adam_config;
+int fcdp_adam_step(int64_t n, const fcdp_adam_config* cfg, float* master, float* m, float* v,
+                   const float* grad, void* param, int32_t param_elem_bytes, void* stream);
+
+/* Init spec: element ranges of the natural layer with a rule each.
+ * kind 0: uniform(-scale, scale) from splitmix64(seed, layer, element)
+ * kind 1: constant `scale`.  Elements not covered are zero. */
+typedef struct fcdp_init_range {
+  int64_t begin, end;
+  int32_t kind;
+  float scale;
+} fcdp_init_range;
+int fcdp_init_natural(const fcdp_layout* layout, uint64_t seed, int32_t layer,
+                      const fcdp_init_range* ranges, int32_t num_ranges, void* natural, void* stream);
+
+/* ================================================================== engine
+ * One engine per process, one process per GPU.  Ranks are numbered
+ * node-major: rank = n * gpus_per_node + j.  Ranks of one job share a
+ * POSIX shared-memory control block named `shm_name` that carries the
+ * cross-rank signals, the NIC emulators' pacing state and byte counters, the
+ * inter-node staging slots, and the CUDA IPC handles of every rank's
+ * peer-visible buffers.
+ */
+typedef struct fcdp_engine fcdp_engine;
+
+typedef struct fcdp_engine_config {
+  const char* shm_name;     /* identical on every rank of the job */
+  int32_t rank, world_size; /* world_size == num_nodes * gpus_per_node */
+  int32_t device;           /* CUDA ordinal of this rank */
+  int32_t x_slots;          /* slice buffer slots (>= 2; default 3) */
+  int32_t inter_slots;      /* NIC staging slots (>= 2; default 2) */
+  int32_t nic_pacing;       /* 1: pace inter-node traffic at topology inter bandwidth */
+  int32_t use_copy_engine;  /* 1: dense intra gathers by cudaMemcpyAsync (CE) not SM kernels */
+  double timeout_s;         /* deadline for host-side cross-rank waits */
+} fcdp_engine_config;
+
+/* Counters of one rank (bytes).  Per node = sum over that node's ranks. */
+typedef struct fcdp_counters {
+  uint64_t nic_tx_fwd_ag, nic_tx_bwd_ag, nic_tx_rs;   /* bytes this rank put on its node's NIC */
+  uint64_t nic_rx_fwd_ag, nic_rx_bwd_ag, nic_rx_rs;
+  uint64_t nvlink_rx;                                  /* intra-node ingress (AG + RS) */
+  uint64_t cache_h2d, cache_d2h;                       /* FCDP-Cache PCIe bytes */
+  uint64_t staging_h2d, staging_d2h;                   /* NIC-emulator host staging bytes */
+  uint64_t ag_inter_events_fwd, ag_inter_events_bwd;
+  uint64_t nic_busy_ns;                                /* paced wire time charged by this rank */
+} fcdp_counters;
+
+/* Compute callback: `kind` FCDP_EV_COMPUTE_FWD/BWD.  `weights` is the natural
+ * gathered layer (read-only), `grad_out` the natural gradient buffer to fill
+ * in backward (NULL in forward).  Work must be enqueued on `stream`. */
+typedef int (*fcdp_compute_fn)(void* user, int32_t kind, int32_t layer, const void* weights,
+                               void* grad_out, void* stream);
+
+int fcdp_engine_create(const fcdp_engine_config* cfg, const fcdp_model* model,
+                       const fcdp_topology* topo, const fcdp_plan* plan,
+                       const uint8_t* const* chunk_masks, fcdp_engine** out);
+int fcdp_engine_init_params(fcdp_engine* e, uint64_t seed, const fcdp_init_range* const* ranges,
+                            const int32_t* num_ranges);
+int fcdp_engine_set_adam(fcdp_engine* e, const fcdp_adam_config* cfg);
+int fcdp_engine_set_compute(fcdp_engine* e, fcdp_compute_fn fn, void* user);
+/* Execute one program (built for this engine's plan/model/topology) and apply
+ * step_state.  Asynchronous: returns once every event is enqueued. */
+int fcdp_engine_run(fcdp_engine* e, const fcdp_program* program, fcdp_states* states);
+int fcdp_engine_sync(fcdp_engine* e);
+int fcdp_engine_barrier(fcdp_engine* e);
+int fcdp_engine_streams(fcdp_engine* e, void** compute_stream);
+int fcdp_engine_counters(fcdp_engine* e, int32_t rank, fcdp_counters* out);
+int fcdp_engine_reset_counters(fcdp_engine* e);
+/* Read back (device->host, synchronous) for tests: */
+int fcdp_engine_read_shard(fcdp_engine* e, int32_t layer, int32_t frozen, void* host, size_t bytes);
+int fcdp_engine_read_master(fcdp_engine* e, int32_t layer, float* host, size_t count);
+int fcdp_engine_read_grad(fcdp_engine* e, int32_t layer, float* host, size_t count);
+int fcdp_engine_read_host_cache(fcdp_engine* e, int32_t layer, int32_t frozen, void* host, size_t bytes);
+int fcdp_engine_last_gathered(fcdp_engine* e, int32_t layer, void* host, size_t bytes);
+void fcdp_engine_destroy(fcdp_engine* e);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCDP_H_ */

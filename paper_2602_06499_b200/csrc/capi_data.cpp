@@ -1,0 +1,157 @@
+// C ABI over the stateless data-plane kernels (include/fcdp.h, "data plane").
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "capi_util.hpp"
+#include "common/layout.hpp"
+#include "fcdp.h"
+#include "kernels/kernels.hpp"
+
+struct fcdp_layout {
+  fcdp::Layout host;
+  std::uint32_t* d_bits = nullptr;
+  std::uint32_t* d_tpre = nullptr;
+  ~fcdp_layout() {
+    if (d_bits) cudaFree(d_bits);
+    if (d_tpre) cudaFree(d_tpre);
+  }
+};
+
+namespace fcdp {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();  // clear sticky-free errors
+  if (e == cudaErrorMemoryAllocation) throw OomError(std::string(what) + ": " + cudaGetErrorString(e));
+  throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void upload_layout(Layout& L, std::uint32_t** d_bits, std::uint32_t** d_tpre) {
+  const std::size_t bytes = L.bits.size() * sizeof(std::uint32_t);
+  check_cuda(cudaMalloc(d_bits, bytes), "cudaMalloc(layout bits)");
+  check_cuda(cudaMalloc(d_tpre, bytes), "cudaMalloc(layout prefix)");
+  check_cuda(cudaMemcpy(*d_bits, L.bits.data(), bytes, cudaMemcpyHostToDevice), "upload layout bits");
+  check_cuda(cudaMemcpy(*d_tpre, L.tpre.data(), bytes, cudaMemcpyHostToDevice), "upload layout prefix");
+  L.dev.bits = *d_bits;
+  L.dev.tpre = *d_tpre;
+}
+
+}  // namespace fcdp
+
+using fcdp::check_cuda;
+using fcdp::guarded;
+
+extern "C" {
+
+const char* fcdp_last_error(void) { return fcdp::g_last_error.c_str(); }
+
+int fcdp_layout_create(int64_t chunks, const uint8_t* mask, int32_t eb, int32_t N, int32_t g,
+                       fcdp_layout** out) {
+  return guarded([&] {
+    auto* L = new fcdp_layout;
+    try {
+      L->host = fcdp::build_layout(chunks, mask, eb, N, g);
+      fcdp::upload_layout(L->host, &L->d_bits, &L->d_tpre);
+    } catch (...) {
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+
+int fcdp_layout_info(const fcdp_layout* L, int64_t* pt, int64_t* pf, int64_t* st, int64_t* sf,
+                     int64_t* lt, int64_t* lf) {
+  return guarded([&] {
+    const auto& d = L->host.dev;
+    if (pt) *pt = d.pt;
+    if (pf) *pf = d.pf;
+    if (st) *st = d.shard_t;
+    if (sf) *sf = d.shard_f;
+    if (lt) *lt = d.slice_t;
+    if (lf) *lf = d.slice_f;
+  });
+}
+
+void fcdp_layout_destroy(fcdp_layout* L) { delete L; }
+
+int fcdp_partition(const fcdp_layout* L, const void* natural, void* t, void* f, void* stream) {
+  return guarded([&] {
+    check_cuda(fcdp::launch_partition(L->host, natural, t, f, static_cast<cudaStream_t>(stream)),
+               "fcdp_partition");
+  });
+}
+
+int fcdp_expand(const fcdp_layout* L, const void* const* ts, const void* const* fs, void* natural,
+                int32_t set, void* stream) {
+  return guarded([&] {
+    fcdp::SlicePtrs a{}, b{};
+    for (int j = 0; j < L->host.dev.local; ++j) {
+      a.p[j] = ts ? ts[j] : nullptr;
+      b.p[j] = fs ? fs[j] : nullptr;
+    }
+    check_cuda(fcdp::launch_expand(L->host, a, b, natural, set, static_cast<cudaStream_t>(stream)),
+               "fcdp_expand");
+  });
+}
+
+int fcdp_rs_slice(const fcdp_layout* L, const void* const* grads, int32_t j, int32_t n, float scale,
+                  int32_t final_scale, float* own, void* wire, void* stream) {
+  return guarded([&] {
+    fcdp::GradPtrs gp{};
+    for (int i = 0; i < L->host.dev.local; ++i) gp.p[i] = grads[i];
+    check_cuda(fcdp::launch_rs_slice(L->host, gp, j, n, scale, final_scale != 0, own, wire,
+                                     static_cast<cudaStream_t>(stream)),
+               "fcdp_rs_slice");
+  });
+}
+
+int fcdp_rs_finalize(int64_t n, int32_t N, int32_t node, int32_t eb, const float* own, const void* wire,
+                     int64_t stride, float scale, float* out, void* stream) {
+  return guarded([&] {
+    check_cuda(fcdp::launch_rs_finalize(n, N, node, eb, own, wire, stride, scale, out,
+                                        static_cast<cudaStream_t>(stream)),
+               "fcdp_rs_finalize");
+  });
+}
+
+int fcdp_adam_step(int64_t n, const fcdp_adam_config* c, float* master, float* m, float* v,
+                   const float* grad, void* param, int32_t eb, void* stream) {
+  return guarded([&] {
+    fcdp::AdamParams p{c->lr, c->beta1, c->beta2, c->eps, c->weight_decay,
+                       static_cast<float>(1.0 - std::pow(static_cast<double>(c->beta1), c->step)),
+                       static_cast<float>(1.0 - std::pow(static_cast<double>(c->beta2), c->step))};
+    check_cuda(fcdp::launch_adam(n, p, master, m, v, grad, param, eb, static_cast<cudaStream_t>(stream)),
+               "fcdp_adam_step");
+  });
+}
+
+int fcdp_init_natural(const fcdp_layout* L, uint64_t seed, int32_t layer, const fcdp_init_range* r,
+                      int32_t nr, void* natural, void* stream) {
+  return guarded([&] {
+    auto s = static_cast<cudaStream_t>(stream);
+    fcdp::InitRange* d = nullptr;
+    if (nr > 0) {
+      check_cuda(cudaMallocAsync(&d, sizeof(fcdp::InitRange) * nr, s), "init ranges alloc");
+      static_assert(sizeof(fcdp::InitRange) == sizeof(fcdp_init_range), "init range ABI");
+      check_cuda(cudaMemcpyAsync(d, r, sizeof(fcdp::InitRange) * nr, cudaMemcpyHostToDevice, s),
+                 "init ranges upload");
+    }
+    const int64_t elems = L->host.dev.chunks * fcdp::kChunkBytes / L->host.dev.elem_bytes;
+    check_cuda(fcdp::launch_init_natural(elems, L->host.dev.elem_bytes, seed, layer, d, nr, natural, s),
+               "fcdp_init_natural");
+    if (d) check_cuda(cudaFreeAsync(d, s), "init ranges free");
+    check_cuda(cudaStreamSynchronize(s), "init sync");  // ranges live on the caller's stack
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,476 @@
+// sm_100a data-plane kernels for the FCDP parameter-movement hot path.
+//
+// Every kernel here is bandwidth-bound byte movement (HBM, NVLink peer reads):
+//   * 16-byte vector loads/stores (one 16 B "chunk" per lane),
+//   * mask handled per warp: 32 chunks = one mask word; the per-lane trainable
+//     predicate is turned into ranks with __ballot_sync + __popc and a
+//     per-word exclusive prefix precomputed once (the mask is static),
+//   * kUnroll independent chunks in flight per lane (loads issued before
+//     stores) to cover NVLink latency (~2 us) and HBM latency,
+//   * grid = a multiple of the SM count, grid-stride loops.
+// Reference semantics: the data plane is described, not implemented, by the
+// reference (Algorithm 1); the CPU restatement these kernels
+// are checked against bit-for-bit is oracle/fcdp_oracle.c.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "kernels/kernels.hpp"
+
+namespace fcdp {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+constexpr unsigned kFull = 0xffffffffu;
+
+int g_sm_count = 0;
+
+int grid_for(std::int64_t work_items, int per_block) {
+  const std::int64_t want = (work_items + per_block - 1) / per_block;
+  const std::int64_t cap = static_cast<std::int64_t>(sm_count()) * 8;
+  return static_cast<int>(std::max<std::int64_t>(1, std::min(want, cap)));
+}
+
+__device__ __forceinline__ int slice_of(std::int64_t k, std::int64_t per, int local) {
+  int j = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxLocal; ++i) j += (i < local && k >= i * per) ? 1 : 0;
+  return j;
+}
+
+__device__ __forceinline__ const uint4* pick(const SlicePtrs& s, int j) {
+  // Unrolled select keeps the pointer table in registers (no local-memory spill).
+  const void* p = s.p[0];
+#pragma unroll
+  for (int i = 1; i < kMaxLocal; ++i)
+    if (j == i) p = s.p[i];
+  return static_cast<const uint4*>(p);
+}
+
+// ------------------------------------------------------------------ expand
+// Intra-node all-gather fused with the PEFT expansion: natural chunk c takes
+// its value from rank k of its portion, which lives in slice k / slice_size
+// (that GPU's memory, local or NVLink peer).
+template <bool kWriteT, bool kWriteF>
+__global__ void __launch_bounds__(kThreads) expand_kernel(LayoutDev L, SlicePtrs ts, SlicePtrs fs,
+                                                          uint4* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t warp = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const unsigned below = (1u << lane) - 1u;
+  for (std::int64_t w0 = warp; w0 < L.words; w0 += nwarps * kUnroll) {
+    uint4 v[kUnroll];
+    std::int64_t dst[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const std::int64_t w = w0 + u * nwarps;
+      dst[u] = -1;
+      if (w < L.words) {  // warp-uniform
+        const std::int64_t c = w * 32 + lane;
+        const bool valid = c < L.chunks;
+        const bool tr = valid && ((__ldg(L.bits + w) >> lane) & 1u);
+        const unsigned ballot = __ballot_sync(kFull, tr);
+        const std::int64_t kt = static_cast<std::int64_t>(__ldg(L.tpre + w)) + __popc(ballot & below);
+        if (valid && (tr ? kWriteT : kWriteF)) {
+          const std::int64_t k = tr ? kt : c - kt;
+          const std::int64_t per = tr ? L.slice_t : L.slice_f;
+          const int j = slice_of(k, per, L.local);
+          v[u] = pick(tr ? ts : fs, j)[k - j * per];
+          dst[u] = c;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      if (dst[u] >= 0) out[dst[u]] = v[u];
+  }
+}
+
+// Dense portion (no mask): natural = concat of the g slices (each trimmed to
+// the real chunk count).  blockIdx.y selects the source slice.
+__global__ void __launch_bounds__(kThreads) concat_kernel(SlicePtrs src, std::int64_t per,
+                                                          std::int64_t total, uint4* __restrict__ out) {
+  const int j = blockIdx.y;
+  const std::int64_t lo = j * per;
+  if (lo >= total) return;
+  const std::int64_t n = std::min(per, total - lo);
+  const uint4* s = pick(src, j);
+  uint4* d = out + lo;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = s[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) d[i + u * stride] = v[u];
+  }
+  for (; i < n; i += stride) d[i] = s[i];
+}
+
+// --------------------------------------------------------------- partition
+// natural -> (trainable, frozen) portion vectors: warp-ballot compaction.
+__global__ void __launch_bounds__(kThreads) partition_kernel(LayoutDev L, const uint4* __restrict__ in,
+                                                             uint4* __restrict__ t, uint4* __restrict__ f) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t warp = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const unsigned below = (1u << lane) - 1u;
+  for (std::int64_t w = warp; w < L.words; w += nwarps) {
+    const std::int64_t c = w * 32 + lane;
+    const bool valid = c < L.chunks;
+    const bool tr = valid && ((__ldg(L.bits + w) >> lane) & 1u);
+    const unsigned ballot = __ballot_sync(kFull, tr);
+    const std::int64_t kt = static_cast<std::int64_t>(__ldg(L.tpre + w)) + __popc(ballot & below);
+    if (!valid) continue;
+    const uint4 v = in[c];
+    if (tr)
+      t[kt] = v;
+    else
+      f[c - kt] = v;
+  }
+}
+
+// ------------------------------------------------------------ reduce-scatter
+template <typename T>
+struct Vec;
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int kN = 8;
+  __device__ static void add(float* acc, const uint4& q) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(h[i]);
+      acc[2 * i] = __fadd_rn(acc[2 * i], f.x);
+      acc[2 * i + 1] = __fadd_rn(acc[2 * i + 1], f.y);
+    }
+  }
+  __device__ static uint4 pack(const float* a) {
+    uint4 q;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
+    return q;
+  }
+  __device__ static float load1(const void* p, std::int64_t i) {
+    return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+  }
+  __device__ static void store1(void* p, std::int64_t i, float x) {
+    static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(x);
+  }
+};
+template <>
+struct Vec<float> {
+  static constexpr int kN = 4;
+  __device__ static void add(float* acc, const uint4& q) {
+    acc[0] = __fadd_rn(acc[0], __uint_as_float(q.x));
+    acc[1] = __fadd_rn(acc[1], __uint_as_float(q.y));
+    acc[2] = __fadd_rn(acc[2], __uint_as_float(q.z));
+    acc[3] = __fadd_rn(acc[3], __uint_as_float(q.w));
+  }
+  __device__ static uint4 pack(const float* a) {
+    return make_uint4(__float_as_uint(a[0]), __float_as_uint(a[1]), __float_as_uint(a[2]),
+                      __float_as_uint(a[3]));
+  }
+  __device__ static float load1(const void* p, std::int64_t i) { return static_cast<const float*>(p)[i]; }
+  __device__ static void store1(void* p, std::int64_t i, float x) { static_cast<float*>(p)[i] = x; }
+};
+
+struct RsArgs {
+  std::int64_t k0, k1;          // trainable ranks of this slice
+  std::int64_t own_lo, own_hi;  // slice-relative chunk range of this rank's shard
+  float scale;
+  int final_scale;
+  int local;
+};
+
+template <typename T>
+__device__ __forceinline__ void rs_emit(const RsArgs& a, const GradPtrs& g, std::int64_t c,
+                                        std::int64_t rel, float* own_out, uint4* wire_out) {
+  constexpr int V = Vec<T>::kN;
+  uint4 q[kMaxLocal];
+#pragma unroll
+  for (int i = 0; i < kMaxLocal; ++i)
+    if (i < a.local) q[i] = static_cast<const uint4*>(g.p[i])[c];
+  float acc[V];
+#pragma unroll
+  for (int e = 0; e < V; ++e) acc[e] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kMaxLocal; ++i)  // fixed order 0..g-1: deterministic
+    if (i < a.local) Vec<T>::add(acc, q[i]);
+  if (rel >= a.own_lo && rel < a.own_hi) {
+    float4* o = reinterpret_cast<float4*>(own_out + (rel - a.own_lo) * V);
+#pragma unroll
+    for (int e = 0; e < V; e += 4) {
+      float4 r = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
+      if (a.final_scale) {
+        r.x = __fmul_rn(r.x, a.scale);
+        r.y = __fmul_rn(r.y, a.scale);
+        r.z = __fmul_rn(r.z, a.scale);
+        r.w = __fmul_rn(r.w, a.scale);
+      }
+      o[e / 4] = r;
+    }
+  } else {
+    wire_out[rel] = Vec<T>::pack(acc);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) rs_masked_kernel(LayoutDev L, GradPtrs g, RsArgs a,
+                                                             std::int64_t wb, std::int64_t we,
+                                                             float* __restrict__ own_out,
+                                                             uint4* __restrict__ wire_out) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t warp = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const unsigned below = (1u << lane) - 1u;
+  for (std::int64_t w = wb + warp; w < we; w += nwarps) {
+    const std::int64_t c = w * 32 + lane;
+    const bool valid = c < L.chunks;
+    const bool tr = valid && ((__ldg(L.bits + w) >> lane) & 1u);
+    const unsigned ballot = __ballot_sync(kFull, tr);
+    const std::int64_t kt = static_cast<std::int64_t>(__ldg(L.tpre + w)) + __popc(ballot & below);
+    if (tr && kt >= a.k0 && kt < a.k1) rs_emit<T>(a, g, c, kt - a.k0, own_out, wire_out);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) rs_dense_kernel(GradPtrs g, RsArgs a, float* __restrict__ own_out,
+                                                            uint4* __restrict__ wire_out) {
+  const std::int64_t n = a.k1 - a.k0;
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    rs_emit<T>(a, g, a.k0 + i, i, own_out, wire_out);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) rs_finalize_kernel(std::int64_t n, int nodes, int node,
+                                                               const float* __restrict__ own,
+                                                               const void* __restrict__ wire,
+                                                               std::int64_t stride, float scale,
+                                                               float* __restrict__ out) {
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += step) {
+    float acc = 0.0f;
+    for (int m = 0; m < nodes; ++m)  // fixed node order
+      acc = __fadd_rn(acc, m == node ? own[i] : Vec<T>::load1(wire, m * stride + i));
+    out[i] = __fmul_rn(acc, scale);
+  }
+}
+
+// -------------------------------------------------------------------- Adam
+template <typename T>
+__global__ void __launch_bounds__(kThreads) adam_kernel(std::int64_t n, AdamParams p, float* __restrict__ master,
+                                                        float* __restrict__ m, float* __restrict__ v,
+                                                        const float* __restrict__ grad, void* __restrict__ param) {
+  const float omb1 = __fsub_rn(1.0f, p.beta1), omb2 = __fsub_rn(1.0f, p.beta2);
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += step) {
+    const float g = grad[i];
+    float w = master[i];
+    const float mi = __fmaf_rn(p.beta1, m[i], __fmul_rn(omb1, g));
+    const float vi = __fmaf_rn(p.beta2, v[i], __fmul_rn(__fmul_rn(omb2, g), g));
+    const float mhat = __fdiv_rn(mi, p.bias_c1);
+    const float vhat = __fdiv_rn(vi, p.bias_c2);
+    const float denom = __fadd_rn(__fsqrt_rn(vhat), p.eps);
+    const float upd = __fadd_rn(__fdiv_rn(mhat, denom), __fmul_rn(p.weight_decay, w));
+    w = __fsub_rn(w, __fmul_rn(p.lr, upd));
+    m[i] = mi;
+    v[i] = vi;
+    master[i] = w;
+    Vec<T>::store1(param, i, w);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) widen_kernel(std::int64_t n, const void* __restrict__ src,
+                                                         float* __restrict__ dst) {
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += step)
+    dst[i] = Vec<T>::load1(src, i);
+}
+
+// --------------------------------------------------------------------- init
+__device__ __forceinline__ std::uint64_t splitmix64(std::uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) init_kernel(std::int64_t n, std::uint64_t seed, int layer,
+                                                        const InitRange* __restrict__ ranges, int nr,
+                                                        void* __restrict__ out) {
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t e = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += step) {
+    float x = 0.0f;
+    for (int r = 0; r < nr; ++r) {
+      if (e < ranges[r].begin || e >= ranges[r].end) continue;
+      if (ranges[r].kind == 1) {
+        x = ranges[r].scale;
+      } else {
+        const std::uint64_t z =
+            splitmix64(seed ^ (static_cast<std::uint64_t>(layer) << 40) ^ static_cast<std::uint64_t>(e));
+        const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f);  // exact
+        x = __fmul_rn(__fsub_rn(__fmul_rn(2.0f, u), 1.0f), ranges[r].scale);
+      }
+      break;
+    }
+    Vec<T>::store1(out, e, x);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) copy_kernel(const uint4* __restrict__ s, uint4* __restrict__ d,
+                                                        std::int64_t n) {
+  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = s[i + u * stride];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) d[i + u * stride] = v[u];
+  }
+  for (; i < n; i += stride) d[i] = s[i];
+}
+
+}  // namespace
+
+int sm_count() {
+  if (g_sm_count == 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      g_sm_count = n;
+    else
+      return 148;
+  }
+  return g_sm_count;
+}
+
+cudaError_t launch_partition(const Layout& L, const void* natural, void* t, void* f, cudaStream_t s) {
+  const std::int64_t bytes = L.dev.chunks * kChunkBytes;
+  if (L.dense_trainable()) return cudaMemcpyAsync(t, natural, bytes, cudaMemcpyDeviceToDevice, s);
+  if (L.dense_frozen()) return cudaMemcpyAsync(f, natural, bytes, cudaMemcpyDeviceToDevice, s);
+  partition_kernel<<<grid_for(L.dev.words * 32, kThreads), kThreads, 0, s>>>(
+      L.dev, static_cast<const uint4*>(natural), static_cast<uint4*>(t), static_cast<uint4*>(f));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const Layout& L, const SlicePtrs& ts, const SlicePtrs& fs, void* natural,
+                          int set, cudaStream_t s) {
+  const bool want_t = set != kSetFrozen, want_f = set != kSetTrainable;
+  uint4* out = static_cast<uint4*>(natural);
+  if (L.dense_trainable() || L.dense_frozen()) {
+    const bool tr = L.dense_trainable();
+    if (tr ? !want_t : !want_f) return cudaSuccess;
+    const std::int64_t per = tr ? L.dev.slice_t : L.dev.slice_f;
+    dim3 grid(std::max(1, grid_for(per, kThreads * kUnroll) / L.dev.local), L.dev.local);
+    concat_kernel<<<grid, kThreads, 0, s>>>(tr ? ts : fs, per, L.dev.chunks, out);
+    return cudaGetLastError();
+  }
+  const int grid = grid_for(L.dev.words * 32, kThreads * kUnroll);
+  if (want_t && want_f)
+    expand_kernel<true, true><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
+  else if (want_t)
+    expand_kernel<true, false><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
+  else
+    expand_kernel<false, true><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n, float scale,
+                            bool final_scale, float* own_out, void* wire_out, cudaStream_t s) {
+  RsArgs a;
+  a.k0 = j * L.dev.slice_t;
+  a.k1 = std::min<std::int64_t>((j + 1) * L.dev.slice_t, L.dev.pt);
+  if (a.k0 >= a.k1) return cudaSuccess;
+  a.own_lo = n * L.dev.shard_t;
+  a.own_hi = a.own_lo + L.dev.shard_t;
+  a.scale = scale;
+  a.final_scale = final_scale ? 1 : 0;
+  a.local = L.dev.local;
+  uint4* wire = static_cast<uint4*>(wire_out);
+  const bool bf16 = L.dev.elem_bytes == 2;
+  if (L.dense_trainable()) {
+    const int grid = grid_for(a.k1 - a.k0, kThreads);
+    if (bf16)
+      rs_dense_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(grads, a, own_out, wire);
+    else
+      rs_dense_kernel<float><<<grid, kThreads, 0, s>>>(grads, a, own_out, wire);
+  } else {
+    const std::int64_t wb = L.rs_word_begin[j], we = L.rs_word_end[j];
+    const int grid = grid_for((we - wb) * 32, kThreads);
+    if (bf16)
+      rs_masked_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(L.dev, grads, a, wb, we, own_out, wire);
+    else
+      rs_masked_kernel<float><<<grid, kThreads, 0, s>>>(L.dev, grads, a, wb, we, own_out, wire);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rs_finalize(std::int64_t n_elems, int nodes, int node, int elem_bytes,
+                               const float* own, const void* wire, std::int64_t wire_stride,
+                               float scale, float* out, cudaStream_t s) {
+  if (n_elems <= 0) return cudaSuccess;
+  const int grid = grid_for(n_elems, kThreads);
+  if (elem_bytes == 2)
+    rs_finalize_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(n_elems, nodes, node, own, wire,
+                                                                wire_stride, scale, out);
+  else
+    rs_finalize_kernel<float><<<grid, kThreads, 0, s>>>(n_elems, nodes, node, own, wire, wire_stride,
+                                                        scale, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam(std::int64_t n, const AdamParams& p, float* master, float* m, float* v,
+                        const float* grad, void* param, int param_elem_bytes, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = grid_for(n, kThreads);
+  if (param_elem_bytes == 2)
+    adam_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(n, p, master, m, v, grad, param);
+  else
+    adam_kernel<float><<<grid, kThreads, 0, s>>>(n, p, master, m, v, grad, param);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_natural(std::int64_t n_elems, int elem_bytes, std::uint64_t seed, int layer,
+                                const InitRange* ranges_dev, int num_ranges, void* natural,
+                                cudaStream_t s) {
+  if (n_elems <= 0) return cudaSuccess;
+  const int grid = grid_for(n_elems, kThreads);
+  if (elem_bytes == 2)
+    init_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(n_elems, seed, layer, ranges_dev, num_ranges, natural);
+  else
+    init_kernel<float><<<grid, kThreads, 0, s>>>(n_elems, seed, layer, ranges_dev, num_ranges, natural);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_widen(std::int64_t n, const void* src, int elem_bytes, float* dst, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = grid_for(n, kThreads);
+  if (elem_bytes == 2)
+    widen_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(n, src, dst);
+  else
+    widen_kernel<float><<<grid, kThreads, 0, s>>>(n, src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy(const void* src, void* dst, std::int64_t bytes, cudaStream_t s) {
+  const std::int64_t n = bytes / kChunkBytes;
+  if (n > 0)
+    copy_kernel<<<grid_for(n, kThreads * kUnroll), kThreads, 0, s>>>(static_cast<const uint4*>(src),
+                                                                      static_cast<uint4*>(dst), n);
+  const std::int64_t tail = bytes - n * kChunkBytes;
+  if (tail > 0)
+    return cudaMemcpyAsync(static_cast<char*>(dst) + n * kChunkBytes,
+                           static_cast<const char*>(src) + n * kChunkBytes, tail,
+                           cudaMemcpyDeviceToDevice, s);
+  return cudaGetLastError();
+}
+
+}  // namespace fcdp

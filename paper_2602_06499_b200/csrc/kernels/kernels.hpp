@@ -1,0 +1,66 @@
+// Launchers for the sm_100a data-plane kernels (kernels.cu).
+//
+// All kernels are HBM- or link-bound byte movers: 16-byte vector accesses,
+// warp-granular mask handling (ballot + popc over 32 chunks), grid sized as a
+// multiple of the SM count.  None of them reshapes work into GEMMs.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "common/layout.hpp"
+
+namespace fcdp {
+
+struct SlicePtrs {
+  const void* p[kMaxLocal];
+};
+struct GradPtrs {
+  const void* p[kMaxLocal];
+};
+
+enum PortionSet : int { kSetAll = 0, kSetTrainable = 1, kSetFrozen = 2 };
+
+// natural -> (t, f) compaction.  Dense layers degrade to a copy.
+cudaError_t launch_partition(const Layout& L, const void* natural, void* t, void* f, cudaStream_t s);
+
+// g slice pointers per portion -> natural layer (fused gather + PEFT expand).
+cudaError_t launch_expand(const Layout& L, const SlicePtrs& ts, const SlicePtrs& fs, void* natural,
+                          int set, cudaStream_t s);
+
+// Intra-node reduce-scatter of the trainable gradient for slice `j`.
+cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n, float scale,
+                            bool final_scale, float* own_out, void* wire_out, cudaStream_t s);
+
+// Inter-node epilogue: out = scale * sum_m part_m (fixed order).
+cudaError_t launch_rs_finalize(std::int64_t n_elems, int nodes, int node, int elem_bytes,
+                               const float* own, const void* wire, std::int64_t wire_stride,
+                               float scale, float* out, cudaStream_t s);
+
+struct AdamParams {
+  float lr, beta1, beta2, eps, weight_decay;
+  float bias_c1, bias_c2;  // 1 - beta^t, computed on the host in double
+};
+cudaError_t launch_adam(std::int64_t n, const AdamParams& p, float* master, float* m, float* v,
+                        const float* grad, void* param, int param_elem_bytes, cudaStream_t s);
+
+// Deterministic init of a natural layer; `ranges` is a device array.
+struct InitRange {
+  std::int64_t begin, end;
+  std::int32_t kind;
+  float scale;
+};
+cudaError_t launch_init_natural(std::int64_t n_elems, int elem_bytes, std::uint64_t seed, int layer,
+                                const InitRange* ranges_dev, int num_ranges, void* natural,
+                                cudaStream_t s);
+
+// Widen a portion shard (param dtype) to fp32 (master init).
+cudaError_t launch_widen(std::int64_t n, const void* src, int elem_bytes, float* dst, cudaStream_t s);
+
+// Dense 16B-vector copy kernel (SM-driven; used for peer pulls when CE is off).
+cudaError_t launch_copy(const void* src, void* dst, std::int64_t bytes, cudaStream_t s);
+
+int sm_count();
+
+}  // namespace fcdp

@@ -1,0 +1,184 @@
+"""Parity of each sm_100a data-plane kernel with the CPU oracle (bit-exact).
+
+All calls go through the C ABI (include/fcdp.h) on cuda:0; slices that in a
+real job live on NVLink peers are separate local allocations here (the
+multi-GPU path is covered by tests/test_engine_gpu.py).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.maskgen import masks
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda:0")
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def _layout(lib, chunks, mask, eb, N, g):
+    from paper_2602_06499_b200._capi import check
+    m = (C.c_uint8 * chunks)(*mask.tolist())
+    out = C.c_void_p()
+    check(lib.fcdp_layout_create(chunks, m, eb, N, g, C.byref(out)))
+    return out
+
+
+def _u8(a: np.ndarray, dev):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8).copy()).to(dev)
+
+
+SIZES = [1, 33, 4096 + 7]
+GEOS = [(1, 1), (2, 1), (1, 4), (2, 2), (2, 4), (4, 2)]
+
+
+@pytest.mark.parametrize("chunks", SIZES)
+@pytest.mark.parametrize("N,g", GEOS)
+def test_expand_bit_exact(built, chunks, N, g):
+    from paper_2602_06499_b200._capi import check
+    dev = _dev()
+    lib = built
+    rng = np.random.default_rng(chunks * 31 + N * 7 + g)
+    for name, m in masks(chunks, chunks + g):
+        geo = O.geom(chunks, m, N, g)
+        lay = _layout(lib, chunks, m, 2, N, g)
+        ts = [rng.integers(0, 256, max(geo.slice_t, 1) * 16, dtype=np.uint8) for _ in range(g)]
+        fs = [rng.integers(0, 256, max(geo.slice_f, 1) * 16, dtype=np.uint8) for _ in range(g)]
+        dts = [_u8(x, dev) for x in ts]
+        dfs = [_u8(x, dev) for x in fs]
+        for pset in (0, 1, 2):
+            ref = np.full(chunks * 16, 0x5A, np.uint8)
+            O.expand(geo, m, ts, fs, ref, pset)
+            out = torch.full((chunks * 16,), 0x5A, dtype=torch.uint8, device=dev)
+            T = (C.c_void_p * g)(*[t.data_ptr() for t in dts])
+            F = (C.c_void_p * g)(*[t.data_ptr() for t in dfs])
+            check(lib.fcdp_expand(lay, T, F, _ptr(out), pset, None))
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy(), ref), (name, pset)
+        lib.fcdp_layout_destroy(lay)
+
+
+@pytest.mark.parametrize("chunks", SIZES)
+def test_partition_bit_exact(built, chunks):
+    from paper_2602_06499_b200._capi import check
+    dev = _dev()
+    lib = built
+    rng = np.random.default_rng(chunks)
+    for name, m in masks(chunks, chunks):
+        nat = rng.integers(0, 256, chunks * 16, dtype=np.uint8)
+        t, f = O.partition(nat, m)
+        lay = _layout(lib, chunks, m, 2, 2, 2)
+        dt = torch.zeros(max(t.size, 16), dtype=torch.uint8, device=dev)
+        df = torch.zeros(max(f.size, 16), dtype=torch.uint8, device=dev)
+        check(lib.fcdp_partition(lay, _ptr(_u8(nat, dev)), _ptr(dt), _ptr(df), None))
+        torch.cuda.synchronize()
+        assert np.array_equal(dt.cpu().numpy()[:t.size], t), name
+        assert np.array_equal(df.cpu().numpy()[:f.size], f), name
+        lib.fcdp_layout_destroy(lay)
+
+
+@pytest.mark.parametrize("eb", [2, 4])
+@pytest.mark.parametrize("N,g", [(1, 1), (2, 1), (1, 4), (2, 2), (2, 4)])
+def test_rs_slice_bit_exact(built, eb, N, g):
+    from paper_2602_06499_b200._capi import check
+    dev = _dev()
+    lib = built
+    chunks = 777
+    V = 16 // eb
+    rng = np.random.default_rng(eb * 100 + N * 10 + g)
+    for name, m in masks(chunks, 11):
+        geo = O.geom(chunks, m, N, g)
+        lay = _layout(lib, chunks, m, eb, N, g)
+        x = [rng.standard_normal(chunks * V).astype(np.float32) for _ in range(g)]
+        grads = [O.f32_to_bf16(a) for a in x] if eb == 2 else x
+        dg = [_u8(a, dev) for a in grads]
+        G = (C.c_void_p * g)(*[t.data_ptr() for t in dg])
+        for j in range(g):
+            for n in range(N):
+                for final in (False, True):
+                    own, wire = O.rs_slice(geo, m, eb, grads, j, n, 1.0 / (N * g), final)
+                    down = torch.zeros(max(own.size, 4), dtype=torch.float32, device=dev)
+                    dwire = torch.zeros(max(wire.nbytes, 16), dtype=torch.uint8, device=dev)
+                    check(lib.fcdp_rs_slice(lay, G, j, n, 1.0 / (N * g), int(final), _ptr(down), _ptr(dwire), None))
+                    torch.cuda.synchronize()
+                    assert np.array_equal(down.cpu().numpy()[:own.size].view(np.uint32), own.view(np.uint32)), (name, j, n)
+                    # only non-own shard chunks of the wire buffer are defined
+                    w = dwire.cpu().numpy()[:wire.nbytes].view(wire.dtype)
+                    sel = np.ones(wire.size, bool)
+                    sel[n * geo.shard_t * V:(n + 1) * geo.shard_t * V] = False
+                    real = np.zeros(wire.size, bool)
+                    real[:max(0, min(geo.slice_t, geo.pt - j * geo.slice_t)) * V] = True
+                    sel &= real
+                    assert np.array_equal(w[sel].view(np.uint8), wire[sel].view(np.uint8)), (name, j, n)
+        lib.fcdp_layout_destroy(lay)
+
+
+@pytest.mark.parametrize("eb", [2, 4])
+def test_rs_finalize_bit_exact(built, eb):
+    from paper_2602_06499_b200._capi import check
+    dev = _dev()
+    lib = built
+    rng = np.random.default_rng(5)
+    n, N = 10007, 4
+    own = rng.standard_normal(n).astype(np.float32)
+    wf = rng.standard_normal(N * n).astype(np.float32)
+    wire = O.f32_to_bf16(wf) if eb == 2 else wf
+    for node in range(N):
+        ref = O.rs_finalize(own, wire, N, node, eb, n, 0.125)
+        out = torch.zeros(n, dtype=torch.float32, device=dev)
+        check(lib.fcdp_rs_finalize(n, N, node, eb, _ptr(_u8(own, dev)), _ptr(_u8(wire, dev)), n,
+                                   0.125, _ptr(out), None))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("eb", [2, 4])
+def test_adam_bit_exact(built, eb):
+    from paper_2602_06499_b200 import _capi
+    dev = _dev()
+    lib = built
+    rng = np.random.default_rng(9)
+    n = 50001
+    w = rng.standard_normal(n).astype(np.float32)
+    m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+    p = np.zeros(n, np.uint16 if eb == 2 else np.float32)
+    dw, dm, dv = (torch.from_numpy(a.copy()).to(dev) for a in (w, m, v))
+    dp = torch.zeros(n * eb, dtype=torch.uint8, device=dev)
+    for step in range(1, 4):
+        g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+        O.adam(w, m, v, g, p, 1e-3, 0.9, 0.95, 1e-8, 0.1, step)
+        cfg = _capi.AdamConfig(1e-3, 0.9, 0.95, 1e-8, 0.1, step)
+        _capi.check(lib.fcdp_adam_step(n, C.byref(cfg), _ptr(dw), _ptr(dm), _ptr(dv),
+                                       _ptr(torch.from_numpy(g).to(dev)), _ptr(dp), eb, None))
+        torch.cuda.synchronize()
+        assert np.array_equal(dw.cpu().numpy().view(np.uint32), w.view(np.uint32)), step
+        assert np.array_equal(dv.cpu().numpy().view(np.uint32), v.view(np.uint32)), step
+        assert np.array_equal(dp.cpu().numpy(), p.view(np.uint8)), step
+
+
+@pytest.mark.parametrize("eb", [2, 4])
+def test_init_bit_exact(built, eb):
+    from paper_2602_06499_b200 import _capi
+    dev = _dev()
+    lib = built
+    chunks = 5000
+    n = chunks * 16 // eb
+    lay = _layout(lib, chunks, np.ones(chunks, np.uint8), eb, 1, 1)
+    ranges = [(0, n // 2, 0, 0.02), (n // 2, n // 2 + 100, 1, 1.0), (n // 2 + 100, n, 0, 0.5)]
+    ref = O.init_natural(n, eb, 0x5EED, 7, ranges)
+    R = (_capi.InitRange * 3)(*[_capi.InitRange(*r) for r in ranges])
+    out = torch.zeros(n * eb, dtype=torch.uint8, device=dev)
+    _capi.check(lib.fcdp_init_natural(lay, 0x5EED, 7, R, 3, _ptr(out), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref.view(np.uint8))
+    lib.fcdp_layout_destroy(lay)
