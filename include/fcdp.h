@@ -3,11 +3,11 @@
  *
  * The reference (arxiv 2602.06499, `shardsim`, /root/reference/proj) is a
  * C++20 library with no FFI of its own: its public surface is the set of free
- * functions and value types in proj/include/shardsim/*.hpp.  This header is
+ * functions and value types in proj/include/shardsim/ (*.hpp).  This header is
  * the C boundary a maintainer binds (ctypes / cgo / JNI) to reach
  *
  *   (1) that control plane, re-implemented from scratch behind the same C++
- *       headers (include/shardsim/*.hpp), flattened to plain C types, and
+ *       headers (include/shardsim/), flattened to plain C types, and
  *   (2) the data plane the reference only describes (PAPER.md:431-549,
  *       SPEC.md:315-376): an HBM shard store with a pinned host-cache tier,
  *       NVLink gathers fused with PEFT expansion, a throttled host-staged NIC
@@ -303,6 +303,13 @@ int fcdp_engine_read_grad(fcdp_engine* e, int32_t layer, float* host, size_t cou
 int fcdp_engine_read_host_cache(fcdp_engine* e, int32_t layer, int32_t frozen, void* host, size_t bytes);
 int fcdp_engine_last_gathered(fcdp_engine* e, int32_t layer, void* host, size_t bytes);
 void fcdp_engine_destroy(fcdp_engine* e);
+
+/* Host-only protocol self-test (no GPU needed): attach the shared control
+ * block, run `rounds` barrier-separated rounds in which every rank charges
+ * `payload` bytes to its node's NIC emulator, return the wall time.  A node's
+ * ranks serialise on its single NIC, nodes run in parallel. */
+int fcdp_nic_selftest(const char* shm_name, int32_t rank, int32_t num_nodes, int32_t gpus_per_node,
+                      double bytes_per_s, uint64_t payload, int32_t rounds, double* elapsed_s);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -158,6 +158,7 @@ SIGNATURES = {
     "fcdp_engine_read_host_cache": (C.c_int, [P, i32, i32, P, C.c_size_t]),
     "fcdp_engine_last_gathered": (C.c_int, [P, i32, P, C.c_size_t]),
     "fcdp_engine_destroy": (None, [P]),
+    "fcdp_nic_selftest": (C.c_int, [C.c_char_p, i32, i32, i32, f64, u64, i32, C.POINTER(f64)]),
 }
 
 _lib = None

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "fcdp.h"
 #include "shardsim/error.hpp"
 #include "shardsim/schedule.hpp"
@@ -25,6 +27,7 @@ struct TimeoutError : std::runtime_error {
 };
 
 void set_last_error(const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
 
 template <typename F>
 int guarded(F&& body) {

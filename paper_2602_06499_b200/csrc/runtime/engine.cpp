@@ -1,0 +1,797 @@
+// Per-rank FCDP engine (see engine.hpp for the overall contract).
+//
+// Event semantics follow the reference builder (proj/src/schedule.cpp:107-292)
+// and Algorithm 1; the data layout is the one in
+// common/layout.hpp.  Cross-rank ordering uses monotone 32-bit flags in the
+// shared control block:
+//   slice fill q :  [wait peers SliceFree >= q-K] fill X[q%K] [SliceReady=q]
+//   pull       q :  [wait peers SliceReady >= q] expand/gather -> W [SliceFree=q]
+//   inter send s :  [wait receivers RxDone >= s-K] D2H -> staging slot
+//                   -> NIC thread paces, then TxReady=s
+//   inter recv s :  [wait senders TxReady >= s] H2D from their slots [RxDone=s]
+//   rs         u :  [GradReady=u] [wait peers GradReady >= u] pull-reduce [GradFree=u]
+// Every rank walks the same program, so sequence numbers agree and no wait
+// can close a cycle (each rank publishes before it waits on the same index).
+#include "runtime/engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "capi_util.hpp"
+#include "runtime/streamops.hpp"
+
+namespace fcdp {
+
+void check_cuda(cudaError_t e, const char* what);
+
+namespace {
+
+#define CK(expr) check_cuda((expr), #expr)
+
+using shardsim::Event;
+using shardsim::EventKind;
+using shardsim::ParamSet;
+
+constexpr int kStagedRing = 32;
+
+std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
+
+template <typename T>
+T* dalloc(std::size_t bytes, const char* what) {
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, std::max<std::size_t>(bytes, 256));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw OomError(std::string("cudaMalloc(") + what + ", " + std::to_string(bytes) + " B) failed: " +
+                   cudaGetErrorString(e));
+  }
+  check_cuda(cudaMemset(p, 0, std::max<std::size_t>(bytes, 256)), what);
+  return static_cast<T*>(p);
+}
+
+bool wants_t(ParamSet s) { return s != ParamSet::FrozenOnly; }
+bool wants_f(ParamSet s) { return s != ParamSet::TrainableOnly; }
+
+}  // namespace
+
+Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
+               const shardsim::ClusterTopology& topo, const shardsim::StrategyPlan& plan,
+               const std::uint8_t* const* chunk_masks)
+    : cfg_(cfg), shm_name_(cfg.shm_name ? cfg.shm_name : ""), model_(model), topo_(topo), plan_(plan) {
+  topo_.validate();
+  plan_.validate(topo_);
+  model_.validate();
+  if (plan_.kind != shardsim::StrategyKind::Zero3 && plan_.kind != shardsim::StrategyKind::Fcdp &&
+      plan_.kind != shardsim::StrategyKind::FcdpComm)
+    throw shardsim::ConfigError("engine: the B200 data plane executes zero3, fcdp and fcdp-comm programs");
+  if (shm_name_.empty()) throw shardsim::ConfigError("engine: shm_name is required");
+  N_ = topo_.num_nodes;
+  g_ = topo_.gpus_per_node;
+  G_ = N_ * g_;
+  if (g_ > kMaxLocal || N_ > kMaxNodes) throw shardsim::ConfigError("engine: at most 8 nodes x 8 GPUs");
+  if (cfg.world_size != G_) throw shardsim::ConfigError("engine: world_size must equal num_nodes * gpus_per_node");
+  rank_ = cfg.rank;
+  n_ = rank_ / g_;
+  j_ = rank_ % g_;
+  eb_ = model_.param_bytes_per_element;
+  V_ = kChunkBytes / eb_;
+  if (cfg_.x_slots < 2) cfg_.x_slots = 3;
+  if (cfg_.inter_slots < 2) cfg_.inter_slots = 2;
+  if (cfg_.timeout_s <= 0) cfg_.timeout_s = 300.0;
+  use_ce_ = cfg_.use_copy_engine != 0;
+
+  CK(cudaSetDevice(cfg_.device));
+  build_layouts(chunk_masks);
+
+  std::uint64_t slot_bytes = 0;
+  for (const LayerRt& l : layers_) {
+    slot_bytes = std::max<std::uint64_t>(slot_bytes, (l.L.dev.shard_t + l.L.dev.shard_f) * kChunkBytes);
+    slot_bytes = std::max<std::uint64_t>(slot_bytes, l.L.dev.slice_t * kChunkBytes);
+  }
+  shm_ = std::make_unique<SharedBlock>(shm_name_, rank_, G_, N_, g_, cfg_.inter_slots, slot_bytes, cfg_.timeout_s);
+  CK(cudaHostRegister(shm_->base(), shm_->bytes(), cudaHostRegisterPortable | cudaHostRegisterMapped));
+  CK(cudaHostGetDevicePointer(&shm_dev_base_, shm_->base(), 0));
+  if (!StreamOps::available()) throw CudaError("engine: stream memory operations unavailable on this device");
+
+  allocate();
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithPriority(&s_comp_, cudaStreamNonBlocking, lo));
+  CK(cudaStreamCreateWithPriority(&s_gather_, cudaStreamNonBlocking, hi));
+  CK(cudaStreamCreateWithPriority(&s_cache_, cudaStreamNonBlocking, hi));
+  CK(cudaStreamCreateWithPriority(&s_rs_, cudaStreamNonBlocking, hi));
+  x_reader_.assign(static_cast<std::size_t>(cfg_.x_slots), nullptr);
+  for (auto& e : x_reader_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : rs_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&iter_done_, cudaEventDisableTiming));
+  for (auto& e : join_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  staged_.assign(kStagedRing, nullptr);
+  for (auto& e : staged_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
+  exchange_handles();
+  nic_ = std::make_unique<NicEmulator>(*shm_, rank_, n_, cfg_.device, topo_.inter_node.bandwidth_bytes_per_s,
+                                       cfg_.nic_pacing != 0);
+  shm_->barrier(cfg_.timeout_s);
+}
+
+Engine::~Engine() {
+  try {
+    sync();
+    if (shm_) shm_->barrier(cfg_.timeout_s);  // no peer still reads our memory
+  } catch (...) {
+  }
+  nic_.reset();
+  for (int jj = 0; jj < g_; ++jj)
+    if (jj != j_ && peer_base_[jj]) cudaIpcCloseMemHandle(peer_base_[jj]);
+  for (cudaEvent_t e : ev_done_) cudaEventDestroy(e);
+  for (cudaEvent_t e : x_reader_) cudaEventDestroy(e);
+  for (cudaEvent_t e : staged_) cudaEventDestroy(e);
+  for (cudaEvent_t e : rs_done_) cudaEventDestroy(e);
+  if (iter_done_) cudaEventDestroy(iter_done_);
+  for (cudaEvent_t e : join_)
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_})
+    if (s) cudaStreamDestroy(s);
+  for (void* p : {static_cast<void*>(param_t_), static_cast<void*>(param_f_), static_cast<void*>(master_),
+                  static_cast<void*>(adam_m_), static_cast<void*>(adam_v_), static_cast<void*>(grad32_),
+                  static_cast<void*>(w_slots_[0]), static_cast<void*>(w_slots_[1]),
+                  static_cast<void*>(peer_arena_), static_cast<void*>(own32_[0]), static_cast<void*>(own32_[1]),
+                  static_cast<void*>(wire_[0]), static_cast<void*>(wire_[1]), static_cast<void*>(rx_[0]),
+                  static_cast<void*>(rx_[1])})
+    if (p) cudaFree(p);
+  for (unsigned char* p : retained_)
+    if (p) cudaFree(p);
+  for (LayerRt& l : layers_) {
+    if (l.d_bits) cudaFree(l.d_bits);
+    if (l.d_tpre) cudaFree(l.d_tpre);
+  }
+  if (host_cache_) cudaFreeHost(host_cache_);
+  if (shm_) cudaHostUnregister(shm_->base());
+  shm_.reset();
+}
+
+// ------------------------------------------------------------------- setup
+
+void Engine::build_layouts(const std::uint8_t* const* masks) {
+  const int L = model_.num_layers();
+  layers_.resize(static_cast<std::size_t>(L));
+  const int r = j_ * N_ + n_;  // global shard index of this GPU
+  for (int l = 0; l < L; ++l) {
+    LayerRt& lr = layers_[l];
+    const std::int64_t E = model_.layers[l].param_count;
+    if ((E * eb_) % kChunkBytes != 0)
+      throw shardsim::ConfigError("layer " + std::to_string(l) + ": " + std::to_string(E) +
+                                  " params is not a whole number of 16-byte chunks");
+    lr.elems = E;
+    lr.chunks = E * eb_ / kChunkBytes;
+    const std::int64_t trainable = shardsim::layer_trainable_params(model_.layers[l]);
+    std::vector<std::uint8_t> derived;
+    const std::uint8_t* mask = masks ? masks[l] : nullptr;
+    if (!mask) {
+      if ((trainable * eb_) % kChunkBytes != 0)
+        throw shardsim::ConfigError("layer " + std::to_string(l) +
+                                    ": trainable_fraction does not select whole 16-byte chunks; pass a chunk mask");
+      derived.assign(static_cast<std::size_t>(lr.chunks), 0);
+      std::fill_n(derived.begin(), trainable * eb_ / kChunkBytes, 1);
+      mask = derived.data();
+    }
+    lr.L = build_layout(lr.chunks, mask, eb_, N_, g_);
+    if (lr.L.dev.pt * V_ != trainable)
+      throw shardsim::ConfigError("layer " + std::to_string(l) + ": chunk mask selects " +
+                                  std::to_string(lr.L.dev.pt * V_) + " trainable params, trainable_fraction gives " +
+                                  std::to_string(trainable));
+    const std::size_t wb = lr.L.bits.size() * sizeof(std::uint32_t);
+    CK(cudaMalloc(&lr.d_bits, wb));
+    CK(cudaMalloc(&lr.d_tpre, wb));
+    CK(cudaMemcpy(lr.d_bits, lr.L.bits.data(), wb, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(lr.d_tpre, lr.L.tpre.data(), wb, cudaMemcpyHostToDevice));
+    lr.L.dev.bits = lr.d_bits;
+    lr.L.dev.tpre = lr.d_tpre;
+    lr.has_t = lr.L.dev.pt > 0;
+    lr.has_f = lr.L.dev.pf > 0;
+    lr.off_t = arena_t_;
+    arena_t_ += lr.L.dev.shard_t;
+    lr.off_f = arena_f_;
+    arena_f_ += lr.L.dev.shard_f;
+    lr.host_off = host_chunks_;
+    host_chunks_ += lr.L.dev.slice_t + lr.L.dev.slice_f;
+    lr.my_real_t = lr.L.real_chunks(false, r);
+    lr.my_real_f = lr.L.real_chunks(true, r);
+    lr.slice_real_t = lr.L.real_slice_chunks(false, j_);
+    lr.slice_real_f = lr.L.real_slice_chunks(true, j_);
+    max_chunks_ = std::max(max_chunks_, lr.chunks);
+    max_slice_ = std::max(max_slice_, lr.L.dev.slice_t + lr.L.dev.slice_f);
+    max_shard_t_ = std::max(max_shard_t_, lr.L.dev.shard_t);
+    max_slice_t_ = std::max(max_slice_t_, lr.L.dev.slice_t);
+  }
+  pending_h2d_.assign(static_cast<std::size_t>(L), {});
+  x_of_t_.assign(static_cast<std::size_t>(L), -1);
+  x_of_f_.assign(static_cast<std::size_t>(L), -1);
+  w_of_layer_.assign(static_cast<std::size_t>(L), -1);
+  grad_slot_of_layer_.assign(static_cast<std::size_t>(L), -1);
+  u_of_layer_.assign(static_cast<std::size_t>(L), 0);
+  retained_.assign(static_cast<std::size_t>(L), nullptr);
+  retained_content_.assign(static_cast<std::size_t>(L), {});
+}
+
+void Engine::allocate() {
+  const std::size_t C = kChunkBytes;
+  param_t_ = dalloc<unsigned char>(arena_t_ * C, "trainable shards");
+  param_f_ = dalloc<unsigned char>(arena_f_ * C, "frozen shards");
+  const std::size_t nt = static_cast<std::size_t>(arena_t_) * V_ * sizeof(float);
+  master_ = dalloc<float>(nt, "fp32 master");
+  adam_m_ = dalloc<float>(nt, "adam m");
+  adam_v_ = dalloc<float>(nt, "adam v");
+  grad32_ = dalloc<float>(nt, "fp32 grad shards");
+  for (auto& w : w_slots_) w = dalloc<unsigned char>(max_chunks_ * C, "gathered layer");
+  x_slot_bytes_ = round_up(static_cast<std::size_t>(max_slice_) * C, 4096);
+  grad_slot_bytes_ = round_up(static_cast<std::size_t>(max_chunks_) * C, 4096);
+  arena_bytes_ = x_slot_bytes_ * cfg_.x_slots + 2 * grad_slot_bytes_;
+  peer_arena_ = dalloc<unsigned char>(arena_bytes_, "peer arena");
+  for (int i = 0; i < 2; ++i) {
+    own32_[i] = dalloc<float>(static_cast<std::size_t>(max_shard_t_) * V_ * sizeof(float), "rs own");
+    wire_[i] = dalloc<unsigned char>(max_slice_t_ * C, "rs wire");
+    rx_[i] = dalloc<unsigned char>(static_cast<std::size_t>(N_) * max_shard_t_ * C, "rs rx");
+  }
+  const cudaError_t e = cudaHostAlloc(&host_cache_, std::max<std::size_t>(host_chunks_ * C, 4096),
+                                      cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw OomError("cudaHostAlloc(host cache, " + std::to_string(host_chunks_ * C) + " B) failed");
+  }
+  std::memset(host_cache_, 0, host_chunks_ * C);
+}
+
+void Engine::exchange_handles() {
+  RankBlock& mine = shm_->rank_block(rank_);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, peer_arena_));
+  static_assert(sizeof(h) <= sizeof(mine.ipc_handle), "ipc handle size");
+  std::memcpy(mine.ipc_handle, &h, sizeof(h));
+  mine.arena_bytes = arena_bytes_;
+  mine.device = cfg_.device;
+  shm_->barrier(cfg_.timeout_s);
+  for (int jj = 0; jj < g_; ++jj) {
+    if (jj == j_) {
+      peer_base_[jj] = peer_arena_;
+      continue;
+    }
+    const RankBlock& pb = shm_->rank_block(n_ * g_ + jj);
+    if (pb.arena_bytes != arena_bytes_) throw shardsim::ConfigError("engine: ranks disagree on arena size");
+    cudaIpcMemHandle_t ph;
+    std::memcpy(&ph, pb.ipc_handle, sizeof(ph));
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess));
+    peer_base_[jj] = static_cast<unsigned char*>(p);
+  }
+}
+
+void Engine::init_params(std::uint64_t seed, const fcdp_init_range* const* ranges, const int32_t* num_ranges) {
+  const std::size_t C = kChunkBytes;
+  cudaStream_t s = s_comp_;
+  unsigned char* nat = dalloc<unsigned char>(max_chunks_ * C, "init natural");
+  std::int64_t max_t = 0, max_f = 0;
+  for (const LayerRt& l : layers_) {
+    max_t = std::max(max_t, l.L.dev.shard_t * G_);
+    max_f = std::max(max_f, l.L.dev.shard_f * G_);
+  }
+  unsigned char* tv = dalloc<unsigned char>(max_t * C, "init t");
+  unsigned char* fv = dalloc<unsigned char>(max_f * C, "init f");
+  InitRange* d_ranges = nullptr;
+  int max_r = 1;
+  for (std::size_t l = 0; l < layers_.size(); ++l) max_r = std::max(max_r, num_ranges ? num_ranges[l] : 0);
+  d_ranges = dalloc<InitRange>(sizeof(InitRange) * max_r, "init ranges");
+  const int r = j_ * N_ + n_;
+  try {
+    for (std::size_t li = 0; li < layers_.size(); ++li) {
+      LayerRt& l = layers_[li];
+      const int nr = num_ranges ? num_ranges[li] : 0;
+      if (nr > 0) CK(cudaMemcpy(d_ranges, ranges[li], sizeof(InitRange) * nr, cudaMemcpyHostToDevice));
+      CK(launch_init_natural(l.elems, eb_, seed, static_cast<int>(li), d_ranges, nr, nat, s));
+      CK(cudaMemsetAsync(tv, 0, l.L.dev.shard_t * G_ * C, s));
+      CK(cudaMemsetAsync(fv, 0, l.L.dev.shard_f * G_ * C, s));
+      CK(launch_partition(l.L, nat, tv, fv, s));
+      if (l.has_t)
+        CK(cudaMemcpyAsync(param_t_ + l.off_t * C, tv + r * l.L.dev.shard_t * C, l.L.dev.shard_t * C,
+                           cudaMemcpyDeviceToDevice, s));
+      if (l.has_f)
+        CK(cudaMemcpyAsync(param_f_ + l.off_f * C, fv + r * l.L.dev.shard_f * C, l.L.dev.shard_f * C,
+                           cudaMemcpyDeviceToDevice, s));
+      l.shard_version_t = 0;
+      l.host_version_t = l.host_version_f = -1;
+      CK(cudaStreamSynchronize(s));
+    }
+    CK(launch_widen(arena_t_ * V_, param_t_, eb_, master_, s));
+    CK(cudaMemsetAsync(adam_m_, 0, arena_t_ * V_ * sizeof(float), s));
+    CK(cudaMemsetAsync(adam_v_, 0, arena_t_ * V_ * sizeof(float), s));
+    CK(cudaMemsetAsync(grad32_, 0, arena_t_ * V_ * sizeof(float), s));
+    CK(cudaStreamSynchronize(s));
+  } catch (...) {
+    cudaFree(nat);
+    cudaFree(tv);
+    cudaFree(fv);
+    cudaFree(d_ranges);
+    throw;
+  }
+  cudaFree(nat);
+  cudaFree(tv);
+  cudaFree(fv);
+  cudaFree(d_ranges);
+  opt_steps_ = 0;
+}
+
+// ----------------------------------------------------------------- helpers
+
+unsigned char* Engine::x_slot(int jj, int slot) const { return peer_base_[jj] + slot * x_slot_bytes_; }
+
+unsigned char* Engine::grad_slot(int jj, int slot) const {
+  return peer_base_[jj] + cfg_.x_slots * x_slot_bytes_ + slot * grad_slot_bytes_;
+}
+
+void Engine::wait_flag(cudaStream_t s, int rank, Flag f, std::uint32_t v) {
+  const auto off = reinterpret_cast<const volatile unsigned char*>(shm_->flag(rank, f)) -
+                   static_cast<const volatile unsigned char*>(shm_->base());
+  StreamOps::wait_geq(s, reinterpret_cast<const volatile std::uint32_t*>(
+                             static_cast<const unsigned char*>(shm_dev_base_) + off), v);
+}
+
+void Engine::write_flag(cudaStream_t s, Flag f, std::uint32_t v) {
+  const auto off = reinterpret_cast<unsigned char*>(const_cast<std::uint32_t*>(shm_->flag(rank_, f))) -
+                   static_cast<unsigned char*>(shm_->base());
+  StreamOps::write(s, reinterpret_cast<volatile std::uint32_t*>(static_cast<unsigned char*>(shm_dev_base_) + off), v);
+}
+
+cudaStream_t Engine::stream_for(EventKind k) const {
+  switch (k) {
+    case EventKind::AgInter:
+    case EventKind::AgIntra:
+    case EventKind::H2D:
+      return s_gather_;
+    case EventKind::D2H:
+      return s_cache_;
+    case EventKind::ReduceScatter:
+      return s_rs_;
+    default:
+      return s_comp_;
+  }
+}
+
+unsigned char* Engine::w_buffer(int layer) {
+  if (w_of_layer_[layer] < 0) {
+    if (prog_->layer_retained[layer]) {
+      if (!retained_[layer]) retained_[layer] = dalloc<unsigned char>(layers_[layer].chunks * kChunkBytes, "retained layer");
+      w_of_layer_[layer] = 2;  // marker: retained buffer
+    } else {
+      w_of_layer_[layer] = static_cast<int>(w_instances_++ % 2);
+    }
+  }
+  return w_of_layer_[layer] == 2 ? retained_[layer] : w_slots_[w_of_layer_[layer]];
+}
+
+int Engine::begin_slice_fill(int /*layer*/) {
+  const std::uint32_t q = ++q_;
+  const int slot = static_cast<int>(q % static_cast<std::uint32_t>(cfg_.x_slots));
+  if (q > static_cast<std::uint32_t>(cfg_.x_slots))
+    for (int jj = 0; jj < g_; ++jj)
+      if (jj != j_) wait_flag(s_gather_, n_ * g_ + jj, kSliceFree, q - cfg_.x_slots);
+  CK(cudaStreamWaitEvent(s_gather_, x_reader_[slot], 0));
+  return slot;
+}
+
+void Engine::finish_slice_fill(int /*slot*/, std::uint32_t q) { write_flag(s_gather_, kSliceReady, q); }
+
+void Engine::pull_expand(int layer, int slot, std::uint32_t q, bool want_t, bool want_f, cudaStream_t s) {
+  LayerRt& l = layers_[layer];
+  for (int jj = 0; jj < g_; ++jj)
+    if (jj != j_) wait_flag(s, n_ * g_ + jj, kSliceReady, q);
+  unsigned char* W = w_buffer(layer);
+  SlicePtrs ts{}, fs{};
+  for (int jj = 0; jj < g_; ++jj) {
+    ts.p[jj] = x_slot(jj, slot);
+    fs.p[jj] = x_slot(jj, slot) + l.L.dev.slice_t * kChunkBytes;
+  }
+  const int set = want_t && want_f ? kSetAll : (want_t ? kSetTrainable : kSetFrozen);
+  const bool dense = l.L.dense_trainable() || l.L.dense_frozen();
+  if (use_ce_ && dense) {
+    const bool tr = l.L.dense_trainable();
+    const std::int64_t per = tr ? l.L.dev.slice_t : l.L.dev.slice_f;
+    for (int jj = 0; jj < g_; ++jj) {
+      const std::int64_t lo = jj * per;
+      if (lo >= l.chunks) break;
+      const std::int64_t n = std::min(per, l.chunks - lo);
+      CK(cudaMemcpyAsync(W + lo * kChunkBytes, tr ? ts.p[jj] : fs.p[jj], n * kChunkBytes,
+                         cudaMemcpyDeviceToDevice, s));
+    }
+  } else {
+    CK(launch_expand(l.L, ts, fs, W, set, s));
+  }
+  write_flag(s, kSliceFree, q);
+  std::uint64_t rx = 0;
+  for (int jj = 0; jj < g_; ++jj) {
+    if (jj == j_) continue;
+    if (want_t) rx += l.L.real_slice_chunks(false, jj) * kChunkBytes;
+    if (want_f) rx += l.L.real_slice_chunks(true, jj) * kChunkBytes;
+  }
+  shm_->add(rank_, kNvlinkRx, rx);
+}
+
+void Engine::inter_send(int cls, cudaStream_t s, std::uint32_t seq,
+                        const std::vector<std::pair<const void*, std::size_t>>& parts, std::uint64_t wire_bytes,
+                        Counter counter) {
+  const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
+  unsigned char* dst = shm_->slot(rank_, cls, idx);
+  std::size_t off = 0, staged = 0;
+  for (const auto& [src, bytes] : parts) {
+    if (bytes) CK(cudaMemcpyAsync(dst + off, src, bytes, cudaMemcpyDeviceToHost, s));
+    off += bytes;
+    staged += bytes;
+  }
+  shm_->add(rank_, kStagingD2H, staged);
+  cudaEvent_t ev = staged_[staged_next_++ % staged_.size()];
+  CK(cudaEventRecord(ev, s));
+  nic_->submit({cls, seq, ev, wire_bytes, counter});
+}
+
+// ------------------------------------------------------------------ events
+
+void Engine::ev_ag_inter(const Event& e, bool backward) {
+  LayerRt& l = layers_[e.layer];
+  const bool wt = wants_t(e.param_set) && l.has_t, wf = wants_f(e.param_set) && l.has_f;
+  cudaStream_t s = s_gather_;
+  const std::size_t C = kChunkBytes;
+  const int slot = begin_slice_fill(e.layer);
+  const std::uint32_t q = q_;
+  unsigned char* X = x_slot(j_, slot);
+  unsigned char* Xf = X + l.L.dev.slice_t * C;
+  // own shard -> its position n in this GPU's slice (global shard j*N + n)
+  if (wt && l.my_real_t)
+    CK(cudaMemcpyAsync(X + n_ * l.L.dev.shard_t * C, param_t_ + l.off_t * C, l.my_real_t * C,
+                       cudaMemcpyDeviceToDevice, s));
+  if (wf && l.my_real_f)
+    CK(cudaMemcpyAsync(Xf + n_ * l.L.dev.shard_f * C, param_f_ + l.off_f * C, l.my_real_f * C,
+                       cudaMemcpyDeviceToDevice, s));
+  if (N_ > 1) {
+    // Inter-node all-gather among {(n', j)} through the host-staged NIC path.
+    const std::uint32_t seq = ++seq_ag_;
+    const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
+    if (seq > static_cast<std::uint32_t>(cfg_.inter_slots))
+      for (int nn = 0; nn < N_; ++nn)
+        if (nn != n_) wait_flag(s, nn * g_ + j_, kAgRxDone, seq - cfg_.inter_slots);
+    std::vector<std::pair<const void*, std::size_t>> parts;
+    std::uint64_t payload = 0;
+    if (wt) parts.push_back({param_t_ + l.off_t * C, l.my_real_t * C}), payload += l.my_real_t * C;
+    if (wf) parts.push_back({param_f_ + l.off_f * C, l.my_real_f * C}), payload += l.my_real_f * C;
+    inter_send(0, s, seq, parts, payload * static_cast<std::uint64_t>(N_ - 1), backward ? kTxBwdAg : kTxFwdAg);
+    std::uint64_t rx = 0;
+    for (int nn = 0; nn < N_; ++nn) {
+      if (nn == n_) continue;
+      const int src_rank = nn * g_ + j_;
+      const int r = j_ * N_ + nn;
+      wait_flag(s, src_rank, kAgTxReady, seq);
+      const unsigned char* src = shm_->slot(src_rank, 0, idx);
+      const std::int64_t rt = wt ? l.L.real_chunks(false, r) : 0, rf = wf ? l.L.real_chunks(true, r) : 0;
+      if (rt) CK(cudaMemcpyAsync(X + nn * l.L.dev.shard_t * C, src, rt * C, cudaMemcpyHostToDevice, s));
+      if (rf) CK(cudaMemcpyAsync(Xf + nn * l.L.dev.shard_f * C, src + rt * C, rf * C, cudaMemcpyHostToDevice, s));
+      rx += (rt + rf) * C;
+    }
+    write_flag(s, kAgRxDone, seq);
+    shm_->add(rank_, kStagingH2D, rx);
+    shm_->add(rank_, backward ? kRxBwdAg : kRxFwdAg, rx);
+  }
+  finish_slice_fill(slot, q);
+  // Intra-node all-gather over NVLink, fused with the PEFT expansion.
+  pull_expand(e.layer, slot, q, wt, wf, s);
+  WContent& wc = w_of_layer_[e.layer] == 2 ? retained_content_[e.layer] : w_content_[w_of_layer_[e.layer]];
+  if (wc.layer != e.layer) wc = WContent{e.layer, -1, -1};
+  if (wt) wc.ver_t = static_cast<std::int64_t>(l.shard_version_t), x_of_t_[e.layer] = slot;
+  if (wf) wc.ver_f = 0, x_of_f_[e.layer] = slot;
+  shm_->add(rank_, backward ? kAgEventsBwd : kAgEventsFwd, 1);
+}
+
+void Engine::ev_h2d(const Event& e) {
+  LayerRt& l = layers_[e.layer];
+  const bool wt = wants_t(e.param_set) && l.has_t, wf = wants_f(e.param_set) && l.has_f;
+  // Freshness (Algorithm 1 line 10): only a clean host copy may be reloaded.
+  if (wt && l.host_version_t != static_cast<std::int64_t>(l.shard_version_t))
+    throw shardsim::ProtocolError("freshness: layer " + std::to_string(e.layer) +
+                                  " trainable portion reloaded from a stale host cache");
+  if (wf && l.host_version_f != 0)
+    throw shardsim::ProtocolError("freshness: layer " + std::to_string(e.layer) +
+                                  " frozen portion reloaded before it was cached");
+  const std::size_t C = kChunkBytes;
+  const int slot = begin_slice_fill(e.layer);
+  const std::uint32_t q = q_;
+  unsigned char* X = x_slot(j_, slot);
+  const unsigned char* H = host_cache_ + l.host_off * C;
+  std::uint64_t bytes = 0;
+  if (wt && l.slice_real_t) {
+    CK(cudaMemcpyAsync(X, H, l.slice_real_t * C, cudaMemcpyHostToDevice, s_gather_));
+    bytes += l.slice_real_t * C;
+  }
+  if (wf && l.slice_real_f) {
+    CK(cudaMemcpyAsync(X + l.L.dev.slice_t * C, H + l.L.dev.slice_t * C, l.slice_real_f * C,
+                       cudaMemcpyHostToDevice, s_gather_));
+    bytes += l.slice_real_f * C;
+  }
+  shm_->add(rank_, kCacheH2D, bytes);
+  finish_slice_fill(slot, q);
+  PendingSlice& p = pending_h2d_[e.layer];
+  p.slot = slot;
+  p.q = q;
+  p.t = wt;
+  p.f = wf;
+  p.ver_t = wt ? l.host_version_t : -1;
+  p.ver_f = wf ? 0 : -1;
+}
+
+void Engine::ev_ag_intra(const Event& e) {
+  PendingSlice p = pending_h2d_[e.layer];
+  if (p.slot < 0) throw shardsim::ProtocolError("ag_intra without a preceding h2d for layer " + std::to_string(e.layer));
+  pull_expand(e.layer, p.slot, p.q, p.t, p.f, s_gather_);
+  WContent& wc = w_of_layer_[e.layer] == 2 ? retained_content_[e.layer] : w_content_[w_of_layer_[e.layer]];
+  if (wc.layer != e.layer) wc = WContent{e.layer, -1, -1};
+  if (p.t) wc.ver_t = p.ver_t;
+  if (p.f) wc.ver_f = p.ver_f;
+  pending_h2d_[e.layer] = {};
+}
+
+void Engine::ev_d2h(const Event& e) {
+  LayerRt& l = layers_[e.layer];
+  const bool wt = wants_t(e.param_set) && l.has_t, wf = wants_f(e.param_set) && l.has_f;
+  const std::size_t C = kChunkBytes;
+  unsigned char* H = host_cache_ + l.host_off * C;
+  std::uint64_t bytes = 0;
+  int slot_t = -1, slot_f = -1;
+  if (wt) {
+    slot_t = x_of_t_[e.layer];
+    if (slot_t < 0) throw shardsim::ProtocolError("d2h of a trainable portion that was not gathered");
+    if (l.slice_real_t)
+      CK(cudaMemcpyAsync(H, x_slot(j_, slot_t), l.slice_real_t * C, cudaMemcpyDeviceToHost, s_cache_));
+    bytes += l.slice_real_t * C;
+    l.host_version_t = static_cast<std::int64_t>(l.shard_version_t);
+  }
+  if (wf) {
+    slot_f = x_of_f_[e.layer];
+    if (slot_f < 0) throw shardsim::ProtocolError("d2h of a frozen portion that was not gathered");
+    if (l.slice_real_f)
+      CK(cudaMemcpyAsync(H + l.L.dev.slice_t * C, x_slot(j_, slot_f) + l.L.dev.slice_t * C, l.slice_real_f * C,
+                         cudaMemcpyDeviceToHost, s_cache_));
+    bytes += l.slice_real_f * C;
+    l.host_version_f = 0;
+  }
+  for (int sl : {slot_t, slot_f})
+    if (sl >= 0) CK(cudaEventRecord(x_reader_[sl], s_cache_));
+  shm_->add(rank_, kCacheD2H, bytes);
+}
+
+void Engine::ev_compute(const Event& e, bool backward) {
+  const int li = e.layer;
+  LayerRt& l = layers_[li];
+  if (w_of_layer_[li] < 0) throw shardsim::ProtocolError("freshness: layer " + std::to_string(li) + " computed without a gather");
+  const WContent& wc = w_of_layer_[li] == 2 ? retained_content_[li] : w_content_[w_of_layer_[li]];
+  if (wc.layer != li || (l.has_t && wc.ver_t != static_cast<std::int64_t>(l.shard_version_t)) ||
+      (l.has_f && wc.ver_f != 0))
+    throw shardsim::ProtocolError("freshness: layer " + std::to_string(li) +
+                                  " would compute on parameters that are not at their current version");
+  unsigned char* W = w_of_layer_[li] == 2 ? retained_[li] : w_slots_[w_of_layer_[li]];
+  void* grad = nullptr;
+  if (backward && l.has_t) {
+    const std::uint32_t u = ++u_;
+    const int gs = static_cast<int>(u % 2);
+    u_of_layer_[li] = u;
+    grad_slot_of_layer_[li] = gs;
+    if (u > 2) {
+      for (int jj = 0; jj < g_; ++jj)
+        if (jj != j_) wait_flag(s_comp_, n_ * g_ + jj, kGradFree, u - 2);
+      CK(cudaStreamWaitEvent(s_comp_, rs_done_[gs], 0));
+    }
+    grad = grad_slot(j_, gs);
+  }
+  if (compute_fn_) {
+    const int rc = compute_fn_(compute_user_, backward ? FCDP_EV_COMPUTE_BWD : FCDP_EV_COMPUTE_FWD, li, W, grad,
+                               s_comp_);
+    if (rc != 0) throw std::runtime_error("compute callback failed for layer " + std::to_string(li));
+  } else if (grad) {
+    CK(cudaMemsetAsync(grad, 0, l.chunks * kChunkBytes, s_comp_));  // data-plane-only mode
+  }
+  if (!backward && w_of_layer_[li] != 2) w_of_layer_[li] = -1;  // the slot is free for the backward re-gather
+}
+
+void Engine::ev_reduce_scatter(const Event& e) {
+  const int li = e.layer;
+  LayerRt& l = layers_[li];
+  if (!l.has_t) return;
+  const std::uint32_t u = u_of_layer_[li];
+  const int gs = grad_slot_of_layer_[li];
+  if (gs < 0) throw shardsim::ProtocolError("reduce_scatter before compute_bwd of layer " + std::to_string(li));
+  cudaStream_t s = s_rs_;
+  const std::size_t C = kChunkBytes;
+  write_flag(s, kGradReady, u);
+  for (int jj = 0; jj < g_; ++jj)
+    if (jj != j_) wait_flag(s, n_ * g_ + jj, kGradReady, u);
+  GradPtrs gp{};
+  for (int jj = 0; jj < g_; ++jj) gp.p[jj] = grad_slot(jj, gs);
+  const float scale = 1.0f / static_cast<float>(G_);
+  float* final_out = grad32_ + l.off_t * V_;
+  if (N_ == 1) {
+    CK(launch_rs_slice(l.L, gp, j_, 0, scale, true, final_out, wire_[gs], s));
+  } else {
+    CK(launch_rs_slice(l.L, gp, j_, n_, scale, false, own32_[gs], wire_[gs], s));
+  }
+  write_flag(s, kGradFree, u);
+  CK(cudaEventRecord(rs_done_[gs], s));
+  shm_->add(rank_, kNvlinkRx, static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
+  grad_slot_of_layer_[li] = -1;
+  if (N_ == 1) return;
+
+  // Inter-node reduce-scatter among {(n', j)}: partial sums of the other
+  // nodes' shards cross the NIC in the parameter dtype (costmodel.cpp:86-88).
+  const std::uint32_t seq = ++seq_rs_;
+  const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
+  if (seq > static_cast<std::uint32_t>(cfg_.inter_slots))
+    for (int nn = 0; nn < N_; ++nn)
+      if (nn != n_) wait_flag(s, nn * g_ + j_, kRsRxDone, seq - cfg_.inter_slots);
+  // stage the slice with the own-shard hole: slot layout == slice layout
+  unsigned char* dst = shm_->slot(rank_, 1, idx);
+  std::uint64_t wire = 0;
+  for (int nn = 0; nn < N_; ++nn) {
+    if (nn == n_) continue;
+    const std::int64_t real = l.L.real_chunks(false, j_ * N_ + nn);
+    if (!real) continue;
+    const std::size_t off = nn * l.L.dev.shard_t * C;
+    CK(cudaMemcpyAsync(dst + off, wire_[gs] + off, real * C, cudaMemcpyDeviceToHost, s));
+    wire += real * C;
+  }
+  shm_->add(rank_, kStagingD2H, wire);
+  cudaEvent_t ev = staged_[staged_next_++ % staged_.size()];
+  CK(cudaEventRecord(ev, s));
+  nic_->submit({1, seq, ev, wire, kTxRs});
+  std::uint64_t rx = 0;
+  for (int nn = 0; nn < N_; ++nn) {
+    if (nn == n_) continue;
+    const int src_rank = nn * g_ + j_;
+    wait_flag(s, src_rank, kRsTxReady, seq);
+    if (l.my_real_t) {
+      CK(cudaMemcpyAsync(rx_[gs] + nn * l.L.dev.shard_t * C, shm_->slot(src_rank, 1, idx) + n_ * l.L.dev.shard_t * C,
+                         l.my_real_t * C, cudaMemcpyHostToDevice, s));
+      rx += l.my_real_t * C;
+    }
+  }
+  write_flag(s, kRsRxDone, seq);
+  shm_->add(rank_, kStagingH2D, rx);
+  shm_->add(rank_, kRxRs, rx);
+  CK(launch_rs_finalize(l.L.dev.shard_t * V_, N_, n_, eb_, own32_[gs], rx_[gs], l.L.dev.shard_t * V_, scale,
+                        final_out, s));
+}
+
+void Engine::ev_optimizer(const Event&) {
+  ++opt_steps_;
+  AdamParams p{adam_.lr, adam_.beta1, adam_.beta2, adam_.eps, adam_.weight_decay,
+               static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta1), opt_steps_)),
+               static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta2), opt_steps_))};
+  CK(launch_adam(arena_t_ * V_, p, master_, adam_m_, adam_v_, grad32_, param_t_, eb_, s_comp_));
+  for (LayerRt& l : layers_)
+    if (l.has_t) ++l.shard_version_t;
+}
+
+// --------------------------------------------------------------------- run
+
+void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::ParamState>& states) {
+  if (prog.strategy != plan_.kind) throw shardsim::ConfigError("engine: program strategy differs from the engine plan");
+  if (prog.layer_retained.size() != layers_.size()) throw shardsim::ConfigError("engine: program is for another model");
+  CK(cudaSetDevice(cfg_.device));
+  prog_ = &prog;
+  const std::size_t n_ev = prog.events.size();
+  while (ev_done_.size() < n_ev) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ev_done_.push_back(e);
+  }
+  std::vector<cudaStream_t> stream_of(n_ev);
+  std::uint32_t last_fwd = 0;
+  for (const Event& e : prog.events) {
+    stream_of[e.id] = stream_for(e.kind);
+    if (e.kind == EventKind::ComputeFwd) last_fwd = e.id;
+  }
+  for (cudaStream_t s : {s_gather_, s_cache_, s_rs_}) CK(cudaStreamWaitEvent(s, iter_done_, 0));
+  std::fill(x_of_t_.begin(), x_of_t_.end(), -1);
+  std::fill(x_of_f_.begin(), x_of_f_.end(), -1);
+  std::fill(w_of_layer_.begin(), w_of_layer_.end(), -1);
+
+  for (const Event& e : prog.events) {
+    cudaStream_t s = stream_of[e.id];
+    for (shardsim::EventId d : e.deps)
+      if (stream_of[d] != s) CK(cudaStreamWaitEvent(s, ev_done_[d], 0));
+    const bool bwd = e.id > last_fwd;
+    switch (e.kind) {
+      case EventKind::AgInter: ev_ag_inter(e, bwd); break;
+      case EventKind::H2D: ev_h2d(e); break;
+      case EventKind::AgIntra: ev_ag_intra(e); break;
+      case EventKind::D2H: ev_d2h(e); break;
+      case EventKind::ComputeFwd: ev_compute(e, false); break;
+      case EventKind::ComputeBwd: ev_compute(e, true); break;
+      case EventKind::ReduceScatter: ev_reduce_scatter(e); break;
+      case EventKind::OptimizerStep: ev_optimizer(e); break;
+      case EventKind::MaskDirty: break;  // bookkeeping only (step_state)
+      case EventKind::Broadcast:
+        throw shardsim::ConfigError("engine: broadcast events (zero2) are not part of this data plane");
+    }
+    CK(cudaEventRecord(ev_done_[e.id], s));
+  }
+  // join: the next iteration starts after everything of this one
+  const cudaStream_t side[3] = {s_gather_, s_cache_, s_rs_};
+  for (int i = 0; i < 3; ++i) {
+    CK(cudaEventRecord(join_[i], side[i]));
+    CK(cudaStreamWaitEvent(s_comp_, join_[i], 0));
+  }
+  CK(cudaEventRecord(iter_done_, s_comp_));
+  for (std::size_t li = 0; li < layers_.size(); ++li)
+    if (!prog.layer_retained[li] && retained_[li]) {
+      // retention is per iteration; the buffer stays allocated for reuse
+      retained_content_[li] = {};
+    }
+  states = shardsim::step_state(std::move(states), prog);
+  prog_ = nullptr;
+}
+
+void Engine::sync() {
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_})
+    if (s) CK(cudaStreamSynchronize(s));
+}
+
+void Engine::barrier() { shm_->barrier(cfg_.timeout_s); }
+
+void Engine::counters(int rank, fcdp_counters* o) const {
+  if (rank < 0 || rank >= G_) throw shardsim::ConfigError("counters: rank out of range");
+  o->nic_tx_fwd_ag = shm_->counter(rank, kTxFwdAg);
+  o->nic_tx_bwd_ag = shm_->counter(rank, kTxBwdAg);
+  o->nic_tx_rs = shm_->counter(rank, kTxRs);
+  o->nic_rx_fwd_ag = shm_->counter(rank, kRxFwdAg);
+  o->nic_rx_bwd_ag = shm_->counter(rank, kRxBwdAg);
+  o->nic_rx_rs = shm_->counter(rank, kRxRs);
+  o->nvlink_rx = shm_->counter(rank, kNvlinkRx);
+  o->cache_h2d = shm_->counter(rank, kCacheH2D);
+  o->cache_d2h = shm_->counter(rank, kCacheD2H);
+  o->staging_h2d = shm_->counter(rank, kStagingH2D);
+  o->staging_d2h = shm_->counter(rank, kStagingD2H);
+  o->ag_inter_events_fwd = shm_->counter(rank, kAgEventsFwd);
+  o->ag_inter_events_bwd = shm_->counter(rank, kAgEventsBwd);
+  o->nic_busy_ns = shm_->counter(rank, kNicBusyNs);
+}
+
+void Engine::reset_counters() { shm_->reset_counters(rank_); }
+
+void Engine::read_shard(int layer, bool frozen, void* host, std::size_t bytes) {
+  const LayerRt& l = layers_.at(layer);
+  const std::size_t have = (frozen ? l.L.dev.shard_f : l.L.dev.shard_t) * kChunkBytes;
+  sync();
+  CK(cudaMemcpy(host, (frozen ? param_f_ + l.off_f * kChunkBytes : param_t_ + l.off_t * kChunkBytes),
+                std::min(bytes, have), cudaMemcpyDeviceToHost));
+}
+
+void Engine::read_master(int layer, float* host, std::size_t count) {
+  const LayerRt& l = layers_.at(layer);
+  sync();
+  CK(cudaMemcpy(host, master_ + l.off_t * V_, std::min<std::size_t>(count, l.L.dev.shard_t * V_) * sizeof(float),
+                cudaMemcpyDeviceToHost));
+}
+
+void Engine::read_grad(int layer, float* host, std::size_t count) {
+  const LayerRt& l = layers_.at(layer);
+  sync();
+  CK(cudaMemcpy(host, grad32_ + l.off_t * V_, std::min<std::size_t>(count, l.L.dev.shard_t * V_) * sizeof(float),
+                cudaMemcpyDeviceToHost));
+}
+
+void Engine::read_host_cache(int layer, bool frozen, void* host, std::size_t bytes) {
+  const LayerRt& l = layers_.at(layer);
+  sync();
+  const unsigned char* H = host_cache_ + l.host_off * kChunkBytes + (frozen ? l.L.dev.slice_t * kChunkBytes : 0);
+  const std::size_t have = (frozen ? l.slice_real_f : l.slice_real_t) * kChunkBytes;
+  std::memcpy(host, H, std::min(bytes, have));
+}
+
+}  // namespace fcdp

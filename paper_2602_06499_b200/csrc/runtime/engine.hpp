@@ -1,0 +1,175 @@
+// Per-rank FCDP engine: shard store + executor of shardsim event programs.
+//
+// One process per GPU.  The engine owns
+//   * the shard store: this GPU's trainable / frozen parameter shards (param
+//     dtype), fp32 master / Adam moments / gradient shards for the trainable
+//     portion, and the pinned host-cache tier holding this GPU's intra slice
+//     of every layer (FCDP-Cache);
+//   * peer-visible HBM (slice slots, natural gradient slots) that the other
+//     GPUs of its emulated node read over NVLink;
+//   * the executor that walks an EventProgram (reference schedule.hpp:53-61)
+//     in id order and maps each event onto streams:
+//        AgInter        -> host-staged NIC emulator + NVLink gather/expand
+//        H2D / AgIntra  -> PCIe reload from the host cache + NVLink gather
+//        D2H            -> FCDP-Cache store on a side stream
+//        ComputeFwd/Bwd -> the user's compute callback on the compute stream
+//        ReduceScatter  -> NVLink pull-reduce (fp32) + NIC hop + cast/scale
+//        OptimizerStep  -> AdamW over the fp32 trainable arena
+//     Event deps become cudaStreamWaitEvent edges; cross-rank edges are
+//     stream waits on flags in the shared control block.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "common/layout.hpp"
+#include "fcdp.h"
+#include "kernels/kernels.hpp"
+#include "runtime/nic.hpp"
+#include "runtime/shm.hpp"
+#include "shardsim/schedule.hpp"
+
+namespace fcdp {
+
+struct LayerRt {
+  Layout L;
+  std::uint32_t* d_bits = nullptr;
+  std::uint32_t* d_tpre = nullptr;
+  std::int64_t elems = 0, chunks = 0;
+  bool has_t = false, has_f = false;
+  std::int64_t off_t = 0, off_f = 0;          // this rank's shards in the param arenas (chunks)
+  std::int64_t host_off = 0;                  // this rank's slice in the host cache (chunks)
+  std::int64_t my_real_t = 0, my_real_f = 0;  // real chunks of this rank's shards
+  std::int64_t slice_real_t = 0, slice_real_f = 0;
+  std::uint64_t shard_version_t = 0;          // version of this rank's trainable shard
+  std::int64_t host_version_t = -1, host_version_f = -1;  // versions in the host cache (-1 none)
+  std::int8_t retained_slot = -1;
+};
+
+struct WContent {
+  int layer = -1;
+  std::int64_t ver_t = -1, ver_f = -1;  // -1: portion not present
+};
+
+class Engine {
+ public:
+  Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
+         const shardsim::ClusterTopology& topo, const shardsim::StrategyPlan& plan,
+         const std::uint8_t* const* chunk_masks);
+  ~Engine();
+
+  void init_params(std::uint64_t seed, const fcdp_init_range* const* ranges, const int32_t* num_ranges);
+  void set_adam(const fcdp_adam_config& c) { adam_ = c; }
+  void set_compute(fcdp_compute_fn fn, void* user) {
+    compute_fn_ = fn;
+    compute_user_ = user;
+  }
+  void run(const shardsim::EventProgram& prog, std::vector<shardsim::ParamState>& states);
+  void sync();
+  void barrier();
+  cudaStream_t compute_stream() const { return s_comp_; }
+  void counters(int rank, fcdp_counters* out) const;
+  void reset_counters();
+
+  void read_shard(int layer, bool frozen, void* host, std::size_t bytes);
+  void read_master(int layer, float* host, std::size_t count);
+  void read_grad(int layer, float* host, std::size_t count);
+  void read_host_cache(int layer, bool frozen, void* host, std::size_t bytes);
+
+ private:
+  // ---- setup
+  void build_layouts(const std::uint8_t* const* masks);
+  void allocate();
+  void exchange_handles();
+  // ---- events
+  void ev_ag_inter(const shardsim::Event& e, bool backward);
+  void ev_h2d(const shardsim::Event& e);
+  void ev_ag_intra(const shardsim::Event& e);
+  void ev_d2h(const shardsim::Event& e);
+  void ev_compute(const shardsim::Event& e, bool backward);
+  void ev_reduce_scatter(const shardsim::Event& e);
+  void ev_optimizer(const shardsim::Event& e);
+  // ---- helpers
+  cudaStream_t stream_for(shardsim::EventKind k) const;
+  int begin_slice_fill(int layer);                       // returns X slot, waits WAR
+  void finish_slice_fill(int slot, std::uint32_t q);
+  void pull_expand(int layer, int slot, std::uint32_t q, bool want_t, bool want_f, cudaStream_t s);
+  unsigned char* w_buffer(int layer);                    // W slot / retained buffer for layer
+  unsigned char* x_slot(int rank_local, int slot) const; // local or peer pointer
+  unsigned char* grad_slot(int rank_local, int slot) const;
+  void wait_flag(cudaStream_t s, int rank, Flag f, std::uint32_t v);
+  void write_flag(cudaStream_t s, Flag f, std::uint32_t v);
+  void inter_send(int cls, cudaStream_t s, std::uint32_t seq, const std::vector<std::pair<const void*, std::size_t>>& parts,
+                  std::uint64_t wire_bytes, Counter counter);
+  bool is_peer_rank(int r) const { return r / g_ == n_; }
+
+  fcdp_engine_config cfg_;
+  std::string shm_name_;
+  shardsim::ModelSpec model_;
+  shardsim::ClusterTopology topo_;
+  shardsim::StrategyPlan plan_;
+  int N_, g_, G_, n_, j_, rank_, eb_, V_;
+  std::vector<LayerRt> layers_;
+  std::int64_t max_chunks_ = 0, max_slice_ = 0, max_shard_t_ = 0, max_slice_t_ = 0;
+  std::int64_t arena_t_ = 0, arena_f_ = 0, host_chunks_ = 0;
+
+  std::unique_ptr<SharedBlock> shm_;
+  void* shm_dev_base_ = nullptr;
+  std::unique_ptr<NicEmulator> nic_;
+
+  // device memory
+  unsigned char* param_t_ = nullptr;
+  unsigned char* param_f_ = nullptr;
+  float *master_ = nullptr, *adam_m_ = nullptr, *adam_v_ = nullptr, *grad32_ = nullptr;
+  unsigned char* w_slots_[2] = {nullptr, nullptr};
+  std::vector<unsigned char*> retained_;
+  unsigned char* peer_arena_ = nullptr;  // [X slots | grad slots]
+  std::size_t x_slot_bytes_ = 0, grad_slot_bytes_ = 0, arena_bytes_ = 0;
+  unsigned char* peer_base_[kMaxLocal] = {};  // local index -> arena base (own = peer_arena_)
+  float* own32_[2] = {nullptr, nullptr};
+  unsigned char* wire_[2] = {nullptr, nullptr};
+  unsigned char* rx_[2] = {nullptr, nullptr};
+  unsigned char* host_cache_ = nullptr;
+
+  cudaStream_t s_comp_ = nullptr, s_gather_ = nullptr, s_cache_ = nullptr, s_rs_ = nullptr;
+  std::vector<cudaEvent_t> ev_done_;
+  std::vector<cudaEvent_t> x_reader_;  // last local reader of each X slot
+  cudaEvent_t rs_done_[2] = {nullptr, nullptr};
+  cudaEvent_t iter_done_ = nullptr;
+  cudaEvent_t join_[3] = {nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> staged_;    // staging D2H events for the NIC (ring)
+  std::size_t staged_next_ = 0;
+
+  // sequence counters (identical on every rank)
+  std::uint32_t q_ = 0, seq_ag_ = 0, seq_rs_ = 0, u_ = 0;
+  std::uint64_t w_instances_ = 0;
+  std::uint32_t grad_slot_seq_ = 0;
+  int opt_steps_ = 0;
+
+  // per-iteration bookkeeping
+  struct PendingSlice {
+    int slot = -1;
+    std::uint32_t q = 0;
+    bool t = false, f = false;
+    std::int64_t ver_t = -1, ver_f = -1;
+  };
+  std::vector<PendingSlice> pending_h2d_;             // per layer (H2D -> AgIntra)
+  std::vector<int> x_of_t_, x_of_f_;                  // per layer: X slot holding fresh gather
+  std::vector<int> w_of_layer_;                       // per layer: W slot index or -1
+  WContent w_content_[2];
+  std::vector<WContent> retained_content_;
+  std::vector<int> grad_slot_of_layer_;
+  std::vector<std::uint32_t> u_of_layer_;
+  const shardsim::EventProgram* prog_ = nullptr;
+
+  fcdp_adam_config adam_{1e-4f, 0.9f, 0.95f, 1e-8f, 0.0f, 0};
+  fcdp_compute_fn compute_fn_ = nullptr;
+  void* compute_user_ = nullptr;
+  bool use_ce_ = false;
+};
+
+}  // namespace fcdp

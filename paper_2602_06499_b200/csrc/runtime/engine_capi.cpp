@@ -1,26 +1,115 @@
-// Temporary: engine entry points (filled in by engine.cpp).
+// C ABI of the per-rank engine (include/fcdp.h, "engine").
 #include "capi_util.hpp"
 #include "fcdp.h"
+#include "runtime/engine.hpp"
+
+#include <chrono>
+#include <thread>
+
+struct fcdp_engine {
+  fcdp::Engine* impl;
+};
 
 using fcdp::guarded;
 
-extern "C" {
-#define NOT_YET return guarded([] { throw std::runtime_error("engine: not implemented yet"); })
-int fcdp_engine_create(const fcdp_engine_config*, const fcdp_model*, const fcdp_topology*, const fcdp_plan*,
-                       const uint8_t* const*, fcdp_engine**) { NOT_YET; }
-int fcdp_engine_init_params(fcdp_engine*, uint64_t, const fcdp_init_range* const*, const int32_t*) { NOT_YET; }
-int fcdp_engine_set_adam(fcdp_engine*, const fcdp_adam_config*) { NOT_YET; }
-int fcdp_engine_set_compute(fcdp_engine*, fcdp_compute_fn, void*) { NOT_YET; }
-int fcdp_engine_run(fcdp_engine*, const fcdp_program*, fcdp_states*) { NOT_YET; }
-int fcdp_engine_sync(fcdp_engine*) { NOT_YET; }
-int fcdp_engine_barrier(fcdp_engine*) { NOT_YET; }
-int fcdp_engine_streams(fcdp_engine*, void**) { NOT_YET; }
-int fcdp_engine_counters(fcdp_engine*, int32_t, fcdp_counters*) { NOT_YET; }
-int fcdp_engine_reset_counters(fcdp_engine*) { NOT_YET; }
-int fcdp_engine_read_shard(fcdp_engine*, int32_t, int32_t, void*, size_t) { NOT_YET; }
-int fcdp_engine_read_master(fcdp_engine*, int32_t, float*, size_t) { NOT_YET; }
-int fcdp_engine_read_grad(fcdp_engine*, int32_t, float*, size_t) { NOT_YET; }
-int fcdp_engine_read_host_cache(fcdp_engine*, int32_t, int32_t, void*, size_t) { NOT_YET; }
-int fcdp_engine_last_gathered(fcdp_engine*, int32_t, void*, size_t) { NOT_YET; }
-void fcdp_engine_destroy(fcdp_engine*) {}
+namespace {
+fcdp::Engine& E(fcdp_engine* e) {
+  if (!e || !e->impl) throw shardsim::ConfigError("engine: null handle");
+  return *e->impl;
 }
+}  // namespace
+
+extern "C" {
+
+int fcdp_engine_create(const fcdp_engine_config* cfg, const fcdp_model* model, const fcdp_topology* topo,
+                       const fcdp_plan* plan, const uint8_t* const* masks, fcdp_engine** out) {
+  return guarded([&] {
+    auto* impl = new fcdp::Engine(*cfg, fcdp::model_from_c(model), fcdp::topo_from_c(topo),
+                                  fcdp::plan_from_c(plan), masks);
+    *out = new fcdp_engine{impl};
+  });
+}
+
+int fcdp_engine_init_params(fcdp_engine* e, uint64_t seed, const fcdp_init_range* const* ranges,
+                            const int32_t* num_ranges) {
+  return guarded([&] { E(e).init_params(seed, ranges, num_ranges); });
+}
+
+int fcdp_engine_set_adam(fcdp_engine* e, const fcdp_adam_config* cfg) {
+  return guarded([&] { E(e).set_adam(*cfg); });
+}
+
+int fcdp_engine_set_compute(fcdp_engine* e, fcdp_compute_fn fn, void* user) {
+  return guarded([&] { E(e).set_compute(fn, user); });
+}
+
+int fcdp_engine_run(fcdp_engine* e, const fcdp_program* program, fcdp_states* states) {
+  return guarded([&] { E(e).run(fcdp::program_from_c(program), fcdp::states_from_c(states)); });
+}
+
+int fcdp_engine_sync(fcdp_engine* e) { return guarded([&] { E(e).sync(); }); }
+int fcdp_engine_barrier(fcdp_engine* e) { return guarded([&] { E(e).barrier(); }); }
+
+int fcdp_engine_streams(fcdp_engine* e, void** compute_stream) {
+  return guarded([&] { *compute_stream = E(e).compute_stream(); });
+}
+
+int fcdp_engine_counters(fcdp_engine* e, int32_t rank, fcdp_counters* out) {
+  return guarded([&] { E(e).counters(rank, out); });
+}
+
+int fcdp_engine_reset_counters(fcdp_engine* e) { return guarded([&] { E(e).reset_counters(); }); }
+
+int fcdp_engine_read_shard(fcdp_engine* e, int32_t layer, int32_t frozen, void* host, size_t bytes) {
+  return guarded([&] { E(e).read_shard(layer, frozen != 0, host, bytes); });
+}
+
+int fcdp_engine_read_master(fcdp_engine* e, int32_t layer, float* host, size_t count) {
+  return guarded([&] { E(e).read_master(layer, host, count); });
+}
+
+int fcdp_engine_read_grad(fcdp_engine* e, int32_t layer, float* host, size_t count) {
+  return guarded([&] { E(e).read_grad(layer, host, count); });
+}
+
+int fcdp_engine_read_host_cache(fcdp_engine* e, int32_t layer, int32_t frozen, void* host, size_t bytes) {
+  return guarded([&] { E(e).read_host_cache(layer, frozen != 0, host, bytes); });
+}
+
+int fcdp_engine_last_gathered(fcdp_engine* e, int32_t, void*, size_t) {
+  return guarded([&] {
+    E(e);
+    throw shardsim::ConfigError("engine: capture gathered layers in the compute callback instead");
+  });
+}
+
+int fcdp_nic_selftest(const char* name, int32_t rank, int32_t nodes, int32_t local, double bw, uint64_t payload,
+                      int32_t rounds, double* elapsed) {
+  return guarded([&] {
+    fcdp::SharedBlock shm(name ? name : "", rank, nodes * local, nodes, local, 2, 4096, 60.0);
+    shm.barrier(60.0);
+    const std::uint64_t t0 = fcdp::SharedBlock::now_ns();
+    const int node = rank / local;
+    const auto ns = static_cast<std::uint64_t>(static_cast<double>(payload) / bw * 1e9);
+    for (int i = 0; i < rounds; ++i) {
+      const std::uint64_t finish = shm.reserve_nic(node, ns);
+      while (fcdp::SharedBlock::now_ns() < finish) std::this_thread::sleep_for(std::chrono::microseconds(50));
+      shm.add(rank, fcdp::kTxFwdAg, payload);
+      shm.barrier(60.0);
+    }
+    *elapsed = static_cast<double>(fcdp::SharedBlock::now_ns() - t0) * 1e-9;
+    std::uint64_t node_bytes = 0;
+    for (int j = 0; j < local; ++j) node_bytes += shm.counter(node * local + j, fcdp::kTxFwdAg);
+    if (node_bytes != payload * static_cast<std::uint64_t>(rounds) * static_cast<std::uint64_t>(local))
+      throw std::runtime_error("nic selftest: node byte counter mismatch");
+    shm.barrier(60.0);
+  });
+}
+
+void fcdp_engine_destroy(fcdp_engine* e) {
+  if (!e) return;
+  delete e->impl;
+  delete e;
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+// NIC emulator: one thread per rank that turns "my staged payload is in host
+// memory" (a CUDA event on the staging D2H) into "my payload has crossed the
+// emulated network" (a flag peers' streams wait on), after charging the
+// payload's wire time to the sending node's single NIC (reference
+// topology.hpp:23-25 "one NIC per node"; "Per-node NIC serializes
+// all its GPUs' inter-node traffic").  Wire time = bytes / inter-node
+// bandwidth of the topology preset (topology.cpp:22-34 in the reference).
+#pragma once
+
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <mutex>
+#include <thread>
+
+#include <cuda_runtime.h>
+
+#include "runtime/shm.hpp"
+
+namespace fcdp {
+
+struct NicJob {
+  int cls;               // 0 = all-gather, 1 = reduce-scatter
+  std::uint32_t seq;     // per-class sequence number, monotone
+  cudaEvent_t staged;    // recorded after the staging D2H
+  std::uint64_t wire_bytes;  // bytes this rank puts on its node's NIC
+  Counter counter;       // which tx counter to charge
+};
+
+class NicEmulator {
+ public:
+  NicEmulator(SharedBlock& shm, int rank, int node, int device, double bytes_per_s, bool pacing);
+  ~NicEmulator();
+  void submit(const NicJob& job);
+  std::uint64_t published(int cls) const;
+
+ private:
+  void loop();
+  struct Flight {
+    NicJob job;
+    std::uint64_t finish_ns;
+  };
+  SharedBlock& shm_;
+  int rank_, node_, device_;
+  double bytes_per_ns_;
+  bool pacing_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<NicJob> queue_[2];
+  std::deque<Flight> flight_[2];
+  bool stop_ = false;
+  std::thread thread_;
+};
+
+}  // namespace fcdp

@@ -1,0 +1,137 @@
+#include "runtime/shm.hpp"
+
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <chrono>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <thread>
+
+#include "capi_util.hpp"
+
+namespace fcdp {
+namespace {
+
+std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
+
+std::string shm_path(const std::string& name) { return name.empty() || name[0] != '/' ? "/" + name : name; }
+
+}  // namespace
+
+std::uint64_t SharedBlock::now_ns() {
+  return static_cast<std::uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                        std::chrono::steady_clock::now().time_since_epoch())
+                                        .count());
+}
+
+SharedBlock::SharedBlock(const std::string& name, int rank, int world, int nodes, int local,
+                         int inter_slots, std::uint64_t slot_bytes, double timeout_s)
+    : name_(shm_path(name)), rank_(rank) {
+  if (world < 1 || world > kMaxRanks || nodes * local != world || rank < 0 || rank >= world)
+    throw shardsim::ConfigError("engine: world_size must equal num_nodes * gpus_per_node (<= 64)");
+  slot_bytes = round_up(slot_bytes ? slot_bytes : 4096, 4096);
+  slots_offset_ = round_up(sizeof(ShmHeader), 1 << 21);
+  bytes_ = slots_offset_ + static_cast<std::size_t>(world) * 2 * inter_slots * slot_bytes;
+  bytes_ = round_up(bytes_, 1 << 21);
+
+  int fd = -1;
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
+  if (rank == 0) {
+    shm_unlink(name_.c_str());  // a stale segment of a crashed job with the same name
+    fd = shm_open(name_.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) throw std::runtime_error("shm_open(create " + name_ + ") failed: " + std::strerror(errno));
+    if (ftruncate(fd, static_cast<off_t>(bytes_)) != 0) {
+      close(fd);
+      throw std::runtime_error("ftruncate(shm) failed: " + std::string(std::strerror(errno)));
+    }
+  } else {
+    for (;;) {
+      fd = shm_open(name_.c_str(), O_RDWR, 0600);
+      if (fd >= 0) {
+        struct stat st {};
+        if (fstat(fd, &st) == 0 && static_cast<std::size_t>(st.st_size) >= bytes_) break;
+        close(fd);
+        fd = -1;
+      }
+      if (std::chrono::steady_clock::now() > deadline)
+        throw TimeoutError("engine: shared control block " + name_ + " did not appear");
+      std::this_thread::sleep_for(std::chrono::milliseconds(2));
+    }
+  }
+  void* p = mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) throw std::runtime_error("mmap(shm) failed: " + std::string(std::strerror(errno)));
+  hdr_ = static_cast<ShmHeader*>(p);
+
+  if (rank == 0) {
+    // ftruncate zero-fills; publish geometry, then the magic last.
+    hdr_->world = world;
+    hdr_->nodes = nodes;
+    hdr_->local = local;
+    hdr_->inter_slots = inter_slots;
+    hdr_->slot_bytes = slot_bytes;
+    hdr_->total_bytes = bytes_;
+    hdr_->magic.store(kShmMagic, std::memory_order_release);
+  } else {
+    while (hdr_->magic.load(std::memory_order_acquire) != kShmMagic) {
+      if (std::chrono::steady_clock::now() > deadline)
+        throw TimeoutError("engine: shared control block " + name_ + " not initialised");
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+    if (hdr_->world != world || hdr_->nodes != nodes || hdr_->local != local ||
+        hdr_->slot_bytes != slot_bytes || hdr_->inter_slots != inter_slots)
+      throw shardsim::ConfigError("engine: ranks disagree on the job geometry");
+  }
+  hdr_->ranks[rank].pid = static_cast<std::int32_t>(getpid());
+  hdr_->ranks[rank].attached.store(1, std::memory_order_release);
+}
+
+SharedBlock::~SharedBlock() {
+  if (hdr_) munmap(hdr_, bytes_);
+  if (rank_ == 0) shm_unlink(name_.c_str());
+}
+
+unsigned char* SharedBlock::slot(int rank, int cls, int idx) const {
+  const std::size_t per_rank = 2ull * hdr_->inter_slots * hdr_->slot_bytes;
+  return reinterpret_cast<unsigned char*>(hdr_) + slots_offset_ + rank * per_rank +
+         (static_cast<std::size_t>(cls) * hdr_->inter_slots + idx) * hdr_->slot_bytes;
+}
+
+void SharedBlock::reset_counters(int rank) const {
+  for (auto& c : hdr_->ranks[rank].counters) c.store(0, std::memory_order_relaxed);
+}
+
+void SharedBlock::barrier(double timeout_s) const {
+  const std::uint32_t gen = hdr_->barrier_gen.load(std::memory_order_acquire);
+  if (hdr_->barrier_count.fetch_add(1, std::memory_order_acq_rel) + 1 ==
+      static_cast<std::uint32_t>(hdr_->world)) {
+    hdr_->barrier_count.store(0, std::memory_order_relaxed);
+    hdr_->barrier_gen.store(gen + 1, std::memory_order_release);
+    return;
+  }
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
+  int spins = 0;
+  while (hdr_->barrier_gen.load(std::memory_order_acquire) == gen) {
+    if (hdr_->abort_flag.load(std::memory_order_relaxed)) throw TimeoutError("engine: job aborted by a peer");
+    if (++spins > 1000) {
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+      if (std::chrono::steady_clock::now() > deadline) throw TimeoutError("engine: barrier timed out");
+    }
+  }
+}
+
+std::uint64_t SharedBlock::reserve_nic(int node, std::uint64_t ns) const {
+  auto& clock = hdr_->node_blocks[node].nic_busy_until_ns;
+  const std::uint64_t now = now_ns();
+  std::uint64_t cur = clock.load(std::memory_order_relaxed);
+  for (;;) {
+    const std::uint64_t start = cur > now ? cur : now;
+    if (clock.compare_exchange_weak(cur, start + ns, std::memory_order_acq_rel)) return start + ns;
+  }
+}
+
+}  // namespace fcdp

@@ -151,9 +151,12 @@ class _ModelHandle:
         self.ptr = ptr
 
     def __del__(self):
-        if self.ptr and _capi._lib is not None:
-            _capi._lib.fcdp_model_destroy(self.ptr)
-            self.ptr = None
+        try:
+            if self.ptr and _capi._lib is not None:
+                _capi._lib.fcdp_model_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
 
 
 @dataclass
@@ -406,9 +409,12 @@ class _States:
         self.ptr = ptr
 
     def __del__(self):
-        if self.ptr and _capi._lib is not None:
-            _capi._lib.fcdp_states_destroy(self.ptr)
-            self.ptr = None
+        try:
+            if self.ptr and _capi._lib is not None:
+                _capi._lib.fcdp_states_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
 
     @staticmethod
     def from_list(states: Sequence[ParamState]) -> "_States":
@@ -445,9 +451,12 @@ class EventProgram:
         self._events = None
 
     def __del__(self):
-        if getattr(self, "ptr", None) and _capi._lib is not None:
-            _capi._lib.fcdp_program_destroy(self.ptr)
-            self.ptr = None
+        try:
+            if getattr(self, "ptr", None) and _capi._lib is not None:
+                _capi._lib.fcdp_program_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
 
     @property
     def events(self) -> List[Event]:

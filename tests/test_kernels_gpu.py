@@ -80,7 +80,8 @@ def test_partition_bit_exact(built, chunks):
         lay = _layout(lib, chunks, m, 2, 2, 2)
         dt = torch.zeros(max(t.size, 16), dtype=torch.uint8, device=dev)
         df = torch.zeros(max(f.size, 16), dtype=torch.uint8, device=dev)
-        check(lib.fcdp_partition(lay, _ptr(_u8(nat, dev)), _ptr(dt), _ptr(df), None))
+        dnat = _u8(nat, dev)
+        check(lib.fcdp_partition(lay, _ptr(dnat), _ptr(dt), _ptr(df), None))
         torch.cuda.synchronize()
         assert np.array_equal(dt.cpu().numpy()[:t.size], t), name
         assert np.array_equal(df.cpu().numpy()[:f.size], f), name
@@ -136,8 +137,8 @@ def test_rs_finalize_bit_exact(built, eb):
     for node in range(N):
         ref = O.rs_finalize(own, wire, N, node, eb, n, 0.125)
         out = torch.zeros(n, dtype=torch.float32, device=dev)
-        check(lib.fcdp_rs_finalize(n, N, node, eb, _ptr(_u8(own, dev)), _ptr(_u8(wire, dev)), n,
-                                   0.125, _ptr(out), None))
+        down, dwire = _u8(own, dev), _u8(wire, dev)  # keep alive until the kernel ran
+        check(lib.fcdp_rs_finalize(n, N, node, eb, _ptr(down), _ptr(dwire), n, 0.125, _ptr(out), None))
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
 
@@ -158,8 +159,9 @@ def test_adam_bit_exact(built, eb):
         g = (rng.standard_normal(n) * 1e-2).astype(np.float32)
         O.adam(w, m, v, g, p, 1e-3, 0.9, 0.95, 1e-8, 0.1, step)
         cfg = _capi.AdamConfig(1e-3, 0.9, 0.95, 1e-8, 0.1, step)
-        _capi.check(lib.fcdp_adam_step(n, C.byref(cfg), _ptr(dw), _ptr(dm), _ptr(dv),
-                                       _ptr(torch.from_numpy(g).to(dev)), _ptr(dp), eb, None))
+        dg = torch.from_numpy(g).to(dev)
+        _capi.check(lib.fcdp_adam_step(n, C.byref(cfg), _ptr(dw), _ptr(dm), _ptr(dv), _ptr(dg), _ptr(dp),
+                                       eb, None))
         torch.cuda.synchronize()
         assert np.array_equal(dw.cpu().numpy().view(np.uint32), w.view(np.uint32)), step
         assert np.array_equal(dv.cpu().numpy().view(np.uint32), v.view(np.uint32)), step
