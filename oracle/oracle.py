@@ -113,8 +113,9 @@ def rs_finalize(own: np.ndarray, wire: np.ndarray, nodes: int, node: int, elem_b
 
 
 def adam(master, m, v, grad, param, lr, beta1, beta2, eps, wd, step):
-    bc1 = np.float32(1.0 - beta1 ** step) if False else np.float32(1.0 - float(np.float64(beta1) ** step))
-    bc2 = np.float32(1.0 - float(np.float64(beta2) ** step))
+    # bias corrections in double from the fp32 betas, as the engine computes them
+    bc1 = np.float32(1.0 - float(np.float64(np.float32(beta1)) ** step))
+    bc2 = np.float32(1.0 - float(np.float64(np.float32(beta2)) ** step))
     eb = param.dtype.itemsize
     lib().fo_adam(master.size, lr, beta1, beta2, eps, wd, float(bc1), float(bc2), _p(master), _p(m), _p(v),
                   _p(grad), _p(param), eb)

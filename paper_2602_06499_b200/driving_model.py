@@ -1,0 +1,210 @@
+"""Driving models for the FCDP data plane (the compute behind ComputeFwd/Bwd).
+
+The reference models a layer only by its size (workload.hpp:13-33); to train
+something real the B200 build needs the layers themselves.  Each layer is ONE
+flat natural-order buffer (the unit the shard store gathers) carved into
+named tensors, so a ModelSpec layer list and the PEFT chunk mask fall out of
+the tensor list:
+
+    GPT-2 (LayerNorm, GELU, biased MHA)        - configs C1 (tiny) and C2 (1.3B)
+    Llama (RMSNorm, SwiGLU, RoPE) + LoRA q,k,v,o - configs C3 (7B r=16) and C4 (13B)
+
+Explicit layer lists: [embedding] + blocks + [final norm + untied head].  The
+compute uses torch (cuBLAS GEMMs on tensor cores, SDPA attention) on the
+engine's compute stream: it is the consumer of the hot path, not the hot path.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+CHUNK = 16
+
+
+@dataclass
+class TensorSpec:
+    name: str
+    shape: Tuple[int, ...]
+    init: str = "uniform"   # uniform(-scale, scale) | const
+    scale: float = 0.02
+    trainable: bool = True
+
+    @property
+    def numel(self) -> int:
+        return int(np.prod(self.shape))
+
+
+@dataclass
+class LayerDef:
+    kind: str                       # "embed" | "gpt2_block" | "llama_block" | "head"
+    tensors: List[TensorSpec]
+    offsets: Dict[str, int] = field(default_factory=dict)
+
+    def __post_init__(self):
+        off = 0
+        for t in self.tensors:
+            self.offsets[t.name] = off
+            off += t.numel
+        self.numel = off
+
+    def chunk_mask(self, elem_bytes: int) -> np.ndarray:
+        V = CHUNK // elem_bytes
+        if self.numel % V:
+            raise ValueError(f"{self.kind}: {self.numel} params is not a whole number of 16-byte chunks")
+        m = np.zeros(self.numel // V, np.uint8)
+        for t in self.tensors:
+            if t.trainable:
+                o = self.offsets[t.name]
+                if o % V or t.numel % V:
+                    raise ValueError(f"trainable tensor {t.name} is not 16-byte aligned")
+                m[o // V:(o + t.numel) // V] = 1
+        return m
+
+    def trainable_params(self) -> int:
+        return sum(t.numel for t in self.tensors if t.trainable)
+
+    def init_ranges(self):
+        rs = []
+        for t in self.tensors:
+            o = self.offsets[t.name]
+            rs.append((o, o + t.numel, 1 if t.init == "const" else 0, float(t.scale)))
+        return rs
+
+
+@dataclass
+class ModelConfig:
+    family: str          # "gpt2" | "llama"
+    hidden: int
+    layers: int
+    heads: int
+    vocab: int
+    seq: int
+    ffn: int = 0
+    lora_rank: int = 0   # > 0: LoRA on q,k,v,o; base weights frozen
+    dtype_bytes: int = 2
+    name: str = ""
+
+    def layer_defs(self) -> List[LayerDef]:
+        h, V = self.hidden, self.vocab
+        peft = self.lora_rank > 0
+        defs = []
+        if self.family == "gpt2":
+            defs.append(LayerDef("embed", [TensorSpec("wte", (V, h), scale=0.02, trainable=not peft),
+                                           TensorSpec("wpe", (self.seq, h), scale=0.01, trainable=not peft)]))
+            s = 0.02
+            for _ in range(self.layers):
+                defs.append(LayerDef("gpt2_block", [
+                    TensorSpec("ln1_w", (h,), "const", 1.0), TensorSpec("ln1_b", (h,), "const", 0.0),
+                    TensorSpec("qkv_w", (3 * h, h), scale=s), TensorSpec("qkv_b", (3 * h,), "const", 0.0),
+                    TensorSpec("proj_w", (h, h), scale=s / math.sqrt(2 * self.layers)),
+                    TensorSpec("proj_b", (h,), "const", 0.0),
+                    TensorSpec("ln2_w", (h,), "const", 1.0), TensorSpec("ln2_b", (h,), "const", 0.0),
+                    TensorSpec("fc_w", (4 * h, h), scale=s), TensorSpec("fc_b", (4 * h,), "const", 0.0),
+                    TensorSpec("fc2_w", (h, 4 * h), scale=s / math.sqrt(2 * self.layers)),
+                    TensorSpec("fc2_b", (h,), "const", 0.0)]))
+            defs.append(LayerDef("head", [TensorSpec("lnf_w", (h,), "const", 1.0),
+                                          TensorSpec("lnf_b", (h,), "const", 0.0),
+                                          TensorSpec("lm_w", (V, h), scale=0.02)]))
+        elif self.family == "llama":
+            f, r = self.ffn, self.lora_rank
+            defs.append(LayerDef("embed", [TensorSpec("wte", (V, h), scale=0.02, trainable=not peft)]))
+            for _ in range(self.layers):
+                ts = [TensorSpec("attn_norm", (h,), "const", 1.0, trainable=not peft)]
+                for p in ("q", "k", "v", "o"):
+                    ts.append(TensorSpec(f"{p}_w", (h, h), scale=0.02, trainable=not peft))
+                    if peft:
+                        ts.append(TensorSpec(f"{p}_A", (r, h), scale=0.02, trainable=True))
+                        # B != 0 so that A receives gradient from step 1 (parity runs)
+                        ts.append(TensorSpec(f"{p}_B", (h, r), scale=1e-3, trainable=True))
+                ts += [TensorSpec("mlp_norm", (h,), "const", 1.0, trainable=not peft),
+                       TensorSpec("gate_w", (f, h), scale=0.02, trainable=not peft),
+                       TensorSpec("up_w", (f, h), scale=0.02, trainable=not peft),
+                       TensorSpec("down_w", (h, f), scale=0.02, trainable=not peft)]
+                defs.append(LayerDef("llama_block", ts))
+            defs.append(LayerDef("head", [TensorSpec("norm_w", (h,), "const", 1.0, trainable=not peft),
+                                          TensorSpec("lm_w", (V, h), scale=0.02, trainable=not peft)]))
+        else:
+            raise ValueError(f"unknown family {self.family}")
+        return defs
+
+
+PRESETS: Dict[str, ModelConfig] = {
+    # C1: tiny 2-layer transformer, hidden 256, fp32 (12h^2 + 13h = 789,760 params per block)
+    "tiny": ModelConfig("gpt2", 256, 2, 4, 1024, 64, dtype_bytes=4, name="tiny-h256-fp32"),
+    # C2: GPT-2 1.3B (h=2048, 24 layers, 16 heads, 50,358,272 params per block)
+    "gpt2-1.3b": ModelConfig("gpt2", 2048, 24, 16, 50257, 1024, name="gpt2-1.3b"),
+    # C3: Llama-style 7B + LoRA r=16 on q,k,v,o (202,907,648 params per block, 524,288 trainable)
+    "llama7b-lora16": ModelConfig("llama", 4096, 32, 32, 32000, 2048, ffn=11008, lora_rank=16,
+                                  name="llama7b-lora16"),
+    # C4: Llama-style 13B, full training (317,204,480 params per block)
+    "llama13b": ModelConfig("llama", 5120, 40, 40, 32000, 2048, ffn=13824, name="llama13b"),
+    # small variants for tests / smoke
+    "gpt2-small-test": ModelConfig("gpt2", 128, 3, 4, 512, 32, name="gpt2-small-test"),
+    "llama-lora-test": ModelConfig("llama", 128, 3, 4, 512, 32, ffn=352, lora_rank=8, name="llama-lora-test"),
+}
+
+
+# ---------------------------------------------------------------- compute
+
+def _views(flat, ldef: LayerDef):
+    return {t.name: flat[ldef.offsets[t.name]:ldef.offsets[t.name] + t.numel].view(t.shape)
+            for t in ldef.tensors}
+
+
+def _rope(x, base=10000.0):
+    import torch
+    b, nh, s, d = x.shape
+    pos = torch.arange(s, device=x.device, dtype=torch.float32)
+    inv = base ** (-torch.arange(0, d, 2, device=x.device, dtype=torch.float32) / d)
+    ang = pos[:, None] * inv[None, :]
+    cos, sin = ang.cos().to(x.dtype), ang.sin().to(x.dtype)
+    x1, x2 = x[..., 0::2], x[..., 1::2]
+    out = torch.stack((x1 * cos - x2 * sin, x1 * sin + x2 * cos), dim=-1)
+    return out.flatten(-2)
+
+
+def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=None):
+    """Forward of one layer.  x: [b, s, h] (None for the embedding)."""
+    import torch
+    import torch.nn.functional as F
+    h, nh = cfg.hidden, cfg.heads
+    if ldef.kind == "embed":
+        y = F.embedding(tokens, p["wte"])
+        if "wpe" in p:
+            y = y + p["wpe"][: tokens.shape[1]].unsqueeze(0)
+        return y
+    if ldef.kind == "gpt2_block":
+        b, s, _ = x.shape
+        a = F.layer_norm(x, (h,), p["ln1_w"], p["ln1_b"])
+        qkv = F.linear(a, p["qkv_w"], p["qkv_b"]).view(b, s, 3, nh, h // nh).permute(2, 0, 3, 1, 4)
+        o = F.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], is_causal=True)
+        x = x + F.linear(o.transpose(1, 2).reshape(b, s, h), p["proj_w"], p["proj_b"])
+        m = F.layer_norm(x, (h,), p["ln2_w"], p["ln2_b"])
+        return x + F.linear(F.gelu(F.linear(m, p["fc_w"], p["fc_b"]), approximate="tanh"), p["fc2_w"], p["fc2_b"])
+    if ldef.kind == "llama_block":
+        b, s, _ = x.shape
+        a = F.rms_norm(x, (h,), p["attn_norm"], eps=1e-5)
+
+        def proj(name, inp):
+            y = F.linear(inp, p[f"{name}_w"])
+            if f"{name}_A" in p:
+                y = y + F.linear(F.linear(inp, p[f"{name}_A"]), p[f"{name}_B"])
+            return y
+        q = _rope(proj("q", a).view(b, s, nh, h // nh).transpose(1, 2))
+        k = _rope(proj("k", a).view(b, s, nh, h // nh).transpose(1, 2))
+        v = proj("v", a).view(b, s, nh, h // nh).transpose(1, 2)
+        o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        x = x + proj("o", o.transpose(1, 2).reshape(b, s, h))
+        m = F.rms_norm(x, (h,), p["mlp_norm"], eps=1e-5)
+        return x + F.linear(F.silu(F.linear(m, p["gate_w"])) * F.linear(m, p["up_w"]), p["down_w"])
+    if ldef.kind == "head":
+        if "lnf_w" in p:
+            a = F.layer_norm(x, (h,), p["lnf_w"], p["lnf_b"])
+        else:
+            a = F.rms_norm(x, (h,), p["norm_w"], eps=1e-5)
+        logits = F.linear(a, p["lm_w"])
+        return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), labels.view(-1))
+    raise ValueError(ldef.kind)
