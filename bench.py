@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""FCDP on B200: training-step throughput and inter-group all-gather bytes.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fcdp|reference]
+
+Metric (BASELINE.json): train step tokens/s at 1/2/4/8 B200, with the
+inter-group AG bytes per step against an on-box ZeRO-3 schedule.  The 8-GPU
+config is GPT-2 1.3B as 2 emulated nodes x 4 GPUs behind a throttled
+host-staged inter-node link; N GPUs map to the emulated topology
+1 -> 1x1, 2 -> 2x1, 4 -> 2x2, 8 -> 2x4 (weak scaling: batch per GPU fixed).
+
+One process per GPU (torchrun for N > 1).  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+import uuid
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "train step tokens/s at 1/2/4/8 B200; inter-group AG bytes/step vs ZeRO-3"
+TOPOLOGY = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="fcdp", choices=["fcdp", "reference"])
+    p.add_argument("--preset", default="gpt2-1.3b")
+    p.add_argument("--strategy", default="fcdp")
+    p.add_argument("--inter", default="ib100-rdma-measured")
+    p.add_argument("--batch", type=int, default=8)
+    p.add_argument("--seq", type=int, default=0)
+    p.add_argument("--topology", default="", help="override NxG, e.g. 1x2")
+    p.add_argument("--zero3-steps", type=int, default=3)
+    p.add_argument("--no-zero3", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--copy-engine", action="store_true")
+    return p.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self):
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def ncu_traffic(kernel_class: str):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    try:
+        s = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
+        return s.get(kernel_class, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def run_reference(args, world_n):
+    """--impl reference: the oracle port of the path on the host cores (rank 0)."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle.cpu_step import cpu_step_sample
+    from paper_2602_06499_b200.driving_model import PRESETS
+    mc = PRESETS[args.preset]
+    seq = args.seq or mc.seq
+    N, g = TOPOLOGY.get(world_n, (1, world_n))
+    vals = []
+    t0 = time.time()
+    r = None
+    for _ in range(max(1, args.steps)):
+        r = cpu_step_sample(args.preset, batch=args.batch, seq=seq, repeats=1)
+        vals.append(r["tokens_per_s_per_gpu"])
+        if time.time() - t0 > 240:
+            break
+    value = statistics.median(vals) * 1.0  # the whole job's work runs on the same host cores
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world_n,
+            "steps": len(vals), "warmup": 1, "ms_per_step": 1e3 * args.batch * seq / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if mc.dtype_bytes == 2 else "fp32", "data": "synthetic",
+            "config": workload_config(args, mc, N, g, world_n, seq),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+                             "sample": r["sample"]},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, mc, N, g, world, seq):
+    return {"workload": f"{mc.name} {args.strategy} train step, {N}x{g} emulated nodes x GPUs, "
+                        f"inter link {args.inter} (paced NIC emulator)",
+            "model": mc.name, "global_batch": args.batch * world, "seq_len": seq,
+            "parallelism": f"{args.strategy} dp{world} ({N} emulated nodes x {g} GPUs)",
+            "topology": f"{N}x{g}", "inter_link": args.inter, "strategy": args.strategy,
+            "l2": "inputs larger than L2 (layer params, host cache, optimizer state >> 126 MB)"}
+
+
+def main():
+    args = parse()
+    rank, world, local = env_rank()
+    if args.impl == "reference":
+        run_reference(args, args.gpus if world == 1 else world)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2602_06499_b200 import shardsim as S
+    from paper_2602_06499_b200.driving_model import PRESETS
+    from paper_2602_06499_b200.trainer import FcdpTrainer, synthetic_batch
+
+    if world != args.gpus and world > 1:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if args.topology:
+        N, g = (int(x) for x in args.topology.lower().split("x"))
+    else:
+        N, g = TOPOLOGY.get(world, (1, world))
+    assert N * g == world, "topology must cover every rank"
+    mc = PRESETS[args.preset]
+    seq = args.seq or mc.seq
+    topo = S.make_topology(N, g, inter_preset=args.inter)
+
+    def bcast(obj):
+        if world == 1:
+            return obj
+        box = [obj]
+        dist.broadcast_object_list(box, src=0)
+        return box[0]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def measure(strategy: str, steps: int, warmup: int, timing: bool, e2e_steps: int):
+        plan = S.StrategyPlan(S.StrategyKind.from_string(strategy))
+        shm = bcast(f"fcdp_bench_{uuid.uuid4().hex[:12]}" if rank == 0 else None)
+        tr = FcdpTrainer(mc, topo, plan, rank=rank, world_size=world, device=local, shm_name=shm,
+                         batch_per_gpu=args.batch, seq_len=seq, nic_pacing=True, lr=1e-4,
+                         use_copy_engine=args.copy_engine)
+        batches = [synthetic_batch(mc.vocab, args.batch, seq, 0x5EED, i, rank, device=dev)
+                   for i in range(warmup + steps)]
+        for i in range(warmup):
+            tr.step(*batches[i])
+        tr.sync()
+        torch.cuda.synchronize()
+        barrier()
+        tr.engine.reset_counters()
+        tr.engine.kernel_stats(reset=True)
+        tr.engine.set_timing(timing)
+        barrier()
+        sampler = ClockSampler() if (rank == 0 and timing) else None
+        if sampler:
+            sampler.start()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(tr.stream)
+        for i in range(steps):
+            loss = tr.step(*batches[warmup + i])
+        e1.record(tr.stream)
+        tr.sync()
+        torch.cuda.synchronize()
+        barrier()
+        clocks = sampler.stop() if sampler else None
+        ms = max_over_ranks(e0.elapsed_time(e1))
+        counters = tr.engine.counters()
+        kst = tr.engine.kernel_stats(reset=True)
+        tr.engine.set_timing(False)
+        loss_v = float(loss.item())
+        # per-node inter-group bytes per step (sum over the node's ranks), from the NIC counters
+        node_tx = {k: sum_over_ranks(counters[k]) / N / steps for k in ("nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs")}
+        cache = {k: sum_over_ranks(counters[k]) / N / steps for k in ("cache_h2d", "cache_d2h")}
+        vol = S.comm_volume(plan, tr.model, topo, warmup + steps)
+        e2e = None
+        if e2e_steps:
+            host = [synthetic_batch(mc.vocab, args.batch, seq, 0x5EED, 10_000 + i, rank, pin=True)
+                    for i in range(e2e_steps)]
+            tr.sync()
+            barrier()
+            h2d = sum(x.numel() * x.element_size() + y.numel() * y.element_size() for x, y in host[:1])
+            torch.cuda.synchronize()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(tr.stream)
+            for x, y in host:
+                with torch.cuda.stream(tr.stream):
+                    xd = x.to(dev, non_blocking=True)
+                    yd = y.to(dev, non_blocking=True)
+                l = tr.step(xd, yd)
+                l.item()  # device -> host read of the step's result
+            f1.record(tr.stream)
+            tr.sync()
+            torch.cuda.synchronize()
+            barrier()
+            ems = max_over_ranks(f0.elapsed_time(f1))
+            e2e = {"value": world * args.batch * seq * e2e_steps / (ems / 1e3), "unit": "tokens/s",
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4, "steps": e2e_steps}
+        tr.close()
+        del tr
+        torch.cuda.empty_cache()
+        return {"ms": ms, "counters": counters, "kernels": kst, "clocks": clocks, "loss": loss_v,
+                "node_tx": node_tx, "cache": cache, "vol": vol, "e2e": e2e}
+
+    main_run = measure(args.strategy, args.steps, args.warmup, True, 0 if args.no_e2e else args.steps)
+    z3 = None
+    if not args.no_zero3 and args.strategy != "zero3":
+        z3 = measure("zero3", args.zero3_steps, 2, False, 0)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.cpu_step import cpu_step_sample
+        r = cpu_step_sample(args.preset, batch=args.batch, seq=seq, repeats=2)
+        cpu = {"value": r["tokens_per_s_per_gpu"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+               "sample": r["sample"]}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    tokens_per_step = world * args.batch * seq
+    ms_step = main_run["ms"] / args.steps
+    value = tokens_per_step / (ms_step / 1e3)
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs")
+    kst = main_run["kernels"]
+    dom = max(kst, key=lambda k: kst[k]["ms"]) if any(v["ms"] for v in kst.values()) else "adamw"
+    d = kst[dom]
+    per_launch_bytes = d["alg_bytes"] / max(d["launches"], 1)
+    per_launch_ms = d["ms"] / max(d["timed_launches"], 1)
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": (achieved / hbm) if (achieved and hbm) else None,
+                "traffic": ncu_traffic(dom), "alg_bytes_per_launch": per_launch_bytes,
+                "ms_per_launch": per_launch_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+                "share_of_step": d["ms"] / main_run["ms"] if main_run["ms"] else None}
+    gpu_launches = sum(v["launches"] for v in kst.values())
+    ag = {"fcdp_fwd": main_run["node_tx"]["nic_tx_fwd_ag"], "fcdp_bwd": main_run["node_tx"]["nic_tx_bwd_ag"],
+          "fcdp_rs": main_run["node_tx"]["nic_tx_rs"],
+          "oracle_fcdp_fwd": main_run["vol"].fwd_ag_inter, "oracle_fcdp_bwd": main_run["vol"].bwd_ag_inter}
+    if z3:
+        ag.update({"zero3_fwd": z3["node_tx"]["nic_tx_fwd_ag"], "zero3_bwd": z3["node_tx"]["nic_tx_bwd_ag"],
+                   "oracle_zero3": z3["vol"].fwd_ag_inter + z3["vol"].bwd_ag_inter})
+        tot_z = ag["zero3_fwd"] + ag["zero3_bwd"]
+        ag["eliminated_frac"] = (1 - (ag["fcdp_fwd"] + ag["fcdp_bwd"]) / tot_z) if tot_z else None
+    kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
+                   "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None} for k, v in kst.items()}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16" if mc.dtype_bytes == 2 else "fp32",
+        "data": "synthetic (counter-based token ids, random-init weights of the named architecture)",
+        "config": workload_config(args, mc, N, g, world, seq),
+        "e2e": main_run["e2e"], "gpu_launches": gpu_launches, "roofline": roofline,
+        "cpu_baseline": cpu, "clocks": main_run["clocks"],
+        "ag_inter_bytes_per_step_per_node": ag,
+        "zero3": ({"tokens_per_s": tokens_per_step / (z3["ms"] / z3_steps(args) / 1e3), "ms_per_step": z3["ms"] / z3_steps(args)}
+                  if z3 else None),
+        "cache_bytes_per_step_per_node": main_run["cache"],
+        "kernels": kernels, "loss": main_run["loss"],
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def z3_steps(args):
+    return args.zero3_steps
+
+
+if __name__ == "__main__":
+    main()

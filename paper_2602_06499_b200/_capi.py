@@ -91,6 +91,11 @@ class Counters(C.Structure):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
+class KernelStats(C.Structure):
+    _fields_ = [("launches", C.c_uint64 * 4), ("total_ms", C.c_double * 4), ("alg_bytes", C.c_uint64 * 4),
+                ("timed_launches", C.c_uint64 * 4)]
+
+
 COMPUTE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p)
 
 P = C.c_void_p
@@ -158,6 +163,8 @@ SIGNATURES = {
     "fcdp_engine_read_host_cache": (C.c_int, [P, i32, i32, P, C.c_size_t]),
     "fcdp_engine_last_gathered": (C.c_int, [P, i32, P, C.c_size_t]),
     "fcdp_engine_destroy": (None, [P]),
+    "fcdp_engine_set_timing": (C.c_int, [P, i32]),
+    "fcdp_engine_kernel_stats": (C.c_int, [P, C.POINTER(KernelStats), i32]),
     "fcdp_nic_selftest": (C.c_int, [C.c_char_p, i32, i32, i32, f64, u64, i32, C.POINTER(f64)]),
 }
 

@@ -57,6 +57,44 @@ bool wants_f(ParamSet s) { return s != ParamSet::TrainableOnly; }
 
 }  // namespace
 
+template <typename F>
+void Engine::timed(int cls, cudaStream_t s, std::uint64_t alg_bytes, F&& launch) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (timing_) {
+    for (cudaEvent_t* e : {&a, &b}) {
+      if (!timing_pool_.empty()) {
+        *e = timing_pool_.back();
+        timing_pool_.pop_back();
+      } else {
+        CK(cudaEventCreate(e));
+      }
+    }
+    CK(cudaEventRecord(a, s));
+  }
+  CK(launch());
+  kstats_.launches[cls] += 1;
+  kstats_.alg_bytes[cls] += alg_bytes;
+  if (timing_) {
+    CK(cudaEventRecord(b, s));
+    timed_pending_.push_back({cls, a, b, alg_bytes});
+  }
+}
+
+void Engine::kernel_stats(fcdp_kernel_stats* out, bool reset) {
+  sync();
+  for (const TimedLaunch& t : timed_pending_) {
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, t.a, t.b));
+    kstats_.total_ms[t.cls] += ms;
+    kstats_.timed_launches[t.cls] += 1;
+    timing_pool_.push_back(t.a);
+    timing_pool_.push_back(t.b);
+  }
+  timed_pending_.clear();
+  *out = kstats_;
+  if (reset) kstats_ = fcdp_kernel_stats{};
+}
+
 Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
                const shardsim::ClusterTopology& topo, const shardsim::StrategyPlan& plan,
                const std::uint8_t* const* chunk_masks)
@@ -130,6 +168,11 @@ Engine::~Engine() {
   for (cudaEvent_t e : x_reader_) cudaEventDestroy(e);
   for (cudaEvent_t e : staged_) cudaEventDestroy(e);
   for (cudaEvent_t e : rs_done_) cudaEventDestroy(e);
+  for (cudaEvent_t e : timing_pool_) cudaEventDestroy(e);
+  for (const TimedLaunch& t : timed_pending_) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
   if (iter_done_) cudaEventDestroy(iter_done_);
   for (cudaEvent_t e : join_)
     if (e) cudaEventDestroy(e);
@@ -406,7 +449,10 @@ void Engine::pull_expand(int layer, int slot, std::uint32_t q, bool want_t, bool
                          cudaMemcpyDeviceToDevice, s));
     }
   } else {
-    CK(launch_expand(l.L, ts, fs, W, set, s));
+    std::uint64_t out_bytes = 0;
+    if (want_t) out_bytes += l.L.dev.pt * kChunkBytes;
+    if (want_f) out_bytes += l.L.dev.pf * kChunkBytes;
+    timed(0, s, 2 * out_bytes, [&] { return launch_expand(l.L, ts, fs, W, set, s); });
   }
   write_flag(s, kSliceFree, q);
   std::uint64_t rx = 0;
@@ -616,10 +662,14 @@ void Engine::ev_reduce_scatter(const Event& e) {
   for (int jj = 0; jj < g_; ++jj) gp.p[jj] = grad_slot(jj, gs);
   const float scale = 1.0f / static_cast<float>(G_);
   float* final_out = grad32_ + l.off_t * V_;
+  // algorithmic bytes: g gradient slices read + fp32 own shard + dtype wire for the rest
+  const std::uint64_t rs_bytes = static_cast<std::uint64_t>(g_) * l.slice_real_t * C +
+                                 static_cast<std::uint64_t>(l.my_real_t) * V_ * sizeof(float) +
+                                 static_cast<std::uint64_t>(l.slice_real_t - l.my_real_t) * C;
   if (N_ == 1) {
-    CK(launch_rs_slice(l.L, gp, j_, 0, scale, true, final_out, wire_[gs], s));
+    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, 0, scale, true, final_out, wire_[gs], s); });
   } else {
-    CK(launch_rs_slice(l.L, gp, j_, n_, scale, false, own32_[gs], wire_[gs], s));
+    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, n_, scale, false, own32_[gs], wire_[gs], s); });
   }
   write_flag(s, kGradFree, u);
   CK(cudaEventRecord(rs_done_[gs], s));
@@ -663,8 +713,11 @@ void Engine::ev_reduce_scatter(const Event& e) {
   write_flag(s, kRsRxDone, seq);
   shm_->add(rank_, kStagingH2D, rx);
   shm_->add(rank_, kRxRs, rx);
-  CK(launch_rs_finalize(l.L.dev.shard_t * V_, N_, n_, eb_, own32_[gs], rx_[gs], l.L.dev.shard_t * V_, scale,
-                        final_out, s));
+  const std::uint64_t fin_elems = static_cast<std::uint64_t>(l.L.dev.shard_t) * V_;
+  timed(2, s, fin_elems * (2 * sizeof(float) + static_cast<std::uint64_t>(N_ - 1) * eb_), [&] {
+    return launch_rs_finalize(l.L.dev.shard_t * V_, N_, n_, eb_, own32_[gs], rx_[gs], l.L.dev.shard_t * V_, scale,
+                              final_out, s);
+  });
 }
 
 void Engine::ev_optimizer(const Event&) {
@@ -672,7 +725,9 @@ void Engine::ev_optimizer(const Event&) {
   AdamParams p{adam_.lr, adam_.beta1, adam_.beta2, adam_.eps, adam_.weight_decay,
                static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta1), opt_steps_)),
                static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta2), opt_steps_))};
-  CK(launch_adam(arena_t_ * V_, p, master_, adam_m_, adam_v_, grad32_, param_t_, eb_, s_comp_));
+  const std::uint64_t n = static_cast<std::uint64_t>(arena_t_) * V_;
+  timed(3, s_comp_, n * (7 * sizeof(float) + eb_),
+        [&] { return launch_adam(arena_t_ * V_, p, master_, adam_m_, adam_v_, grad32_, param_t_, eb_, s_comp_); });
   for (LayerRt& l : layers_)
     if (l.has_t) ++l.shard_version_t;
 }

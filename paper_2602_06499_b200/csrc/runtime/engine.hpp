@@ -75,6 +75,9 @@ class Engine {
   void counters(int rank, fcdp_counters* out) const;
   void reset_counters();
 
+  void set_timing(bool on) { timing_ = on; }
+  void kernel_stats(fcdp_kernel_stats* out, bool reset);
+
   void read_shard(int layer, bool frozen, void* host, std::size_t bytes);
   void read_master(int layer, float* host, std::size_t count);
   void read_grad(int layer, float* host, std::size_t count);
@@ -170,6 +173,19 @@ class Engine {
   fcdp_compute_fn compute_fn_ = nullptr;
   void* compute_user_ = nullptr;
   bool use_ce_ = false;
+
+  // kernel accounting (launch counts always, event timing when enabled)
+  template <typename F>
+  void timed(int cls, cudaStream_t s, std::uint64_t alg_bytes, F&& launch);
+  struct TimedLaunch {
+    int cls;
+    cudaEvent_t a, b;
+    std::uint64_t bytes;
+  };
+  bool timing_ = false;
+  std::vector<TimedLaunch> timed_pending_;
+  std::vector<cudaEvent_t> timing_pool_;
+  fcdp_kernel_stats kstats_{};
 };
 
 }  // namespace fcdp

@@ -83,6 +83,12 @@ int fcdp_engine_last_gathered(fcdp_engine* e, int32_t, void*, size_t) {
   });
 }
 
+int fcdp_engine_set_timing(fcdp_engine* e, int32_t on) { return guarded([&] { E(e).set_timing(on != 0); }); }
+
+int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t reset) {
+  return guarded([&] { E(e).kernel_stats(out, reset != 0); });
+}
+
 int fcdp_nic_selftest(const char* name, int32_t rank, int32_t nodes, int32_t local, double bw, uint64_t payload,
                       int32_t rounds, double* elapsed) {
   return guarded([&] {

@@ -121,6 +121,18 @@ class Engine:
     def reset_counters(self) -> None:
         check(lib().fcdp_engine_reset_counters(self._h))
 
+    KERNEL_CLASSES = ("gather_expand", "rs_slice", "rs_finalize", "adamw")
+
+    def set_timing(self, on: bool) -> None:
+        check(lib().fcdp_engine_set_timing(self._h, int(on)))
+
+    def kernel_stats(self, reset: bool = True) -> Dict[str, Dict[str, float]]:
+        k = _capi.KernelStats()
+        check(lib().fcdp_engine_kernel_stats(self._h, C.byref(k), int(reset)))
+        return {name: {"launches": int(k.launches[i]), "ms": float(k.total_ms[i]),
+                       "alg_bytes": int(k.alg_bytes[i]), "timed_launches": int(k.timed_launches[i])}
+                for i, name in enumerate(self.KERNEL_CLASSES)}
+
     # ----------------------------------------------------------- readback
     def read_shard(self, layer: int, frozen: bool, nbytes: int) -> np.ndarray:
         out = np.zeros(nbytes, np.uint8)

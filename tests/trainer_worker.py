@@ -1,0 +1,45 @@
+"""One rank of a training-parity job (launched by tests/test_trainer_gpu.py)."""
+import json
+import os
+import pickle
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    cfg = json.loads(sys.argv[1])
+    import torch
+    from paper_2602_06499_b200 import shardsim as S
+    from paper_2602_06499_b200.driving_model import PRESETS
+    from paper_2602_06499_b200.trainer import FcdpTrainer, synthetic_batch
+    rank, N, g = cfg["rank"], cfg["N"], cfg["g"]
+    dev = rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
+    mc = PRESETS[cfg["preset"]]
+    topo = S.make_topology(N, g)
+    plan = S.StrategyPlan(S.StrategyKind.from_string(cfg["strategy"]))
+    t = FcdpTrainer(mc, topo, plan, rank=rank, world_size=N * g, device=dev, shm_name=cfg["shm"],
+                    batch_per_gpu=cfg["batch"], seed=cfg["seed"], nic_pacing=False, lr=cfg["lr"],
+                    weight_decay=cfg["wd"])
+    losses = []
+    for step in range(1, cfg["steps"] + 1):
+        x, y = synthetic_batch(mc.vocab, cfg["batch"], mc.seq, cfg["seed"], step, rank, device=t.device)
+        loss = t.step(x, y)
+        t.sync()
+        losses.append(float(loss.item()))
+    shards = {}
+    for l, d in enumerate(t.defs):
+        from oracle import oracle as O
+        geo = O.geom(d.numel * mc.dtype_bytes // 16, d.chunk_mask(mc.dtype_bytes), N, g)
+        shards[l] = (t.engine.read_shard(l, False, geo.shard_t * 16), t.engine.read_shard(l, True, geo.shard_f * 16))
+    with open(os.path.join(cfg["out"], f"rank{rank}.pkl"), "wb") as f:
+        pickle.dump({"losses": losses, "shards": shards}, f)
+    t.engine.barrier()
+    t.close()
+
+
+if __name__ == "__main__":
+    main()
