@@ -317,6 +317,12 @@ typedef struct fcdp_kernel_stats {
 int fcdp_engine_set_timing(fcdp_engine* e, int32_t on);
 int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t reset);
 
+/* Executed-event trace of the last fcdp_engine_run (when tracing is on): for
+ * every program event, the device time (ms, relative to the iteration start)
+ * at which its stream reached it (begin) and finished it (end). */
+int fcdp_engine_set_trace(fcdp_engine* e, int32_t on);
+int fcdp_engine_trace(fcdp_engine* e, float* begin_ms, float* end_ms, uint32_t capacity, uint32_t* count);
+
 /* Host-only protocol self-test (no GPU needed): attach the shared control
  * block, run `rounds` barrier-separated rounds in which every rank charges
  * `payload` bytes to its node's NIC emulator, return the wall time.  A node's

@@ -165,6 +165,8 @@ SIGNATURES = {
     "fcdp_engine_destroy": (None, [P]),
     "fcdp_engine_set_timing": (C.c_int, [P, i32]),
     "fcdp_engine_kernel_stats": (C.c_int, [P, C.POINTER(KernelStats), i32]),
+    "fcdp_engine_set_trace": (C.c_int, [P, i32]),
+    "fcdp_engine_trace": (C.c_int, [P, C.POINTER(f32), C.POINTER(f32), u32, C.POINTER(u32)]),
     "fcdp_nic_selftest": (C.c_int, [C.c_char_p, i32, i32, i32, f64, u64, i32, C.POINTER(f64)]),
 }
 

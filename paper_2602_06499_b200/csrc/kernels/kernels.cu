@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "kernels/kernels.hpp"
 
@@ -186,20 +187,19 @@ struct RsArgs {
   int local;
 };
 
-template <typename T>
+template <typename T, int kG>
 __device__ __forceinline__ void rs_emit(const RsArgs& a, const GradPtrs& g, std::int64_t c,
                                         std::int64_t rel, float* own_out, uint4* wire_out) {
   constexpr int V = Vec<T>::kN;
-  uint4 q[kMaxLocal];
+  uint4 q[kG];
 #pragma unroll
-  for (int i = 0; i < kMaxLocal; ++i)
-    if (i < a.local) q[i] = static_cast<const uint4*>(g.p[i])[c];
+  for (int i = 0; i < kG; ++i) q[i] = static_cast<const uint4*>(g.p[i])[c];
   float acc[V];
 #pragma unroll
   for (int e = 0; e < V; ++e) acc[e] = 0.0f;
 #pragma unroll
-  for (int i = 0; i < kMaxLocal; ++i)  // fixed order 0..g-1: deterministic
-    if (i < a.local) Vec<T>::add(acc, q[i]);
+  for (int i = 0; i < kG; ++i)  // fixed order 0..g-1: deterministic
+    Vec<T>::add(acc, q[i]);
   if (rel >= a.own_lo && rel < a.own_hi) {
     float4* o = reinterpret_cast<float4*>(own_out + (rel - a.own_lo) * V);
 #pragma unroll
@@ -218,7 +218,7 @@ __device__ __forceinline__ void rs_emit(const RsArgs& a, const GradPtrs& g, std:
   }
 }
 
-template <typename T>
+template <typename T, int kG>
 __global__ void __launch_bounds__(kThreads) rs_masked_kernel(LayoutDev L, GradPtrs g, RsArgs a,
                                                              std::int64_t wb, std::int64_t we,
                                                              float* __restrict__ own_out,
@@ -233,17 +233,22 @@ __global__ void __launch_bounds__(kThreads) rs_masked_kernel(LayoutDev L, GradPt
     const bool tr = valid && ((__ldg(L.bits + w) >> lane) & 1u);
     const unsigned ballot = __ballot_sync(kFull, tr);
     const std::int64_t kt = static_cast<std::int64_t>(__ldg(L.tpre + w)) + __popc(ballot & below);
-    if (tr && kt >= a.k0 && kt < a.k1) rs_emit<T>(a, g, c, kt - a.k0, own_out, wire_out);
+    if (tr && kt >= a.k0 && kt < a.k1) rs_emit<T, kG>(a, g, c, kt - a.k0, own_out, wire_out);
   }
 }
 
-template <typename T>
+template <typename T, int kG>
 __global__ void __launch_bounds__(kThreads) rs_dense_kernel(GradPtrs g, RsArgs a, float* __restrict__ own_out,
                                                             uint4* __restrict__ wire_out) {
   const std::int64_t n = a.k1 - a.k0;
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    rs_emit<T>(a, g, a.k0 + i, i, own_out, wire_out);
+  std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // two chunks per lane per trip: 2*g independent 16-byte loads in flight
+  for (; i + stride < n; i += 2 * stride) {
+    rs_emit<T, kG>(a, g, a.k0 + i, i, own_out, wire_out);
+    rs_emit<T, kG>(a, g, a.k0 + i + stride, i + stride, own_out, wire_out);
+  }
+  for (; i < n; i += stride) rs_emit<T, kG>(a, g, a.k0 + i, i, own_out, wire_out);
 }
 
 template <typename T>
@@ -262,25 +267,67 @@ __global__ void __launch_bounds__(kThreads) rs_finalize_kernel(std::int64_t n, i
 }
 
 // -------------------------------------------------------------------- Adam
+__device__ __forceinline__ float adam_one(const AdamParams& p, float omb1, float omb2, float g, float& w,
+                                          float& m, float& v) {
+  const float mi = __fmaf_rn(p.beta1, m, __fmul_rn(omb1, g));
+  const float vi = __fmaf_rn(p.beta2, v, __fmul_rn(__fmul_rn(omb2, g), g));
+  const float mhat = __fdiv_rn(mi, p.bias_c1);
+  const float vhat = __fdiv_rn(vi, p.bias_c2);
+  const float denom = __fadd_rn(__fsqrt_rn(vhat), p.eps);
+  const float upd = __fadd_rn(__fdiv_rn(mhat, denom), __fmul_rn(p.weight_decay, w));
+  w = __fsub_rn(w, __fmul_rn(p.lr, upd));
+  m = mi;
+  v = vi;
+  return w;
+}
+
+template <typename T>
+__device__ __forceinline__ void store4(void* param, std::int64_t i4, const float4& w);
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(void* param, std::int64_t i4, const float4& w) {
+  uint2 q;
+  __nv_bfloat162 a = __floats2bfloat162_rn(w.x, w.y), b = __floats2bfloat162_rn(w.z, w.w);
+  q.x = *reinterpret_cast<unsigned*>(&a);
+  q.y = *reinterpret_cast<unsigned*>(&b);
+  __stcs(static_cast<uint2*>(param) + i4, q);
+}
+template <>
+__device__ __forceinline__ void store4<float>(void* param, std::int64_t i4, const float4& w) {
+  __stcs(static_cast<float4*>(param) + i4, w);
+}
+
+// AdamW over the fp32 trainable arena: 16-byte vectors (4 elements per lane),
+// streaming cache hints (every byte is touched once per step).
 template <typename T>
 __global__ void __launch_bounds__(kThreads) adam_kernel(std::int64_t n, AdamParams p, float* __restrict__ master,
                                                         float* __restrict__ m, float* __restrict__ v,
                                                         const float* __restrict__ grad, void* __restrict__ param) {
   const float omb1 = __fsub_rn(1.0f, p.beta1), omb2 = __fsub_rn(1.0f, p.beta2);
+  const std::int64_t n4 = n / 4;
   const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += step) {
-    const float g = grad[i];
-    float w = master[i];
-    const float mi = __fmaf_rn(p.beta1, m[i], __fmul_rn(omb1, g));
-    const float vi = __fmaf_rn(p.beta2, v[i], __fmul_rn(__fmul_rn(omb2, g), g));
-    const float mhat = __fdiv_rn(mi, p.bias_c1);
-    const float vhat = __fdiv_rn(vi, p.bias_c2);
-    const float denom = __fadd_rn(__fsqrt_rn(vhat), p.eps);
-    const float upd = __fadd_rn(__fdiv_rn(mhat, denom), __fmul_rn(p.weight_decay, w));
-    w = __fsub_rn(w, __fmul_rn(p.lr, upd));
-    m[i] = mi;
-    v[i] = vi;
+  const std::int64_t tid = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  float4* W4 = reinterpret_cast<float4*>(master);
+  float4* M4 = reinterpret_cast<float4*>(m);
+  float4* V4 = reinterpret_cast<float4*>(v);
+  const float4* G4 = reinterpret_cast<const float4*>(grad);
+  for (std::int64_t i = tid; i < n4; i += step) {
+    const float4 g = __ldcs(G4 + i);
+    float4 w = __ldcs(W4 + i), mm = __ldcs(M4 + i), vv = __ldcs(V4 + i);
+    adam_one(p, omb1, omb2, g.x, w.x, mm.x, vv.x);
+    adam_one(p, omb1, omb2, g.y, w.y, mm.y, vv.y);
+    adam_one(p, omb1, omb2, g.z, w.z, mm.z, vv.z);
+    adam_one(p, omb1, omb2, g.w, w.w, mm.w, vv.w);
+    __stcs(W4 + i, w);
+    __stcs(M4 + i, mm);
+    __stcs(V4 + i, vv);
+    store4<T>(param, i, w);
+  }
+  for (std::int64_t i = n4 * 4 + tid; i < n; i += step) {
+    float w = master[i], mm = m[i], vv = v[i];
+    adam_one(p, omb1, omb2, grad[i], w, mm, vv);
     master[i] = w;
+    m[i] = mm;
+    v[i] = vv;
     Vec<T>::store1(param, i, w);
   }
 }
@@ -396,20 +443,33 @@ cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n
   a.local = L.dev.local;
   uint4* wire = static_cast<uint4*>(wire_out);
   const bool bf16 = L.dev.elem_bytes == 2;
-  if (L.dense_trainable()) {
-    const int grid = grid_for(a.k1 - a.k0, kThreads);
-    if (bf16)
-      rs_dense_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(grads, a, own_out, wire);
+  const bool dense = L.dense_trainable();
+  const std::int64_t wb = dense ? 0 : L.rs_word_begin[j], we = dense ? 0 : L.rs_word_end[j];
+  const int grid = dense ? grid_for(a.k1 - a.k0, kThreads * 2) : grid_for((we - wb) * 32, kThreads);
+  auto go = [&](auto tag_t, auto tag_g) {
+    using T = decltype(tag_t);
+    constexpr int G = decltype(tag_g)::value;
+    if (dense)
+      rs_dense_kernel<T, G><<<grid, kThreads, 0, s>>>(grads, a, own_out, wire);
     else
-      rs_dense_kernel<float><<<grid, kThreads, 0, s>>>(grads, a, own_out, wire);
-  } else {
-    const std::int64_t wb = L.rs_word_begin[j], we = L.rs_word_end[j];
-    const int grid = grid_for((we - wb) * 32, kThreads);
-    if (bf16)
-      rs_masked_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(L.dev, grads, a, wb, we, own_out, wire);
-    else
-      rs_masked_kernel<float><<<grid, kThreads, 0, s>>>(L.dev, grads, a, wb, we, own_out, wire);
-  }
+      rs_masked_kernel<T, G><<<grid, kThreads, 0, s>>>(L.dev, grads, a, wb, we, own_out, wire);
+  };
+  auto by_g = [&](auto tag_t) {
+    switch (L.dev.local) {
+      case 1: go(tag_t, std::integral_constant<int, 1>{}); break;
+      case 2: go(tag_t, std::integral_constant<int, 2>{}); break;
+      case 4: go(tag_t, std::integral_constant<int, 4>{}); break;
+      case 8: go(tag_t, std::integral_constant<int, 8>{}); break;
+      case 3: go(tag_t, std::integral_constant<int, 3>{}); break;
+      case 5: go(tag_t, std::integral_constant<int, 5>{}); break;
+      case 6: go(tag_t, std::integral_constant<int, 6>{}); break;
+      default: go(tag_t, std::integral_constant<int, 7>{}); break;
+    }
+  };
+  if (bf16)
+    by_g(__nv_bfloat16{});
+  else
+    by_g(float{});
   return cudaGetLastError();
 }
 
@@ -430,7 +490,7 @@ cudaError_t launch_rs_finalize(std::int64_t n_elems, int nodes, int node, int el
 cudaError_t launch_adam(std::int64_t n, const AdamParams& p, float* master, float* m, float* v,
                         const float* grad, void* param, int param_elem_bytes, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  const int grid = grid_for(n, kThreads);
+  const int grid = grid_for(n / 4 + 1, kThreads);
   if (param_elem_bytes == 2)
     adam_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(n, p, master, m, v, grad, param);
   else

@@ -169,6 +169,9 @@ Engine::~Engine() {
   for (cudaEvent_t e : staged_) cudaEventDestroy(e);
   for (cudaEvent_t e : rs_done_) cudaEventDestroy(e);
   for (cudaEvent_t e : timing_pool_) cudaEventDestroy(e);
+  for (cudaEvent_t e : trace_begin_) cudaEventDestroy(e);
+  for (cudaEvent_t e : trace_end_) cudaEventDestroy(e);
+  if (trace_start_) cudaEventDestroy(trace_start_);
   for (const TimedLaunch& t : timed_pending_) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -752,6 +755,23 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     if (e.kind == EventKind::ComputeFwd) last_fwd = e.id;
   }
   for (cudaStream_t s : {s_gather_, s_cache_, s_rs_}) CK(cudaStreamWaitEvent(s, iter_done_, 0));
+  if (trace_) {
+    auto grow = [&](std::vector<cudaEvent_t>& v) {
+      while (v.size() < n_ev) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        v.push_back(e);
+      }
+    };
+    grow(trace_begin_);
+    grow(trace_end_);
+    if (!trace_start_) CK(cudaEventCreate(&trace_start_));
+    CK(cudaEventRecord(trace_start_, s_comp_));
+    for (cudaStream_t s : {s_gather_, s_cache_, s_rs_}) CK(cudaStreamWaitEvent(s, trace_start_, 0));
+    traced_events_ = static_cast<std::uint32_t>(n_ev);
+  } else {
+    traced_events_ = 0;
+  }
   std::fill(x_of_t_.begin(), x_of_t_.end(), -1);
   std::fill(x_of_f_.begin(), x_of_f_.end(), -1);
   std::fill(w_of_layer_.begin(), w_of_layer_.end(), -1);
@@ -761,6 +781,7 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     for (shardsim::EventId d : e.deps)
       if (stream_of[d] != s) CK(cudaStreamWaitEvent(s, ev_done_[d], 0));
     const bool bwd = e.id > last_fwd;
+    if (trace_) CK(cudaEventRecord(trace_begin_[e.id], s));
     switch (e.kind) {
       case EventKind::AgInter: ev_ag_inter(e, bwd); break;
       case EventKind::H2D: ev_h2d(e); break;
@@ -775,6 +796,7 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
         throw shardsim::ConfigError("engine: broadcast events (zero2) are not part of this data plane");
     }
     CK(cudaEventRecord(ev_done_[e.id], s));
+    if (trace_) CK(cudaEventRecord(trace_end_[e.id], s));
   }
   // join: the next iteration starts after everything of this one
   const cudaStream_t side[3] = {s_gather_, s_cache_, s_rs_};
@@ -790,6 +812,16 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     }
   states = shardsim::step_state(std::move(states), prog);
   prog_ = nullptr;
+}
+
+std::uint32_t Engine::trace(float* begin_ms, float* end_ms, std::uint32_t capacity) {
+  sync();
+  const std::uint32_t n = std::min(capacity, traced_events_);
+  for (std::uint32_t i = 0; i < n; ++i) {
+    CK(cudaEventElapsedTime(&begin_ms[i], trace_start_, trace_begin_[i]));
+    CK(cudaEventElapsedTime(&end_ms[i], trace_start_, trace_end_[i]));
+  }
+  return traced_events_;
 }
 
 void Engine::sync() {

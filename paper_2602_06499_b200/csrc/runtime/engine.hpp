@@ -77,6 +77,8 @@ class Engine {
 
   void set_timing(bool on) { timing_ = on; }
   void kernel_stats(fcdp_kernel_stats* out, bool reset);
+  void set_trace(bool on) { trace_ = on; }
+  std::uint32_t trace(float* begin_ms, float* end_ms, std::uint32_t capacity);
 
   void read_shard(int layer, bool frozen, void* host, std::size_t bytes);
   void read_master(int layer, float* host, std::size_t count);
@@ -186,6 +188,10 @@ class Engine {
   std::vector<TimedLaunch> timed_pending_;
   std::vector<cudaEvent_t> timing_pool_;
   fcdp_kernel_stats kstats_{};
+  bool trace_ = false;
+  std::uint32_t traced_events_ = 0;
+  cudaEvent_t trace_start_ = nullptr;
+  std::vector<cudaEvent_t> trace_begin_, trace_end_;
 };
 
 }  // namespace fcdp

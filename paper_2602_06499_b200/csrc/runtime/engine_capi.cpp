@@ -89,6 +89,12 @@ int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t res
   return guarded([&] { E(e).kernel_stats(out, reset != 0); });
 }
 
+int fcdp_engine_set_trace(fcdp_engine* e, int32_t on) { return guarded([&] { E(e).set_trace(on != 0); }); }
+
+int fcdp_engine_trace(fcdp_engine* e, float* begin_ms, float* end_ms, uint32_t capacity, uint32_t* count) {
+  return guarded([&] { *count = E(e).trace(begin_ms, end_ms, capacity); });
+}
+
 int fcdp_nic_selftest(const char* name, int32_t rank, int32_t nodes, int32_t local, double bw, uint64_t payload,
                       int32_t rounds, double* elapsed) {
   return guarded([&] {

@@ -206,5 +206,5 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         else:
             a = F.rms_norm(x, (h,), p["norm_w"], eps=1e-5)
         logits = F.linear(a, p["lm_w"])
-        return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), labels.view(-1))
+        return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), labels.reshape(-1))
     raise ValueError(ldef.kind)

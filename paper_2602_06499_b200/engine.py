@@ -133,6 +133,18 @@ class Engine:
                        "alg_bytes": int(k.alg_bytes[i]), "timed_launches": int(k.timed_launches[i])}
                 for i, name in enumerate(self.KERNEL_CLASSES)}
 
+    def set_trace(self, on: bool) -> None:
+        check(lib().fcdp_engine_set_trace(self._h, int(on)))
+
+    def trace(self, program: EventProgram):
+        """[(event, begin_ms, end_ms)] of the last run (tracing must be on)."""
+        n = len(program.events)
+        b = (C.c_float * max(n, 1))()
+        e = (C.c_float * max(n, 1))()
+        cnt = C.c_uint32()
+        check(lib().fcdp_engine_trace(self._h, b, e, n, C.byref(cnt)))
+        return [(ev, b[i], e[i]) for i, ev in enumerate(program.events[:cnt.value])]
+
     # ----------------------------------------------------------- readback
     def read_shard(self, layer: int, frozen: bool, nbytes: int) -> np.ndarray:
         out = np.zeros(nbytes, np.uint8)

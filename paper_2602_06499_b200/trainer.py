@@ -123,6 +123,13 @@ class FcdpTrainer:
                 train = [t.name for t in ldef.tensors if t.trainable]
                 inputs = ([x_in] if x_in is not None else []) + [p[n] for n in train]
                 grad_out = None if ldef.kind == "head" else self._grad_act
+                if not inputs or not y.requires_grad:
+                    # nothing upstream needs a gradient (e.g. a frozen embedding under PEFT)
+                    self._bwd_w.pop(layer, None)
+                    self._grad_act = None
+                    if layer == 0:
+                        self._saved_out = None
+                    return
                 grads = torch.autograd.grad(y, inputs, grad_outputs=grad_out, allow_unused=True)
                 self._bwd_w.pop(layer, None)
                 if x_in is not None:
