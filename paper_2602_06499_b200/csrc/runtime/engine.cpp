@@ -496,12 +496,16 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
   unsigned char* X = x_slot(j_, slot);
   unsigned char* Xf = X + l.L.dev.slice_t * C;
   // own shard -> its position n in this GPU's slice (global shard j*N + n)
+  // (an SM copy, not cudaMemcpy: the copy engines are busy with FCDP-Cache D2H
+  //  and host-staged NIC traffic, and a D2D queued behind them stalls the gather)
   if (wt && l.my_real_t)
-    CK(cudaMemcpyAsync(X + n_ * l.L.dev.shard_t * C, param_t_ + l.off_t * C, l.my_real_t * C,
-                       cudaMemcpyDeviceToDevice, s));
+    timed(0, s, 2 * l.my_real_t * C, [&] {
+      return launch_copy(param_t_ + l.off_t * C, X + n_ * l.L.dev.shard_t * C, l.my_real_t * C, s);
+    });
   if (wf && l.my_real_f)
-    CK(cudaMemcpyAsync(Xf + n_ * l.L.dev.shard_f * C, param_f_ + l.off_f * C, l.my_real_f * C,
-                       cudaMemcpyDeviceToDevice, s));
+    timed(0, s, 2 * l.my_real_f * C, [&] {
+      return launch_copy(param_f_ + l.off_f * C, Xf + n_ * l.L.dev.shard_f * C, l.my_real_f * C, s);
+    });
   if (N_ > 1) {
     // Inter-node all-gather among {(n', j)} through the host-staged NIC path.
     const std::uint32_t seq = ++seq_ag_;
