@@ -48,6 +48,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--copy-engine", action="store_true")
+    p.add_argument("--watchdog", type=float, default=1200.0,
+                   help="dump every thread's stack and exit if the run exceeds this many seconds")
+    p.add_argument("--engine-timeout", type=float, default=300.0)
+    p.add_argument("--no-pacing", action="store_true", help="do not throttle the emulated inter-node link")
     return p.parse_args()
 
 
@@ -163,6 +167,8 @@ def workload_config(args, mc, N, g, world, seq):
 def main():
     args = parse()
     rank, world, local = env_rank()
+    import faulthandler
+    faulthandler.dump_traceback_later(args.watchdog, exit=True)
     if args.impl == "reference":
         run_reference(args, args.gpus if world == 1 else world)
         return
@@ -216,8 +222,8 @@ def main():
         plan = S.StrategyPlan(S.StrategyKind.from_string(strategy))
         shm = bcast(f"fcdp_bench_{uuid.uuid4().hex[:12]}" if rank == 0 else None)
         tr = FcdpTrainer(mc, topo, plan, rank=rank, world_size=world, device=local, shm_name=shm,
-                         batch_per_gpu=args.batch, seq_len=seq, nic_pacing=True, lr=1e-4,
-                         use_copy_engine=args.copy_engine)
+                         batch_per_gpu=args.batch, seq_len=seq, nic_pacing=not args.no_pacing, lr=1e-4,
+                         use_copy_engine=args.copy_engine, timeout_s=args.engine_timeout)
         batches = [synthetic_batch(mc.vocab, args.batch, seq, 0x5EED, i, rank, device=dev)
                    for i in range(warmup + steps)]
         for i in range(warmup):

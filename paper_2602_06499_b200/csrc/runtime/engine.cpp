@@ -15,7 +15,11 @@
 #include "runtime/engine.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <thread>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -780,8 +784,12 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
   std::fill(x_of_f_.begin(), x_of_f_.end(), -1);
   std::fill(w_of_layer_.begin(), w_of_layer_.end(), -1);
 
+  static const bool debug = std::getenv("FCDP_DEBUG") != nullptr;
   for (const Event& e : prog.events) {
     cudaStream_t s = stream_of[e.id];
+    if (debug)
+      std::fprintf(stderr, "[fcdp r%d] it=%llu enqueue ev %u %s layer %d\n", rank_,
+                   static_cast<unsigned long long>(prog.iteration_index), e.id, shardsim::to_string(e.kind), e.layer);
     for (shardsim::EventId d : e.deps)
       if (stream_of[d] != s) CK(cudaStreamWaitEvent(s, ev_done_[d], 0));
     const bool bwd = e.id > last_fwd;
@@ -829,8 +837,31 @@ std::uint32_t Engine::trace(float* begin_ms, float* end_ms, std::uint32_t capaci
 }
 
 void Engine::sync() {
-  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_})
-    if (s) CK(cudaStreamSynchronize(s));
+  // Poll instead of blocking so a cross-rank wait that can never be satisfied
+  // (a peer died, a protocol bug) ends in a diagnosable TimeoutError.
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(cfg_.timeout_s);
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_}) {
+    if (!s) continue;
+    for (int spin = 0;; ++spin) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) CK(q);
+      if (std::chrono::steady_clock::now() > deadline) {
+        std::string msg = "engine: rank " + std::to_string(rank_) + " stream did not drain within timeout; " +
+                          "seq q=" + std::to_string(q_) + " ag=" + std::to_string(seq_ag_) + " rs=" +
+                          std::to_string(seq_rs_) + " u=" + std::to_string(u_) + "; flags:";
+        for (int r = 0; r < G_; ++r) {
+          msg += " [r" + std::to_string(r);
+          for (int f = 0; f < kNumFlags; ++f) msg += " " + std::to_string(*shm_->flag(r, static_cast<Flag>(f)));
+          msg += "]";
+        }
+        std::fprintf(stderr, "%s\n", msg.c_str());
+        shm_->header()->abort_flag.store(1);
+        throw TimeoutError(msg);
+      }
+      if (spin > 100) std::this_thread::sleep_for(std::chrono::microseconds(spin > 10000 ? 1000 : 50));
+    }
+  }
 }
 
 void Engine::barrier() { shm_->barrier(cfg_.timeout_s); }
