@@ -382,6 +382,7 @@ unsigned char* Engine::grad_slot(int jj, int slot) const {
 }
 
 void Engine::wait_flag(cudaStream_t s, int rank, Flag f, std::uint32_t v) {
+  shm_->await_posted(rank, f, v, cfg_.timeout_s);
   const auto off = reinterpret_cast<const volatile unsigned char*>(shm_->flag(rank, f)) -
                    static_cast<const volatile unsigned char*>(shm_->base());
   StreamOps::wait_geq(s, reinterpret_cast<const volatile std::uint32_t*>(
@@ -392,6 +393,7 @@ void Engine::write_flag(cudaStream_t s, Flag f, std::uint32_t v) {
   const auto off = reinterpret_cast<unsigned char*>(const_cast<std::uint32_t*>(shm_->flag(rank_, f))) -
                    static_cast<unsigned char*>(shm_->base());
   StreamOps::write(s, reinterpret_cast<volatile std::uint32_t*>(static_cast<unsigned char*>(shm_dev_base_) + off), v);
+  shm_->post(rank_, f, v);
 }
 
 cudaStream_t Engine::stream_for(EventKind k) const {
@@ -486,6 +488,7 @@ void Engine::inter_send(int cls, cudaStream_t s, std::uint32_t seq,
   cudaEvent_t ev = staged_[staged_next_++ % staged_.size()];
   CK(cudaEventRecord(ev, s));
   nic_->submit({cls, seq, ev, wire_bytes, counter});
+  shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, seq);
 }
 
 // ------------------------------------------------------------------ events
@@ -710,6 +713,7 @@ void Engine::ev_reduce_scatter(const Event& e) {
   cudaEvent_t ev = staged_[staged_next_++ % staged_.size()];
   CK(cudaEventRecord(ev, s));
   nic_->submit({1, seq, ev, wire, kTxRs});
+  shm_->post(rank_, kRsTxReady, seq);
   std::uint64_t rx = 0;
   for (int nn = 0; nn < N_; ++nn) {
     if (nn == n_) continue;

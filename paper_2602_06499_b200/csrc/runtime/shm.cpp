@@ -105,6 +105,22 @@ void SharedBlock::reset_counters(int rank) const {
   for (auto& c : hdr_->ranks[rank].counters) c.store(0, std::memory_order_relaxed);
 }
 
+void SharedBlock::await_posted(int rank, Flag f, std::uint32_t v, double timeout_s) const {
+  auto& c = hdr_->ranks[rank].posted[f];
+  if (static_cast<std::int32_t>(c.load(std::memory_order_acquire) - v) >= 0) return;
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
+  int spins = 0;
+  while (static_cast<std::int32_t>(c.load(std::memory_order_acquire) - v) < 0) {
+    if (hdr_->abort_flag.load(std::memory_order_relaxed)) throw TimeoutError("engine: job aborted by a peer");
+    if (++spins > 2000) {
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+      if (std::chrono::steady_clock::now() > deadline)
+        throw TimeoutError("engine: rank " + std::to_string(rank) + " never posted flag " + std::to_string(f) +
+                           " >= " + std::to_string(v));
+    }
+  }
+}
+
 void SharedBlock::barrier(double timeout_s) const {
   const std::uint32_t gen = hdr_->barrier_gen.load(std::memory_order_acquire);
   if (hdr_->barrier_count.fetch_add(1, std::memory_order_acq_rel) + 1 ==

@@ -46,6 +46,11 @@ struct alignas(64) FlagLine {
 
 struct alignas(64) RankBlock {
   FlagLine flags[kNumFlags];
+  // Host-side "posted" counters: the value this rank's host has ENQUEUED a
+  // write of, per flag.  A rank only enqueues a stream wait on a peer flag once
+  // the peer has posted the matching write, so no GPU wait ever depends on
+  // work a (possibly blocked) peer host has not issued yet.
+  std::atomic<std::uint32_t> posted[kNumFlags];
   std::atomic<std::uint64_t> counters[kNumCounters];
   unsigned char ipc_handle[64];  // cudaIpcMemHandle_t of the peer arena
   std::uint64_t arena_bytes;
@@ -94,6 +99,11 @@ class SharedBlock {
     return hdr_->ranks[rank].counters[c].load(std::memory_order_relaxed);
   }
   void reset_counters(int rank) const;
+  void post(int rank, Flag f, std::uint32_t v) const {
+    hdr_->ranks[rank].posted[f].store(v, std::memory_order_release);
+  }
+  // Spin (host) until `rank` has posted >= v for flag f.
+  void await_posted(int rank, Flag f, std::uint32_t v, double timeout_s) const;
 
   // Host barrier over all ranks (sense-reversing on a generation counter).
   void barrier(double timeout_s) const;

@@ -3,6 +3,7 @@ import json
 import os
 import pickle
 import sys
+os_env_set = __import__('os').environ.setdefault('CUDA_DEVICE_MAX_CONNECTIONS', '32')
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]

@@ -9,6 +9,7 @@ import argparse
 import json
 import os
 import sys
+os_env_set = __import__('os').environ.setdefault('CUDA_DEVICE_MAX_CONNECTIONS', '32')
 import uuid
 from collections import defaultdict
 from pathlib import Path
