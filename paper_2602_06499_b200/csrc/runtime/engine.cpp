@@ -154,7 +154,7 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   for (auto& e : staged_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
   exchange_handles();
-  nic_ = std::make_unique<NicEmulator>(*shm_, rank_, n_, cfg_.device, topo_.inter_node.bandwidth_bytes_per_s,
+  nic_ = std::make_unique<NicEmulator>(*shm_, rank_, n_, topo_.inter_node.bandwidth_bytes_per_s,
                                        cfg_.nic_pacing != 0);
   shm_->barrier(cfg_.timeout_s);
 }
@@ -485,9 +485,8 @@ void Engine::inter_send(int cls, cudaStream_t s, std::uint32_t seq,
     staged += bytes;
   }
   shm_->add(rank_, kStagingD2H, staged);
-  cudaEvent_t ev = staged_[staged_next_++ % staged_.size()];
-  CK(cudaEventRecord(ev, s));
-  nic_->submit({cls, seq, ev, wire_bytes, counter});
+  write_flag(s, cls == 0 ? kAgStaged : kRsStaged, seq);
+  nic_->submit({cls, seq, wire_bytes, counter});
   shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, seq);
 }
 
@@ -710,9 +709,8 @@ void Engine::ev_reduce_scatter(const Event& e) {
     wire += real * C;
   }
   shm_->add(rank_, kStagingD2H, wire);
-  cudaEvent_t ev = staged_[staged_next_++ % staged_.size()];
-  CK(cudaEventRecord(ev, s));
-  nic_->submit({1, seq, ev, wire, kTxRs});
+  write_flag(s, kRsStaged, seq);
+  nic_->submit({1, seq, wire, kTxRs});
   shm_->post(rank_, kRsTxReady, seq);
   std::uint64_t rx = 0;
   for (int nn = 0; nn < N_; ++nn) {

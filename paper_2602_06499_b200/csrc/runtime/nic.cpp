@@ -4,8 +4,8 @@
 
 namespace fcdp {
 
-NicEmulator::NicEmulator(SharedBlock& shm, int rank, int node, int device, double bytes_per_s, bool pacing)
-    : shm_(shm), rank_(rank), node_(node), device_(device), bytes_per_ns_(bytes_per_s / 1e9), pacing_(pacing) {
+NicEmulator::NicEmulator(SharedBlock& shm, int rank, int node, double bytes_per_s, bool pacing)
+    : shm_(shm), rank_(rank), node_(node), bytes_per_ns_(bytes_per_s / 1e9), pacing_(pacing) {
   thread_ = std::thread([this] { loop(); });
 }
 
@@ -31,7 +31,6 @@ std::uint64_t NicEmulator::published(int cls) const {
 }
 
 void NicEmulator::loop() {
-  cudaSetDevice(device_);
   std::unique_lock<std::mutex> lk(mu_);
   for (;;) {
     bool idle = true;
@@ -40,8 +39,8 @@ void NicEmulator::loop() {
       // Staged payloads enter the wire in submission order (per class).
       while (!queue_[c].empty()) {
         NicJob& j = queue_[c].front();
-        const cudaError_t q = cudaEventQuery(j.staged);
-        if (q == cudaErrorNotReady) break;
+        const std::uint32_t staged = __atomic_load_n(shm_.flag(rank_, c == 0 ? kAgStaged : kRsStaged), __ATOMIC_ACQUIRE);
+        if (static_cast<std::int32_t>(staged - j.seq) < 0) break;  // staging copy not landed yet
         const std::uint64_t ns =
             pacing_ && bytes_per_ns_ > 0 ? static_cast<std::uint64_t>(j.wire_bytes / bytes_per_ns_) : 0;
         const std::uint64_t finish = ns ? shm_.reserve_nic(node_, ns) : SharedBlock::now_ns();

@@ -1,5 +1,5 @@
 // NIC emulator: one thread per rank that turns "my staged payload is in host
-// memory" (a CUDA event on the staging D2H) into "my payload has crossed the
+// memory" (a flag the staging stream writes after its D2H) into "my payload has crossed the
 // emulated network" (a flag peers' streams wait on), after charging the
 // payload's wire time to the sending node's single NIC (reference
 // topology.hpp:23-25 "one NIC per node"; "Per-node NIC serializes
@@ -13,8 +13,6 @@
 #include <mutex>
 #include <thread>
 
-#include <cuda_runtime.h>
-
 #include "runtime/shm.hpp"
 
 namespace fcdp {
@@ -22,14 +20,16 @@ namespace fcdp {
 struct NicJob {
   int cls;               // 0 = all-gather, 1 = reduce-scatter
   std::uint32_t seq;     // per-class sequence number, monotone
-  cudaEvent_t staged;    // recorded after the staging D2H
+  // The thread makes NO CUDA calls: a host thread blocked inside a launch
+  // (full pushbuffer) can hold driver locks, and the NIC thread must keep
+  // publishing or the stalled streams it feeds would never drain.
   std::uint64_t wire_bytes;  // bytes this rank puts on its node's NIC
   Counter counter;       // which tx counter to charge
 };
 
 class NicEmulator {
  public:
-  NicEmulator(SharedBlock& shm, int rank, int node, int device, double bytes_per_s, bool pacing);
+  NicEmulator(SharedBlock& shm, int rank, int node, double bytes_per_s, bool pacing);
   ~NicEmulator();
   void submit(const NicJob& job);
   std::uint64_t published(int cls) const;
@@ -41,7 +41,7 @@ class NicEmulator {
     std::uint64_t finish_ns;
   };
   SharedBlock& shm_;
-  int rank_, node_, device_;
+  int rank_, node_;
   double bytes_per_ns_;
   bool pacing_;
   std::mutex mu_;

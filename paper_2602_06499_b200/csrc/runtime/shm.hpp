@@ -31,6 +31,8 @@ enum Flag : int {
   kSliceFree,      // intra gather: I finished pulling peers' slices of seq
   kGradReady,      // intra RS: my natural gradient buffer holds rs seq
   kGradFree,       // intra RS: I finished pulling peers' gradients of seq
+  kAgStaged,       // inter AG: my staging D2H of seq landed in host memory (for my NIC thread)
+  kRsStaged,       // inter RS: same
   kNumFlags
 };
 
