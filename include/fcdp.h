@@ -262,6 +262,7 @@ typedef struct fcdp_engine_config {
   int32_t nic_pacing;       /* 1: pace inter-node traffic at topology inter bandwidth */
   int32_t use_copy_engine;  /* 1: dense intra gathers by cudaMemcpyAsync (CE) not SM kernels */
   double timeout_s;         /* deadline for host-side cross-rank waits */
+  int64_t inter_chunk_bytes; /* NIC emulator wire piece size (0: 4 MiB) */
 } fcdp_engine_config;
 
 /* Counters of one rank (bytes).  Per node = sum over that node's ranks. */

@@ -78,7 +78,8 @@ class InitRange(C.Structure):
 class EngineConfig(C.Structure):
     _fields_ = [("shm_name", C.c_char_p), ("rank", C.c_int32), ("world_size", C.c_int32),
                 ("device", C.c_int32), ("x_slots", C.c_int32), ("inter_slots", C.c_int32),
-                ("nic_pacing", C.c_int32), ("use_copy_engine", C.c_int32), ("timeout_s", C.c_double)]
+                ("nic_pacing", C.c_int32), ("use_copy_engine", C.c_int32), ("timeout_s", C.c_double),
+                ("inter_chunk_bytes", C.c_int64)]
 
 
 class Counters(C.Structure):

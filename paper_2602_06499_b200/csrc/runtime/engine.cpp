@@ -39,8 +39,6 @@ using shardsim::Event;
 using shardsim::EventKind;
 using shardsim::ParamSet;
 
-constexpr int kStagedRing = 32;
-
 std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
 
 template <typename T>
@@ -124,6 +122,8 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   if (cfg_.inter_slots < 2) cfg_.inter_slots = 2;
   if (cfg_.timeout_s <= 0) cfg_.timeout_s = 300.0;
   use_ce_ = cfg_.use_copy_engine != 0;
+  chunk_bytes_ = cfg_.inter_chunk_bytes > 0 ? cfg_.inter_chunk_bytes : (4ll << 20);
+  chunk_bytes_ = (chunk_bytes_ + kChunkBytes - 1) / kChunkBytes * kChunkBytes;
 
   CK(cudaSetDevice(cfg_.device));
   build_layouts(chunk_masks);
@@ -150,8 +150,6 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   for (auto& e : rs_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&iter_done_, cudaEventDisableTiming));
   for (auto& e : join_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  staged_.assign(kStagedRing, nullptr);
-  for (auto& e : staged_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
   exchange_handles();
   nic_ = std::make_unique<NicEmulator>(*shm_, rank_, n_, topo_.inter_node.bandwidth_bytes_per_s,
@@ -170,7 +168,6 @@ Engine::~Engine() {
     if (jj != j_ && peer_base_[jj]) cudaIpcCloseMemHandle(peer_base_[jj]);
   for (cudaEvent_t e : ev_done_) cudaEventDestroy(e);
   for (cudaEvent_t e : x_reader_) cudaEventDestroy(e);
-  for (cudaEvent_t e : staged_) cudaEventDestroy(e);
   for (cudaEvent_t e : rs_done_) cudaEventDestroy(e);
   for (cudaEvent_t e : timing_pool_) cudaEventDestroy(e);
   for (cudaEvent_t e : trace_begin_) cudaEventDestroy(e);
@@ -473,21 +470,37 @@ void Engine::pull_expand(int layer, int slot, std::uint32_t q, bool want_t, bool
   shm_->add(rank_, kNvlinkRx, rx);
 }
 
-void Engine::inter_send(int cls, cudaStream_t s, std::uint32_t seq,
-                        const std::vector<std::pair<const void*, std::size_t>>& parts, std::uint64_t wire_bytes,
-                        Counter counter) {
-  const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
-  unsigned char* dst = shm_->slot(rank_, cls, idx);
-  std::size_t off = 0, staged = 0;
-  for (const auto& [src, bytes] : parts) {
-    if (bytes) CK(cudaMemcpyAsync(dst + off, src, bytes, cudaMemcpyDeviceToHost, s));
-    off += bytes;
-    staged += bytes;
+std::int64_t Engine::pieces_of(std::size_t bytes) const {
+  const std::size_t ch = static_cast<std::size_t>(chunk_bytes_);
+  return bytes == 0 ? 0 : static_cast<std::int64_t>((bytes + ch - 1) / ch);
+}
+
+void Engine::stage_pieces(int cls, cudaStream_t s, unsigned char* slot, const void* src, std::size_t bytes,
+                          std::size_t slot_off, std::uint64_t wire_mult, Counter counter) {
+  // Pipelined host-staged wire: each piece is staged, flagged, and handed to
+  // the NIC thread, which puts it on the emulated wire as soon as it lands.
+  const std::size_t ch = static_cast<std::size_t>(chunk_bytes_);
+  for (std::size_t off = 0; off < bytes; off += ch) {
+    const std::size_t n = std::min(ch, bytes - off);
+    CK(cudaMemcpyAsync(slot + slot_off + off, static_cast<const unsigned char*>(src) + off, n,
+                       cudaMemcpyDeviceToHost, s));
+    const std::uint32_t id = ++sent_pieces_[cls];
+    write_flag(s, cls == 0 ? kAgStaged : kRsStaged, id);
+    nic_->submit({cls, id, n * wire_mult, counter});
+    shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, id);
   }
-  shm_->add(rank_, kStagingD2H, staged);
-  write_flag(s, cls == 0 ? kAgStaged : kRsStaged, seq);
-  nic_->submit({cls, seq, wire_bytes, counter});
-  shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, seq);
+  shm_->add(rank_, kStagingD2H, bytes);
+}
+
+void Engine::receive_pieces(int cls, cudaStream_t s, int src_rank, std::uint32_t first_id, const unsigned char* slot,
+                            std::size_t slot_off, std::size_t bytes, unsigned char* dst) {
+  const std::size_t ch = static_cast<std::size_t>(chunk_bytes_);
+  std::uint32_t id = first_id;
+  for (std::size_t off = 0; off < bytes; off += ch, ++id) {
+    wait_flag(s, src_rank, cls == 0 ? kAgTxReady : kRsTxReady, id);
+    CK(cudaMemcpyAsync(dst + off, slot + slot_off + off, std::min(ch, bytes - off), cudaMemcpyHostToDevice, s));
+  }
+  shm_->add(rank_, kStagingH2D, bytes);
 }
 
 // ------------------------------------------------------------------ events
@@ -513,31 +526,33 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
       return launch_copy(param_f_ + l.off_f * C, Xf + n_ * l.L.dev.shard_f * C, l.my_real_f * C, s);
     });
   if (N_ > 1) {
-    // Inter-node all-gather among {(n', j)} through the host-staged NIC path.
+    // Inter-node all-gather among {(n', j)} through the host-staged NIC path,
+    // pipelined in pieces of chunk_bytes_.
     const std::uint32_t seq = ++seq_ag_;
     const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
     if (seq > static_cast<std::uint32_t>(cfg_.inter_slots))
       for (int nn = 0; nn < N_; ++nn)
         if (nn != n_) wait_flag(s, nn * g_ + j_, kAgRxDone, seq - cfg_.inter_slots);
-    std::vector<std::pair<const void*, std::size_t>> parts;
-    std::uint64_t payload = 0;
-    if (wt) parts.push_back({param_t_ + l.off_t * C, l.my_real_t * C}), payload += l.my_real_t * C;
-    if (wf) parts.push_back({param_f_ + l.off_f * C, l.my_real_f * C}), payload += l.my_real_f * C;
-    inter_send(0, s, seq, parts, payload * static_cast<std::uint64_t>(N_ - 1), backward ? kTxBwdAg : kTxFwdAg);
+    unsigned char* mine = shm_->slot(rank_, 0, idx);
+    const std::size_t bt = wt ? l.my_real_t * C : 0, bf = wf ? l.my_real_f * C : 0;
+    const Counter ctr = backward ? kTxBwdAg : kTxFwdAg;
+    stage_pieces(0, s, mine, param_t_ + l.off_t * C, bt, 0, N_ - 1, ctr);
+    stage_pieces(0, s, mine, param_f_ + l.off_f * C, bf, bt, N_ - 1, ctr);
     std::uint64_t rx = 0;
     for (int nn = 0; nn < N_; ++nn) {
-      if (nn == n_) continue;
       const int src_rank = nn * g_ + j_;
       const int r = j_ * N_ + nn;
-      wait_flag(s, src_rank, kAgTxReady, seq);
+      const std::size_t rt = wt ? l.L.real_chunks(false, r) * C : 0, rf = wf ? l.L.real_chunks(true, r) * C : 0;
+      const std::uint32_t base = recv_base_[0][src_rank];
+      recv_base_[0][src_rank] += static_cast<std::uint32_t>(pieces_of(rt) + pieces_of(rf));
+      if (nn == n_) continue;
       const unsigned char* src = shm_->slot(src_rank, 0, idx);
-      const std::int64_t rt = wt ? l.L.real_chunks(false, r) : 0, rf = wf ? l.L.real_chunks(true, r) : 0;
-      if (rt) CK(cudaMemcpyAsync(X + nn * l.L.dev.shard_t * C, src, rt * C, cudaMemcpyHostToDevice, s));
-      if (rf) CK(cudaMemcpyAsync(Xf + nn * l.L.dev.shard_f * C, src + rt * C, rf * C, cudaMemcpyHostToDevice, s));
-      rx += (rt + rf) * C;
+      receive_pieces(0, s, src_rank, base + 1, src, 0, rt, X + nn * l.L.dev.shard_t * C);
+      receive_pieces(0, s, src_rank, base + 1 + static_cast<std::uint32_t>(pieces_of(rt)), src, rt, rf,
+                     Xf + nn * l.L.dev.shard_f * C);
+      rx += rt + rf;
     }
     write_flag(s, kAgRxDone, seq);
-    shm_->add(rank_, kStagingH2D, rx);
     shm_->add(rank_, backward ? kRxBwdAg : kRxFwdAg, rx);
   }
   finish_slice_fill(slot, q);
@@ -697,34 +712,33 @@ void Engine::ev_reduce_scatter(const Event& e) {
   if (seq > static_cast<std::uint32_t>(cfg_.inter_slots))
     for (int nn = 0; nn < N_; ++nn)
       if (nn != n_) wait_flag(s, nn * g_ + j_, kRsRxDone, seq - cfg_.inter_slots);
-  // stage the slice with the own-shard hole: slot layout == slice layout
-  unsigned char* dst = shm_->slot(rank_, 1, idx);
-  std::uint64_t wire = 0;
+  // stage the slice with the own-shard hole: slot layout == slice layout;
+  // region m (partials of shard j*N+m) goes to node m only.
+  unsigned char* mine = shm_->slot(rank_, 1, idx);
   for (int nn = 0; nn < N_; ++nn) {
     if (nn == n_) continue;
-    const std::int64_t real = l.L.real_chunks(false, j_ * N_ + nn);
-    if (!real) continue;
     const std::size_t off = nn * l.L.dev.shard_t * C;
-    CK(cudaMemcpyAsync(dst + off, wire_[gs] + off, real * C, cudaMemcpyDeviceToHost, s));
-    wire += real * C;
+    stage_pieces(1, s, mine, wire_[gs] + off, l.L.real_chunks(false, j_ * N_ + nn) * C, off, 1, kTxRs);
   }
-  shm_->add(rank_, kStagingD2H, wire);
-  write_flag(s, kRsStaged, seq);
-  nic_->submit({1, seq, wire, kTxRs});
-  shm_->post(rank_, kRsTxReady, seq);
   std::uint64_t rx = 0;
   for (int nn = 0; nn < N_; ++nn) {
     if (nn == n_) continue;
     const int src_rank = nn * g_ + j_;
-    wait_flag(s, src_rank, kRsTxReady, seq);
-    if (l.my_real_t) {
-      CK(cudaMemcpyAsync(rx_[gs] + nn * l.L.dev.shard_t * C, shm_->slot(src_rank, 1, idx) + n_ * l.L.dev.shard_t * C,
-                         l.my_real_t * C, cudaMemcpyHostToDevice, s));
-      rx += l.my_real_t * C;
+    // piece ids of sender (nn, j): its regions m != nn in ascending order; ours is m == n
+    std::uint32_t id = recv_base_[1][src_rank];
+    std::uint32_t mine_first = 0;
+    for (int m = 0; m < N_; ++m) {
+      if (m == nn) continue;
+      if (m == n_) mine_first = id + 1;
+      id += static_cast<std::uint32_t>(pieces_of(l.L.real_chunks(false, j_ * N_ + m) * C));
     }
+    recv_base_[1][src_rank] = id;
+    const std::size_t my = l.my_real_t * C;
+    receive_pieces(1, s, src_rank, mine_first, shm_->slot(src_rank, 1, idx), n_ * l.L.dev.shard_t * C, my,
+                   rx_[gs] + nn * l.L.dev.shard_t * C);
+    rx += my;
   }
   write_flag(s, kRsRxDone, seq);
-  shm_->add(rank_, kStagingH2D, rx);
   shm_->add(rank_, kRxRs, rx);
   const std::uint64_t fin_elems = static_cast<std::uint64_t>(l.L.dev.shard_t) * V_;
   timed(2, s, fin_elems * (2 * sizeof(float) + static_cast<std::uint64_t>(N_ - 1) * eb_), [&] {

@@ -108,8 +108,11 @@ class Engine {
   unsigned char* grad_slot(int rank_local, int slot) const;
   void wait_flag(cudaStream_t s, int rank, Flag f, std::uint32_t v);
   void write_flag(cudaStream_t s, Flag f, std::uint32_t v);
-  void inter_send(int cls, cudaStream_t s, std::uint32_t seq, const std::vector<std::pair<const void*, std::size_t>>& parts,
-                  std::uint64_t wire_bytes, Counter counter);
+  std::int64_t pieces_of(std::size_t bytes) const;
+  void stage_pieces(int cls, cudaStream_t s, unsigned char* slot, const void* src, std::size_t bytes,
+                    std::size_t slot_off, std::uint64_t wire_mult, Counter counter);
+  void receive_pieces(int cls, cudaStream_t s, int src_rank, std::uint32_t first_id, const unsigned char* slot,
+                      std::size_t slot_off, std::size_t bytes, unsigned char* dst);
   bool is_peer_rank(int r) const { return r / g_ == n_; }
 
   fcdp_engine_config cfg_;
@@ -146,11 +149,12 @@ class Engine {
   cudaEvent_t rs_done_[2] = {nullptr, nullptr};
   cudaEvent_t iter_done_ = nullptr;
   cudaEvent_t join_[3] = {nullptr, nullptr, nullptr};
-  std::vector<cudaEvent_t> staged_;    // staging D2H events for the NIC (ring)
-  std::size_t staged_next_ = 0;
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, seq_ag_ = 0, seq_rs_ = 0, u_ = 0;
+  std::int64_t chunk_bytes_ = 4ll << 20;          // inter-node wire piece size
+  std::uint32_t sent_pieces_[2] = {0, 0};         // my cumulative staged pieces per class
+  std::uint32_t recv_base_[2][64] = {};           // replica of every sender's piece counter
   std::uint64_t w_instances_ = 0;
   std::uint32_t grad_slot_seq_ = 0;
   int opt_steps_ = 0;

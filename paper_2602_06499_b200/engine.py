@@ -27,7 +27,7 @@ class Engine:
                  world_size: int, device: int, shm_name: str,
                  chunk_masks: Optional[Sequence[Optional[np.ndarray]]] = None, nic_pacing: bool = True,
                  use_copy_engine: bool = False, x_slots: int = 3, inter_slots: int = 2,
-                 timeout_s: float = 300.0):
+                 timeout_s: float = 300.0, inter_chunk_bytes: int = 0):
         self.model, self.topo, self.plan = model, topo, plan
         self.rank, self.world_size, self.device = rank, world_size, device
         self._model_h = model.handle()
@@ -35,7 +35,7 @@ class Engine:
         self._plan_c = plan.to_c()
         self._shm_name = shm_name.encode()
         cfg = _capi.EngineConfig(self._shm_name, rank, world_size, device, x_slots, inter_slots,
-                                 int(nic_pacing), int(use_copy_engine), timeout_s)
+                                 int(nic_pacing), int(use_copy_engine), timeout_s, inter_chunk_bytes)
         masks_arg = None
         self._mask_keep = []
         if chunk_masks is not None:
