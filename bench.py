@@ -41,7 +41,9 @@ def parse():
     p.add_argument("--preset", default="gpt2-1.3b")
     p.add_argument("--strategy", default="fcdp")
     p.add_argument("--inter", default="ib100-rdma-measured")
-    p.add_argument("--batch", type=int, default=8)
+    p.add_argument("--batch", type=int, default=8,
+                   help="sequences per GPU; 0 = ZeRO-3 max batch (reference max_feasible_batch fed with the "
+                        "activation bytes per sample measured on this box)")
     p.add_argument("--seq", type=int, default=0)
     p.add_argument("--topology", default="", help="override NxG, e.g. 1x2")
     p.add_argument("--zero3-steps", type=int, default=3)
@@ -219,6 +221,34 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    def zero3_max_batch() -> int:
+        """strategy.cpp:116-137 with a measured activation coefficient."""
+        plan = S.StrategyPlan(S.StrategyKind.Zero3)
+        shm = bcast(f"fcdp_probe_{uuid.uuid4().hex[:12]}" if rank == 0 else None)
+        tr = FcdpTrainer(mc, topo, plan, rank=rank, world_size=world, device=local, shm_name=shm,
+                         batch_per_gpu=1, seq_len=seq, nic_pacing=False, timeout_s=args.engine_timeout)
+        x, y = synthetic_batch(mc.vocab, 1, seq, 0x5EED, 0, rank, device=dev)
+        tr.step(x, y)
+        tr.sync()
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats(dev)
+        base = torch.cuda.memory_allocated(dev)
+        tr.step(x, y)
+        tr.sync()
+        torch.cuda.synchronize()
+        act = max(torch.cuda.max_memory_allocated(dev) - base, 1)
+        model = tr.model
+        tr.close()
+        del tr
+        torch.cuda.empty_cache()
+        L = model.num_layers()
+        for lyr in model.layers:
+            lyr.activation_bytes_per_sample = act // L
+        cap = torch.cuda.get_device_properties(dev).total_memory
+        b, oom = S.max_feasible_batch(plan, model, topo, cap)
+        b = int(min(b, 256)) if not oom else 1
+        return int(max_over_ranks(-b) * -1) if world > 1 else b
+
     def measure(strategy: str, steps: int, warmup: int, timing: bool, e2e_steps: int):
         plan = S.StrategyPlan(S.StrategyKind.from_string(strategy))
         shm = bcast(f"fcdp_bench_{uuid.uuid4().hex[:12]}" if rank == 0 else None)
@@ -288,6 +318,8 @@ def main():
         return {"ms": ms, "counters": counters, "kernels": kst, "clocks": clocks, "loss": loss_v,
                 "node_tx": node_tx, "cache": cache, "vol": vol, "e2e": e2e}
 
+    if args.batch <= 0:
+        args.batch = zero3_max_batch()
     main_run = measure(args.strategy, args.steps, args.warmup, True, 0 if args.no_e2e else args.steps)
     z3 = None
     if not args.no_zero3 and args.strategy != "zero3":
