@@ -86,9 +86,15 @@ class ModelConfig:
     lora_rank: int = 0   # > 0: LoRA on q,k,v,o; base weights frozen
     dtype_bytes: int = 2
     name: str = ""
+    pad_vocab_to: int = 1  # embedding/head rows rounded up (GPT-2: 50257 -> 50304) for aligned GEMMs
+
+    @property
+    def vocab_rows(self) -> int:
+        m = self.pad_vocab_to
+        return (self.vocab + m - 1) // m * m
 
     def layer_defs(self) -> List[LayerDef]:
-        h, V = self.hidden, self.vocab
+        h, V = self.hidden, self.vocab_rows
         peft = self.lora_rank > 0
         defs = []
         if self.family == "gpt2":
@@ -135,7 +141,7 @@ PRESETS: Dict[str, ModelConfig] = {
     # C1: tiny 2-layer transformer, hidden 256, fp32 (12h^2 + 13h = 789,760 params per block)
     "tiny": ModelConfig("gpt2", 256, 2, 4, 1024, 64, dtype_bytes=4, name="tiny-h256-fp32"),
     # C2: GPT-2 1.3B (h=2048, 24 layers, 16 heads, 50,358,272 params per block)
-    "gpt2-1.3b": ModelConfig("gpt2", 2048, 24, 16, 50257, 1024, name="gpt2-1.3b"),
+    "gpt2-1.3b": ModelConfig("gpt2", 2048, 24, 16, 50257, 1024, name="gpt2-1.3b", pad_vocab_to=64),
     # C3: Llama-style 7B + LoRA r=16 on q,k,v,o (202,907,648 params per block, 524,288 trainable)
     "llama7b-lora16": ModelConfig("llama", 4096, 32, 32, 32000, 2048, ffn=11008, lora_rank=16,
                                   name="llama7b-lora16"),

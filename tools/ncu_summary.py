@@ -24,11 +24,24 @@ def klass(name):
     return None
 
 
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+        "second": 1.0}
+
+
 def raw_rows(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr = rows[0]
-    return [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+    hdr, units = rows[0], rows[1]
+    recs = []
+    for r in rows[2:]:
+        if len(r) != len(hdr):
+            continue
+        d = {}
+        for h, u, v in zip(hdr, units, r):
+            f = num(v)
+            d[h] = f * UNIT[u] if (f is not None and u in UNIT) else v
+        recs.append(d)
+    return recs
 
 
 def num(x):
@@ -58,6 +71,7 @@ def summarise_full(rep):
         mean = {k: sum(v) / len(v) for k, v in d.items() if k != "names" and v}
         rb, wb = mean.get("dram__bytes_read.sum"), mean.get("dram__bytes_write.sum")
         res[c] = {"launches_profiled": len(d["names"]), "kernel": d["names"][0],
+                  "duration_s": mean.get("gpu__time_duration.sum"),
                   "dram_bytes_per_launch": (rb or 0) + (wb or 0) if rb is not None else None,
                   "dram_read": rb, "dram_write": wb, **{k: v for k, v in mean.items()}}
     return res
