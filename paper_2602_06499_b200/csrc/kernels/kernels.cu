@@ -61,27 +61,36 @@ __global__ void __launch_bounds__(kThreads) expand_kernel(LayoutDev L, SlicePtrs
   const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
   const unsigned below = (1u << lane) - 1u;
   for (std::int64_t w0 = warp; w0 < L.words; w0 += nwarps * kUnroll) {
+    // phase 1: the mask words and prefixes of all kUnroll groups (independent loads)
+    unsigned bits[kUnroll];
+    std::uint32_t pre[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const std::int64_t w = w0 + u * nwarps;
+      bits[u] = w < L.words ? __ldg(L.bits + w) : 0u;
+      pre[u] = w < L.words ? __ldg(L.tpre + w) : 0u;
+    }
+    // phase 2: ranks -> source addresses; phase 3: all data loads in flight
     uint4 v[kUnroll];
     std::int64_t dst[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const std::int64_t w = w0 + u * nwarps;
+      const std::int64_t c = (w0 + u * nwarps) * 32 + lane;
+      const bool valid = c < L.chunks;
+      const bool tr = valid && ((bits[u] >> lane) & 1u);
+      // ballot over the lanes' trainable predicates == the mask word for full groups
+      const unsigned ballot = __ballot_sync(kFull, tr);
+      const std::int64_t kt = static_cast<std::int64_t>(pre[u]) + __popc(ballot & below);
       dst[u] = -1;
-      if (w < L.words) {  // warp-uniform
-        const std::int64_t c = w * 32 + lane;
-        const bool valid = c < L.chunks;
-        const bool tr = valid && ((__ldg(L.bits + w) >> lane) & 1u);
-        const unsigned ballot = __ballot_sync(kFull, tr);
-        const std::int64_t kt = static_cast<std::int64_t>(__ldg(L.tpre + w)) + __popc(ballot & below);
-        if (valid && (tr ? kWriteT : kWriteF)) {
-          const std::int64_t k = tr ? kt : c - kt;
-          const std::int64_t per = tr ? L.slice_t : L.slice_f;
-          const int j = slice_of(k, per, L.local);
-          v[u] = pick(tr ? ts : fs, j)[k - j * per];
-          dst[u] = c;
-        }
+      if (valid && (tr ? kWriteT : kWriteF)) {
+        const std::int64_t k = tr ? kt : c - kt;
+        const std::int64_t per = tr ? L.slice_t : L.slice_f;
+        const int j = slice_of(k, per, L.local);
+        v[u] = pick(tr ? ts : fs, j)[k - j * per];
+        dst[u] = c;
       }
     }
+    // phase 4: stores
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
       if (dst[u] >= 0) out[dst[u]] = v[u];
@@ -252,17 +261,40 @@ __global__ void __launch_bounds__(kThreads) rs_dense_kernel(GradPtrs g, RsArgs a
 }
 
 template <typename T>
+__device__ __forceinline__ float4 load4(const void* p, std::int64_t i4);
+template <>
+__device__ __forceinline__ float4 load4<__nv_bfloat16>(const void* p, std::int64_t i4) {
+  const uint2 q = __ldcs(static_cast<const uint2*>(p) + i4);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+template <>
+__device__ __forceinline__ float4 load4<float>(const void* p, std::int64_t i4) {
+  return __ldcs(static_cast<const float4*>(p) + i4);
+}
+
+// Inter-node epilogue, 4 elements per lane (n is a multiple of 4: whole chunks).
+template <typename T>
 __global__ void __launch_bounds__(kThreads) rs_finalize_kernel(std::int64_t n, int nodes, int node,
                                                                const float* __restrict__ own,
                                                                const void* __restrict__ wire,
                                                                std::int64_t stride, float scale,
                                                                float* __restrict__ out) {
+  const std::int64_t n4 = n / 4, s4 = stride / 4;
   const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += step) {
-    float acc = 0.0f;
-    for (int m = 0; m < nodes; ++m)  // fixed node order
-      acc = __fadd_rn(acc, m == node ? own[i] : Vec<T>::load1(wire, m * stride + i));
-    out[i] = __fmul_rn(acc, scale);
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += step) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int m = 0; m < nodes; ++m) {  // fixed node order
+      const float4 x = m == node ? __ldcs(reinterpret_cast<const float4*>(own) + i) : load4<T>(wire, m * s4 + i);
+      acc.x = __fadd_rn(acc.x, x.x);
+      acc.y = __fadd_rn(acc.y, x.y);
+      acc.z = __fadd_rn(acc.z, x.z);
+      acc.w = __fadd_rn(acc.w, x.w);
+    }
+    __stcs(reinterpret_cast<float4*>(out) + i,
+           make_float4(__fmul_rn(acc.x, scale), __fmul_rn(acc.y, scale), __fmul_rn(acc.z, scale),
+                       __fmul_rn(acc.w, scale)));
   }
 }
 
@@ -477,7 +509,8 @@ cudaError_t launch_rs_finalize(std::int64_t n_elems, int nodes, int node, int el
                                const float* own, const void* wire, std::int64_t wire_stride,
                                float scale, float* out, cudaStream_t s) {
   if (n_elems <= 0) return cudaSuccess;
-  const int grid = grid_for(n_elems, kThreads);
+  if (n_elems % 4 || wire_stride % 4) return cudaErrorInvalidValue;
+  const int grid = grid_for(n_elems / 4, kThreads);
   if (elem_bytes == 2)
     rs_finalize_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(n_elems, nodes, node, own, wire,
                                                                 wire_stride, scale, out);

@@ -145,6 +145,10 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   CK(cudaStreamCreateWithPriority(&s_gather_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_cache_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_rs_, cudaStreamNonBlocking, hi));
+  CK(cudaStreamCreateWithPriority(&s_agsend_, cudaStreamNonBlocking, hi));
+  CK(cudaStreamCreateWithPriority(&s_rssend_, cudaStreamNonBlocking, hi));
+  for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : rs_staged_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   x_reader_.assign(static_cast<std::size_t>(cfg_.x_slots), nullptr);
   for (auto& e : x_reader_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -180,7 +184,11 @@ Engine::~Engine() {
   if (iter_done_) cudaEventDestroy(iter_done_);
   for (cudaEvent_t e : join_)
     if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_})
+  for (cudaEvent_t e : rs_kernel_done_)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : rs_staged_)
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_})
     if (s) cudaStreamDestroy(s);
   for (void* p : {static_cast<void*>(param_t_), static_cast<void*>(param_f_), static_cast<void*>(master_),
                   static_cast<void*>(adam_m_), static_cast<void*>(adam_v_), static_cast<void*>(grad32_),
@@ -532,12 +540,14 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
     const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
     if (seq > static_cast<std::uint32_t>(cfg_.inter_slots))
       for (int nn = 0; nn < N_; ++nn)
-        if (nn != n_) wait_flag(s, nn * g_ + j_, kAgRxDone, seq - cfg_.inter_slots);
+        if (nn != n_) wait_flag(s_agsend_, nn * g_ + j_, kAgRxDone, seq - cfg_.inter_slots);
     unsigned char* mine = shm_->slot(rank_, 0, idx);
     const std::size_t bt = wt ? l.my_real_t * C : 0, bf = wf ? l.my_real_f * C : 0;
     const Counter ctr = backward ? kTxBwdAg : kTxFwdAg;
-    stage_pieces(0, s, mine, param_t_ + l.off_t * C, bt, 0, N_ - 1, ctr);
-    stage_pieces(0, s, mine, param_f_ + l.off_f * C, bf, bt, N_ - 1, ctr);
+    // s_agsend_ already waited on this event's deps (run()); stage there so the
+    // receive side below overlaps with our own staging.
+    stage_pieces(0, s_agsend_, mine, param_t_ + l.off_t * C, bt, 0, N_ - 1, ctr);
+    stage_pieces(0, s_agsend_, mine, param_f_ + l.off_f * C, bf, bt, N_ - 1, ctr);
     std::uint64_t rx = 0;
     for (int nn = 0; nn < N_; ++nn) {
       const int src_rank = nn * g_ + j_;
@@ -686,6 +696,7 @@ void Engine::ev_reduce_scatter(const Event& e) {
   write_flag(s, kGradReady, u);
   for (int jj = 0; jj < g_; ++jj)
     if (jj != j_) wait_flag(s, n_ * g_ + jj, kGradReady, u);
+  if (N_ > 1) CK(cudaStreamWaitEvent(s, rs_staged_[gs], 0));  // wire_[gs] staged out (use u-2)
   GradPtrs gp{};
   for (int jj = 0; jj < g_; ++jj) gp.p[jj] = grad_slot(jj, gs);
   const float scale = 1.0f / static_cast<float>(G_);
@@ -709,17 +720,21 @@ void Engine::ev_reduce_scatter(const Event& e) {
   // nodes' shards cross the NIC in the parameter dtype (costmodel.cpp:86-88).
   const std::uint32_t seq = ++seq_rs_;
   const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
+  // staging side (s_rssend_): after this slice's kernel, once receivers freed the slot
+  CK(cudaEventRecord(rs_kernel_done_[gs], s));
+  CK(cudaStreamWaitEvent(s_rssend_, rs_kernel_done_[gs], 0));
   if (seq > static_cast<std::uint32_t>(cfg_.inter_slots))
     for (int nn = 0; nn < N_; ++nn)
-      if (nn != n_) wait_flag(s, nn * g_ + j_, kRsRxDone, seq - cfg_.inter_slots);
+      if (nn != n_) wait_flag(s_rssend_, nn * g_ + j_, kRsRxDone, seq - cfg_.inter_slots);
   // stage the slice with the own-shard hole: slot layout == slice layout;
   // region m (partials of shard j*N+m) goes to node m only.
   unsigned char* mine = shm_->slot(rank_, 1, idx);
   for (int nn = 0; nn < N_; ++nn) {
     if (nn == n_) continue;
     const std::size_t off = nn * l.L.dev.shard_t * C;
-    stage_pieces(1, s, mine, wire_[gs] + off, l.L.real_chunks(false, j_ * N_ + nn) * C, off, 1, kTxRs);
+    stage_pieces(1, s_rssend_, mine, wire_[gs] + off, l.L.real_chunks(false, j_ * N_ + nn) * C, off, 1, kTxRs);
   }
+  CK(cudaEventRecord(rs_staged_[gs], s_rssend_));  // wire_[gs] may be rewritten after this
   std::uint64_t rx = 0;
   for (int nn = 0; nn < N_; ++nn) {
     if (nn == n_) continue;
@@ -778,7 +793,7 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     stream_of[e.id] = stream_for(e.kind);
     if (e.kind == EventKind::ComputeFwd) last_fwd = e.id;
   }
-  for (cudaStream_t s : {s_gather_, s_cache_, s_rs_}) CK(cudaStreamWaitEvent(s, iter_done_, 0));
+  for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_}) CK(cudaStreamWaitEvent(s, iter_done_, 0));
   if (trace_) {
     auto grow = [&](std::vector<cudaEvent_t>& v) {
       while (v.size() < n_ev) {
@@ -791,7 +806,7 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     grow(trace_end_);
     if (!trace_start_) CK(cudaEventCreate(&trace_start_));
     CK(cudaEventRecord(trace_start_, s_comp_));
-    for (cudaStream_t s : {s_gather_, s_cache_, s_rs_}) CK(cudaStreamWaitEvent(s, trace_start_, 0));
+    for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_}) CK(cudaStreamWaitEvent(s, trace_start_, 0));
     traced_events_ = static_cast<std::uint32_t>(n_ev);
   } else {
     traced_events_ = 0;
@@ -808,6 +823,8 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
                    static_cast<unsigned long long>(prog.iteration_index), e.id, shardsim::to_string(e.kind), e.layer);
     for (shardsim::EventId d : e.deps)
       if (stream_of[d] != s) CK(cudaStreamWaitEvent(s, ev_done_[d], 0));
+    if (e.kind == EventKind::AgInter && N_ > 1)
+      for (shardsim::EventId d : e.deps) CK(cudaStreamWaitEvent(s_agsend_, ev_done_[d], 0));
     const bool bwd = e.id > last_fwd;
     if (trace_) CK(cudaEventRecord(trace_begin_[e.id], s));
     switch (e.kind) {
@@ -827,8 +844,8 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     if (trace_) CK(cudaEventRecord(trace_end_[e.id], s));
   }
   // join: the next iteration starts after everything of this one
-  const cudaStream_t side[3] = {s_gather_, s_cache_, s_rs_};
-  for (int i = 0; i < 3; ++i) {
+  const cudaStream_t side[5] = {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_};
+  for (int i = 0; i < 5; ++i) {
     CK(cudaEventRecord(join_[i], side[i]));
     CK(cudaStreamWaitEvent(s_comp_, join_[i], 0));
   }
@@ -856,7 +873,7 @@ void Engine::sync() {
   // Poll instead of blocking so a cross-rank wait that can never be satisfied
   // (a peer died, a protocol bug) ends in a diagnosable TimeoutError.
   const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(cfg_.timeout_s);
-  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_}) {
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_}) {
     if (!s) continue;
     for (int spin = 0;; ++spin) {
       const cudaError_t q = cudaStreamQuery(s);

@@ -144,11 +144,16 @@ class Engine {
   unsigned char* host_cache_ = nullptr;
 
   cudaStream_t s_comp_ = nullptr, s_gather_ = nullptr, s_cache_ = nullptr, s_rs_ = nullptr;
+  // staging (send) side of the NIC path, so a message's pieces are staged
+  // while the same layer's incoming pieces are already being received
+  cudaStream_t s_agsend_ = nullptr, s_rssend_ = nullptr;
+  cudaEvent_t rs_kernel_done_[2] = {nullptr, nullptr};
+  cudaEvent_t rs_staged_[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_done_;
   std::vector<cudaEvent_t> x_reader_;  // last local reader of each X slot
   cudaEvent_t rs_done_[2] = {nullptr, nullptr};
   cudaEvent_t iter_done_ = nullptr;
-  cudaEvent_t join_[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t join_[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, seq_ag_ = 0, seq_rs_ = 0, u_ = 0;

@@ -130,7 +130,7 @@ def test_rs_finalize_bit_exact(built, eb):
     dev = _dev()
     lib = built
     rng = np.random.default_rng(5)
-    n, N = 10007, 4
+    n, N = 10008, 4  # whole 16-byte chunks (multiple of 4 elements)
     own = rng.standard_normal(n).astype(np.float32)
     wf = rng.standard_normal(N * n).astype(np.float32)
     wire = O.f32_to_bf16(wf) if eb == 2 else wf
