@@ -55,6 +55,10 @@ def parse():
                    help="dump every thread's stack and exit if the run exceeds this many seconds")
     p.add_argument("--engine-timeout", type=float, default=300.0)
     p.add_argument("--no-pacing", action="store_true", help="do not throttle the emulated inter-node link")
+    p.add_argument("--tau", type=float, default=0.0,
+                   help="FCDP-Cache GPU-retention threshold of the headline run (0: pure host-cache path)")
+    p.add_argument("--tau-variant", type=float, default=0.9,
+                   help="also measure FCDP with adaptive GPU retention at this tau (0 disables)")
     return p.parse_args()
 
 
@@ -249,12 +253,15 @@ def main():
         b = int(min(b, 256)) if not oom else 1
         return int(max_over_ranks(-b) * -1) if world > 1 else b
 
-    def measure(strategy: str, steps: int, warmup: int, timing: bool, e2e_steps: int):
-        plan = S.StrategyPlan(S.StrategyKind.from_string(strategy))
+    capacity = torch.cuda.get_device_properties(dev).total_memory
+
+    def measure(strategy: str, steps: int, warmup: int, timing: bool, e2e_steps: int, tau: float = 0.0):
+        plan = S.StrategyPlan(S.StrategyKind.from_string(strategy), tau=tau)
         shm = bcast(f"fcdp_bench_{uuid.uuid4().hex[:12]}" if rank == 0 else None)
         tr = FcdpTrainer(mc, topo, plan, rank=rank, world_size=world, device=local, shm_name=shm,
                          batch_per_gpu=args.batch, seq_len=seq, nic_pacing=not args.no_pacing, lr=1e-4,
-                         use_copy_engine=args.copy_engine, timeout_s=args.engine_timeout)
+                         use_copy_engine=args.copy_engine, timeout_s=args.engine_timeout,
+                         gpu_capacity_bytes=capacity if tau > 0 else 0)
         batches = [synthetic_batch(mc.vocab, args.batch, seq, 0x5EED, i, rank, device=dev)
                    for i in range(warmup + steps)]
         for i in range(warmup):
@@ -320,7 +327,10 @@ def main():
 
     if args.batch <= 0:
         args.batch = zero3_max_batch()
-    main_run = measure(args.strategy, args.steps, args.warmup, True, 0 if args.no_e2e else args.steps)
+    main_run = measure(args.strategy, args.steps, args.warmup, True, 0 if args.no_e2e else args.steps, args.tau)
+    tau_run = None
+    if args.tau_variant > 0 and args.strategy in ("fcdp", "fcdp-comm") and args.tau == 0:
+        tau_run = measure(args.strategy, args.zero3_steps, 2, False, 0, args.tau_variant)
     z3 = None
     if not args.no_zero3 and args.strategy != "zero3":
         z3 = measure("zero3", args.zero3_steps, 2, False, 0)
@@ -376,6 +386,10 @@ def main():
         "zero3": ({"tokens_per_s": tokens_per_step / (z3["ms"] / z3_steps(args) / 1e3), "ms_per_step": z3["ms"] / z3_steps(args)}
                   if z3 else None),
         "cache_bytes_per_step_per_node": main_run["cache"],
+        "fcdp_gpu_retention": ({"tau": args.tau_variant, "tokens_per_s": tokens_per_step / (tau_run["ms"] / args.zero3_steps / 1e3),
+                                "ms_per_step": tau_run["ms"] / args.zero3_steps, "cache": tau_run["cache"],
+                                "ag_inter_fwd_bwd": [tau_run["node_tx"]["nic_tx_fwd_ag"], tau_run["node_tx"]["nic_tx_bwd_ag"]]}
+                               if tau_run else None),
         "kernels": kernels, "loss": main_run["loss"],
     }
     print(json.dumps(line), flush=True)

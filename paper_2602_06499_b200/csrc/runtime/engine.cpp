@@ -198,7 +198,7 @@ Engine::~Engine() {
                   static_cast<void*>(rx_[1])})
     if (p) cudaFree(p);
   for (unsigned char* p : retained_)
-    if (p) cudaFree(p);
+    if (p) cudaFree(p);  // cudaMallocAsync memory; cudaFree synchronises
   for (LayerRt& l : layers_) {
     if (l.d_bits) cudaFree(l.d_bits);
     if (l.d_tpre) cudaFree(l.d_tpre);
@@ -419,7 +419,17 @@ cudaStream_t Engine::stream_for(EventKind k) const {
 unsigned char* Engine::w_buffer(int layer) {
   if (w_of_layer_[layer] < 0) {
     if (prog_->layer_retained[layer]) {
-      if (!retained_[layer]) retained_[layer] = dalloc<unsigned char>(layers_[layer].chunks * kChunkBytes, "retained layer");
+      if (!retained_[layer]) {
+        // stream-ordered allocation: no host synchronisation inside run()
+        void* p = nullptr;
+        const std::size_t bytes = static_cast<std::size_t>(layers_[layer].chunks) * kChunkBytes;
+        const cudaError_t e = cudaMallocAsync(&p, bytes, s_gather_);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          throw OomError("cudaMallocAsync(retained layer) failed: " + std::string(cudaGetErrorString(e)));
+        }
+        retained_[layer] = static_cast<unsigned char*>(p);
+      }
       w_of_layer_[layer] = 2;  // marker: retained buffer
     } else {
       w_of_layer_[layer] = static_cast<int>(w_instances_++ % 2);

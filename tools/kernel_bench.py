@@ -100,15 +100,15 @@ def main():
     n = E // 2
     timeit("rs_finalize_N2", lambda: _capi.check(lib.fcdp_rs_finalize(n, 2, 0, 2, P(own), P(wire), n, 0.5, P(own), None)),
            n * (4 + 2 + 4))
-    # --- AdamW over the whole GPT-2 1.3B trainable arena
-    nA = 1416744960 // 4
+    # --- AdamW over the whole GPT-2 1.3B trainable arena (the bench's launch, 1x1)
+    nA = 1416744960
     w = torch.randn(nA, device=dev)
     m = torch.zeros(nA, device=dev)
     v = torch.zeros(nA, device=dev)
     g = torch.randn(nA, device=dev)
     pp = torch.empty(nA, dtype=torch.bfloat16, device=dev)
     cfg = _capi.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0, 1)
-    timeit("adamw_354M", lambda: _capi.check(lib.fcdp_adam_step(nA, C.byref(cfg), P(w), P(m), P(v), P(g), P(pp), 2, None)),
+    timeit("adamw_gpt2_1.3b_arena", lambda: _capi.check(lib.fcdp_adam_step(nA, C.byref(cfg), P(w), P(m), P(v), P(g), P(pp), 2, None)),
            nA * 30)
     Path(a.out).parent.mkdir(parents=True, exist_ok=True)
     Path(a.out).write_text(json.dumps({"peak_hbm_gbs": peak, "kernels": res}, indent=1))
