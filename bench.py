@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--topology", default="", help="override NxG, e.g. 1x2")
     p.add_argument("--zero3-steps", type=int, default=3)
     p.add_argument("--no-zero3", action="store_true")
+    p.add_argument("--zeropp", action="store_true", help="also measure ZeRO++ (GPU node replica) on the same executor")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--copy-engine", action="store_true")
@@ -335,6 +336,10 @@ def main():
     if not args.no_zero3 and args.strategy != "zero3":
         z3 = measure("zero3", args.zero3_steps, 2, False, 0)
 
+    zpp = None
+    if args.zeropp and args.strategy != "zeropp":
+        zpp = measure("zeropp", args.zero3_steps, 2, False, 0)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle.cpu_step import cpu_step_sample
@@ -385,6 +390,10 @@ def main():
         "ag_inter_bytes_per_step_per_node": ag,
         "zero3": ({"tokens_per_s": tokens_per_step / (z3["ms"] / z3_steps(args) / 1e3), "ms_per_step": z3["ms"] / z3_steps(args)}
                   if z3 else None),
+        "zeropp": ({"tokens_per_s": tokens_per_step / (zpp["ms"] / args.zero3_steps / 1e3),
+                    "ms_per_step": zpp["ms"] / args.zero3_steps,
+                    "ag_inter_fwd_bwd": [zpp["node_tx"]["nic_tx_fwd_ag"], zpp["node_tx"]["nic_tx_bwd_ag"]]}
+                   if zpp else None),
         "cache_bytes_per_step_per_node": main_run["cache"],
         "fcdp_gpu_retention": ({"tau": args.tau_variant, "tokens_per_s": tokens_per_step / (tau_run["ms"] / args.zero3_steps / 1e3),
                                 "ms_per_step": tau_run["ms"] / args.zero3_steps, "cache": tau_run["cache"],

@@ -105,8 +105,9 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   plan_.validate(topo_);
   model_.validate();
   if (plan_.kind != shardsim::StrategyKind::Zero3 && plan_.kind != shardsim::StrategyKind::Fcdp &&
-      plan_.kind != shardsim::StrategyKind::FcdpComm)
-    throw shardsim::ConfigError("engine: the B200 data plane executes zero3, fcdp and fcdp-comm programs");
+      plan_.kind != shardsim::StrategyKind::FcdpComm && plan_.kind != shardsim::StrategyKind::ZeroPP)
+    throw shardsim::ConfigError("engine: the B200 data plane executes zero3, zeropp, fcdp and fcdp-comm programs");
+  zeropp_ = plan_.kind == shardsim::StrategyKind::ZeroPP;
   if (shm_name_.empty()) throw shardsim::ConfigError("engine: shm_name is required");
   N_ = topo_.num_nodes;
   g_ = topo_.gpus_per_node;
@@ -285,6 +286,10 @@ void Engine::allocate() {
   x_slot_bytes_ = round_up(static_cast<std::size_t>(max_slice_) * C, 4096);
   grad_slot_bytes_ = round_up(static_cast<std::size_t>(max_chunks_) * C, 4096);
   arena_bytes_ = x_slot_bytes_ * cfg_.x_slots + 2 * grad_slot_bytes_;
+  // ZeRO++ keeps this GPU's intra slice of every gathered layer in HBM (the
+  // node-level secondary partition, W/g per GPU; reference strategy.cpp:107-108)
+  replica_off_ = arena_bytes_;
+  if (zeropp_) arena_bytes_ += round_up(static_cast<std::size_t>(host_chunks_) * C, 4096);
   peer_arena_ = dalloc<unsigned char>(arena_bytes_, "peer arena");
   for (int i = 0; i < 2; ++i) {
     own32_[i] = dalloc<float>(static_cast<std::size_t>(max_shard_t_) * V_ * sizeof(float), "rs own");
@@ -381,6 +386,10 @@ void Engine::init_params(std::uint64_t seed, const fcdp_init_range* const* range
 // ----------------------------------------------------------------- helpers
 
 unsigned char* Engine::x_slot(int jj, int slot) const { return peer_base_[jj] + slot * x_slot_bytes_; }
+
+unsigned char* Engine::replica(int jj, int layer) const {
+  return peer_base_[jj] + replica_off_ + layers_[layer].host_off * kChunkBytes;
+}
 
 unsigned char* Engine::grad_slot(int jj, int slot) const {
   return peer_base_[jj] + cfg_.x_slots * x_slot_bytes_ + slot * grad_slot_bytes_;
@@ -583,6 +592,15 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
   if (wt) wc.ver_t = static_cast<std::int64_t>(l.shard_version_t), x_of_t_[e.layer] = slot;
   if (wf) wc.ver_f = 0, x_of_f_[e.layer] = slot;
   shm_->add(rank_, backward ? kAgEventsBwd : kAgEventsFwd, 1);
+  if (zeropp_ && !backward) {
+    // keep slice j on the GPU for the backward intra-node gather (ZeRO++ hpZ)
+    if (l.last_replica_pull_q)
+      for (int jj = 0; jj < g_; ++jj)
+        if (jj != j_) wait_flag(s, n_ * g_ + jj, kSliceFree, l.last_replica_pull_q);
+    const std::size_t bytes = (l.L.dev.slice_t + l.L.dev.slice_f) * C;
+    timed(0, s, 2 * bytes, [&] { return launch_copy(X, replica(j_, e.layer), bytes, s); });
+    l.replica_version_t = static_cast<std::int64_t>(l.shard_version_t);
+  }
 }
 
 void Engine::ev_h2d(const Event& e) {
@@ -622,6 +640,33 @@ void Engine::ev_h2d(const Event& e) {
 }
 
 void Engine::ev_ag_intra(const Event& e) {
+  if (zeropp_) {
+    // backward reconstruction from the GPU replicas of the node (no PCIe, no NIC)
+    LayerRt& l = layers_[e.layer];
+    if (l.has_t && l.replica_version_t != static_cast<std::int64_t>(l.shard_version_t))
+      throw shardsim::ProtocolError("freshness: stale GPU replica for layer " + std::to_string(e.layer));
+    const std::uint32_t q = ++q_;
+    write_flag(s_gather_, kSliceReady, q);
+    for (int jj = 0; jj < g_; ++jj)
+      if (jj != j_) wait_flag(s_gather_, n_ * g_ + jj, kSliceReady, q);
+    unsigned char* W = w_buffer(e.layer);
+    SlicePtrs ts{}, fs{};
+    for (int jj = 0; jj < g_; ++jj) {
+      ts.p[jj] = replica(jj, e.layer);
+      fs.p[jj] = replica(jj, e.layer) + l.L.dev.slice_t * kChunkBytes;
+    }
+    timed(0, s_gather_, 2 * l.chunks * kChunkBytes,
+          [&] { return launch_expand(l.L, ts, fs, W, kSetAll, s_gather_); });
+    write_flag(s_gather_, kSliceFree, q);
+    l.last_replica_pull_q = q;
+    std::uint64_t rx = 0;
+    for (int jj = 0; jj < g_; ++jj)
+      if (jj != j_) rx += (l.L.real_slice_chunks(false, jj) + l.L.real_slice_chunks(true, jj)) * kChunkBytes;
+    shm_->add(rank_, kNvlinkRx, rx);
+    WContent& wc = w_content_[w_of_layer_[e.layer]];
+    wc = WContent{e.layer, l.has_t ? l.replica_version_t : -1, l.has_f ? 0 : -1};
+    return;
+  }
   PendingSlice p = pending_h2d_[e.layer];
   if (p.slot < 0) throw shardsim::ProtocolError("ag_intra without a preceding h2d for layer " + std::to_string(e.layer));
   pull_expand(e.layer, p.slot, p.q, p.t, p.f, s_gather_);

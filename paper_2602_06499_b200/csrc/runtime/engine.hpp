@@ -48,6 +48,8 @@ struct LayerRt {
   std::uint64_t shard_version_t = 0;          // version of this rank's trainable shard
   std::int64_t host_version_t = -1, host_version_f = -1;  // versions in the host cache (-1 none)
   std::int8_t retained_slot = -1;
+  std::int64_t replica_version_t = -1;   // ZeRO++: version in this GPU's HBM replica slice
+  std::uint32_t last_replica_pull_q = 0; // ZeRO++: gather seq of the last backward pull
 };
 
 struct WContent {
@@ -106,6 +108,7 @@ class Engine {
   unsigned char* w_buffer(int layer);                    // W slot / retained buffer for layer
   unsigned char* x_slot(int rank_local, int slot) const; // local or peer pointer
   unsigned char* grad_slot(int rank_local, int slot) const;
+  unsigned char* replica(int rank_local, int layer) const;
   void wait_flag(cudaStream_t s, int rank, Flag f, std::uint32_t v);
   void write_flag(cudaStream_t s, Flag f, std::uint32_t v);
   std::int64_t pieces_of(std::size_t bytes) const;
@@ -184,6 +187,8 @@ class Engine {
   fcdp_compute_fn compute_fn_ = nullptr;
   void* compute_user_ = nullptr;
   bool use_ce_ = false;
+  bool zeropp_ = false;
+  std::size_t replica_off_ = 0;
 
   // kernel accounting (launch counts always, event timing when enabled)
   template <typename F>

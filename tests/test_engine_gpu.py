@@ -129,11 +129,12 @@ def check_job(cfg, dumps):
                     assert sum(c["cache_d2h"] for c in node) == vol.d2h_total
 
 
-CASES_1 = [(1, 1, "zero3", 2, "dense"), (1, 1, "fcdp", 2, "dense"), (1, 1, "fcdp-comm", 2, "lora"),
+CASES_1 = [(1, 1, "zeropp", 2, "dense"), (1, 1, "zero3", 2, "dense"), (1, 1, "fcdp", 2, "dense"), (1, 1, "fcdp-comm", 2, "lora"),
            (1, 1, "fcdp-comm", 4, "random"), (1, 1, "fcdp", 4, "lora")]
 CASES_2 = [(2, 1, "zero3", 2, "dense"), (2, 1, "fcdp", 2, "dense"), (2, 1, "fcdp-comm", 2, "lora"),
-           (1, 2, "fcdp", 2, "dense"), (1, 2, "fcdp-comm", 2, "random"), (2, 1, "fcdp-comm", 4, "random")]
-CASES_4 = [(2, 2, "zero3", 2, "dense"), (2, 2, "fcdp", 2, "dense"), (2, 2, "fcdp-comm", 2, "lora"),
+           (1, 2, "fcdp", 2, "dense"), (1, 2, "fcdp-comm", 2, "random"), (2, 1, "fcdp-comm", 4, "random"),
+           (1, 2, "zeropp", 2, "lora")]
+CASES_4 = [(2, 2, "zeropp", 2, "dense"), (2, 2, "zero3", 2, "dense"), (2, 2, "fcdp", 2, "dense"), (2, 2, "fcdp-comm", 2, "lora"),
            (4, 1, "fcdp-comm", 2, "random"), (1, 4, "fcdp", 4, "lora")]
 
 
