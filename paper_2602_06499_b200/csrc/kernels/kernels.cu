@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <type_traits>
 
 #include "kernels/kernels.hpp"
@@ -117,6 +118,110 @@ __global__ void __launch_bounds__(kThreads) concat_kernel(SlicePtrs src, std::in
     for (int u = 0; u < kUnroll; ++u) d[i + u * stride] = v[u];
   }
   for (; i < n; i += stride) d[i] = s[i];
+}
+
+// ---------------------------------------------------------- TMA bulk copy
+// Dense gathers and the own-shard pack are pure copies: one elected thread per
+// CTA drives the Tensor Memory Accelerator with 1-D bulk copies
+// (cp.async.bulk global->shared with an mbarrier transaction count, then
+// shared->global), kStages 32 KiB tiles in flight per SM.  One warp per SM
+// moves the bytes, so the copy leaves the SMs to the concurrently running
+// GEMMs of the driving model.  Sources may be NVLink peer mappings.
+constexpr int kBulkTile = 32 * 1024;
+constexpr int kBulkStages = 4;
+
+struct BulkSegs {
+  const unsigned char* src[kMaxLocal + 1];
+  unsigned char* dst[kMaxLocal + 1];
+  std::int64_t bytes[kMaxLocal + 1];
+  std::int64_t tile_base[kMaxLocal + 2];  // exclusive prefix of tiles per segment
+  int n;
+};
+
+__device__ __forceinline__ void bulk_tile(const BulkSegs& s, std::int64_t t, const unsigned char*& src,
+                                          unsigned char*& dst, unsigned& bytes) {
+  int k = 0;
+#pragma unroll
+  for (int i = 1; i <= kMaxLocal; ++i)
+    if (i < s.n && t >= s.tile_base[i]) k = i;
+  const std::int64_t off = (t - s.tile_base[k]) * kBulkTile;
+  const std::int64_t rem = s.bytes[k] - off;
+  bytes = static_cast<unsigned>(rem < kBulkTile ? rem : kBulkTile);
+  src = s.src[k] + off;
+  dst = s.dst[k] + off;
+}
+
+__global__ void __launch_bounds__(32) bulk_copy_kernel(BulkSegs segs) {
+  extern __shared__ __align__(1024) unsigned char bulk_smem[];
+  auto stage = reinterpret_cast<unsigned char(*)[kBulkTile]>(bulk_smem);
+  auto bar = reinterpret_cast<unsigned long long*>(bulk_smem + kBulkStages * kBulkTile);
+  if (threadIdx.x != 0) return;
+  const std::int64_t total = segs.tile_base[segs.n];
+  const std::int64_t n = total > blockIdx.x ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (n == 0) return;
+  for (int i = 0; i < kBulkStages; ++i)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(&bar[i]))));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto issue_load = [&](std::int64_t i) {
+    const int st = static_cast<int>(i % kBulkStages);
+    const unsigned char* src;
+    unsigned char* dst;
+    unsigned bytes;
+    bulk_tile(segs, blockIdx.x + i * gridDim.x, src, dst, bytes);
+    const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(&bar[st]));
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(&stage[st][0]));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+  };
+  for (std::int64_t i = 0; i < kBulkStages - 1 && i < n; ++i) issue_load(i);
+  for (std::int64_t i = 0; i < n; ++i) {
+    // the stage refilled below last held tile i-1, whose store must have read it
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (i + kBulkStages - 1 < n) issue_load(i + kBulkStages - 1);
+    const int st = static_cast<int>(i % kBulkStages);
+    const unsigned phase = static_cast<unsigned>((i / kBulkStages) & 1);
+    const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(&bar[st]));
+    unsigned done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(b), "r"(phase)
+          : "memory");
+    const unsigned char* src;
+    unsigned char* dst;
+    unsigned bytes;
+    bulk_tile(segs, blockIdx.x + i * gridDim.x, src, dst, bytes);
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&stage[st][0]));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(sa), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+cudaError_t launch_bulk(const BulkSegs& segs_in, cudaStream_t s) {
+  BulkSegs segs = segs_in;
+  std::int64_t tiles = 0;
+  for (int i = 0; i < segs.n; ++i) {
+    segs.tile_base[i] = tiles;
+    tiles += (segs.bytes[i] + kBulkTile - 1) / kBulkTile;
+  }
+  segs.tile_base[segs.n] = tiles;
+  if (tiles == 0) return cudaSuccess;
+  constexpr int kSmem = kBulkStages * kBulkTile + kBulkStages * 8;
+  static bool configured = false;
+  if (!configured) {
+    const cudaError_t e = cudaFuncSetAttribute(bulk_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int grid = static_cast<int>(std::min<std::int64_t>(tiles, static_cast<std::int64_t>(sm_count())));
+  bulk_copy_kernel<<<grid, 32, kSmem, s>>>(segs);
+  return cudaGetLastError();
 }
 
 // --------------------------------------------------------------- partition
@@ -448,9 +553,16 @@ cudaError_t launch_expand(const Layout& L, const SlicePtrs& ts, const SlicePtrs&
     const bool tr = L.dense_trainable();
     if (tr ? !want_t : !want_f) return cudaSuccess;
     const std::int64_t per = tr ? L.dev.slice_t : L.dev.slice_f;
-    dim3 grid(std::max(1, grid_for(per, kThreads * kUnroll) / L.dev.local), L.dev.local);
-    concat_kernel<<<grid, kThreads, 0, s>>>(tr ? ts : fs, per, L.dev.chunks, out);
-    return cudaGetLastError();
+    BulkSegs segs{};
+    for (int j = 0; j < L.dev.local; ++j) {
+      const std::int64_t lo = j * per;
+      if (lo >= L.dev.chunks) break;
+      segs.src[segs.n] = static_cast<const unsigned char*>((tr ? ts : fs).p[j]);
+      segs.dst[segs.n] = reinterpret_cast<unsigned char*>(out + lo);
+      segs.bytes[segs.n] = std::min(per, L.dev.chunks - lo) * kChunkBytes;
+      ++segs.n;
+    }
+    return launch_bulk(segs, s);
   }
   const int grid = grid_for(L.dev.words * 32, kThreads * kUnroll);
   if (want_t && want_f)
@@ -554,6 +666,15 @@ cudaError_t launch_widen(std::int64_t n, const void* src, int elem_bytes, float*
 }
 
 cudaError_t launch_copy(const void* src, void* dst, std::int64_t bytes, cudaStream_t s) {
+  if (bytes % kChunkBytes == 0 && reinterpret_cast<std::uintptr_t>(src) % 16 == 0 &&
+      reinterpret_cast<std::uintptr_t>(dst) % 16 == 0) {
+    BulkSegs segs{};
+    segs.src[0] = static_cast<const unsigned char*>(src);
+    segs.dst[0] = static_cast<unsigned char*>(dst);
+    segs.bytes[0] = bytes;
+    segs.n = 1;
+    return launch_bulk(segs, s);
+  }
   const std::int64_t n = bytes / kChunkBytes;
   if (n > 0)
     copy_kernel<<<grid_for(n, kThreads * kUnroll), kThreads, 0, s>>>(static_cast<const uint4*>(src),
