@@ -258,11 +258,11 @@ typedef struct fcdp_engine_config {
   int32_t rank, world_size; /* world_size == num_nodes * gpus_per_node */
   int32_t device;           /* CUDA ordinal of this rank */
   int32_t x_slots;          /* slice buffer slots (>= 2; default 3) */
-  int32_t inter_slots;      /* NIC staging slots (>= 2; default 2) */
+  int32_t inter_slots;      /* NIC staging ring depth in pieces (>= 4; default 16) */
   int32_t nic_pacing;       /* 1: pace inter-node traffic at topology inter bandwidth */
   int32_t use_copy_engine;  /* 1: dense intra gathers by cudaMemcpyAsync (CE) not SM kernels */
   double timeout_s;         /* deadline for host-side cross-rank waits */
-  int64_t inter_chunk_bytes; /* NIC emulator wire piece size (0: 4 MiB) */
+  int64_t inter_chunk_bytes; /* NIC emulator wire piece size (0: 4 MiB); inter_slots = staging ring depth in pieces */
 } fcdp_engine_config;
 
 /* Counters of one rank (bytes).  Per node = sum over that node's ranks. */

@@ -120,7 +120,7 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   eb_ = model_.param_bytes_per_element;
   V_ = kChunkBytes / eb_;
   if (cfg_.x_slots < 2) cfg_.x_slots = 3;
-  if (cfg_.inter_slots < 2) cfg_.inter_slots = 2;
+  if (cfg_.inter_slots < 4) cfg_.inter_slots = 16;  // staging ring depth, in pieces
   if (cfg_.timeout_s <= 0) cfg_.timeout_s = 300.0;
   use_ce_ = cfg_.use_copy_engine != 0;
   chunk_bytes_ = cfg_.inter_chunk_bytes > 0 ? cfg_.inter_chunk_bytes : (4ll << 20);
@@ -129,12 +129,9 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   CK(cudaSetDevice(cfg_.device));
   build_layouts(chunk_masks);
 
-  std::uint64_t slot_bytes = 0;
-  for (const LayerRt& l : layers_) {
-    slot_bytes = std::max<std::uint64_t>(slot_bytes, (l.L.dev.shard_t + l.L.dev.shard_f) * kChunkBytes);
-    slot_bytes = std::max<std::uint64_t>(slot_bytes, l.L.dev.slice_t * kChunkBytes);
-  }
-  shm_ = std::make_unique<SharedBlock>(shm_name_, rank_, G_, N_, g_, cfg_.inter_slots, slot_bytes, cfg_.timeout_s);
+  // staging ring: inter_slots pieces of chunk_bytes_ per class per rank
+  shm_ = std::make_unique<SharedBlock>(shm_name_, rank_, G_, N_, g_, cfg_.inter_slots,
+                                       static_cast<std::uint64_t>(chunk_bytes_), cfg_.timeout_s);
   CK(cudaHostRegister(shm_->base(), shm_->bytes(), cudaHostRegisterPortable | cudaHostRegisterMapped));
   CK(cudaHostGetDevicePointer(&shm_dev_base_, shm_->base(), 0));
   if (!StreamOps::available()) throw CudaError("engine: stream memory operations unavailable on this device");
@@ -502,16 +499,23 @@ std::int64_t Engine::pieces_of(std::size_t bytes) const {
   return bytes == 0 ? 0 : static_cast<std::int64_t>((bytes + ch - 1) / ch);
 }
 
-void Engine::stage_pieces(int cls, cudaStream_t s, unsigned char* slot, const void* src, std::size_t bytes,
-                          std::size_t slot_off, std::uint64_t wire_mult, Counter counter) {
-  // Pipelined host-staged wire: each piece is staged, flagged, and handed to
-  // the NIC thread, which puts it on the emulated wire as soon as it lands.
+void Engine::stage_pieces(int cls, cudaStream_t s, const void* src, std::size_t bytes, std::uint64_t wire_mult,
+                          Counter counter) {
+  // Pipelined host-staged wire: each piece is staged into the next slot of
+  // this rank's ring, flagged, and handed to the NIC thread, which puts it on
+  // the emulated wire as soon as it lands.  A ring slot is reused only once
+  // every receiver has marked the piece it held as consumed.
   const std::size_t ch = static_cast<std::size_t>(chunk_bytes_);
+  const std::uint32_t ring = static_cast<std::uint32_t>(cfg_.inter_slots);
+  const Flag consumed = static_cast<Flag>((cls == 0 ? kAgConsumed0 : kRsConsumed0) + n_);
   for (std::size_t off = 0; off < bytes; off += ch) {
     const std::size_t n = std::min(ch, bytes - off);
-    CK(cudaMemcpyAsync(slot + slot_off + off, static_cast<const unsigned char*>(src) + off, n,
-                       cudaMemcpyDeviceToHost, s));
     const std::uint32_t id = ++sent_pieces_[cls];
+    if (id > ring)
+      for (int nn = 0; nn < N_; ++nn)
+        if (nn != n_) wait_flag(s, nn * g_ + j_, consumed, id - ring);
+    CK(cudaMemcpyAsync(shm_->slot(rank_, cls, static_cast<int>(id % ring)), static_cast<const unsigned char*>(src) + off,
+                       n, cudaMemcpyDeviceToHost, s));
     write_flag(s, cls == 0 ? kAgStaged : kRsStaged, id);
     nic_->submit({cls, id, n * wire_mult, counter});
     shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, id);
@@ -519,13 +523,24 @@ void Engine::stage_pieces(int cls, cudaStream_t s, unsigned char* slot, const vo
   shm_->add(rank_, kStagingD2H, bytes);
 }
 
-void Engine::receive_pieces(int cls, cudaStream_t s, int src_rank, std::uint32_t first_id, const unsigned char* slot,
-                            std::size_t slot_off, std::size_t bytes, unsigned char* dst) {
+void Engine::mark_consumed(int cls, cudaStream_t s, int src_node, std::uint32_t id) {
+  std::uint32_t& last = consumed_[cls][src_node];
+  if (static_cast<std::int32_t>(id - last) <= 0) return;  // monotone
+  last = id;
+  write_flag(s, static_cast<Flag>((cls == 0 ? kAgConsumed0 : kRsConsumed0) + src_node), id);
+}
+
+void Engine::receive_pieces(int cls, cudaStream_t s, int src_rank, std::uint32_t first_id, std::size_t bytes,
+                            unsigned char* dst) {
   const std::size_t ch = static_cast<std::size_t>(chunk_bytes_);
+  const std::uint32_t ring = static_cast<std::uint32_t>(cfg_.inter_slots);
+  const int src_node = src_rank / g_;
   std::uint32_t id = first_id;
   for (std::size_t off = 0; off < bytes; off += ch, ++id) {
     wait_flag(s, src_rank, cls == 0 ? kAgTxReady : kRsTxReady, id);
-    CK(cudaMemcpyAsync(dst + off, slot + slot_off + off, std::min(ch, bytes - off), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dst + off, shm_->slot(src_rank, cls, static_cast<int>(id % ring)), std::min(ch, bytes - off),
+                       cudaMemcpyHostToDevice, s));
+    mark_consumed(cls, s, src_node, id);
   }
   shm_->add(rank_, kStagingH2D, bytes);
 }
@@ -554,34 +569,26 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
     });
   if (N_ > 1) {
     // Inter-node all-gather among {(n', j)} through the host-staged NIC path,
-    // pipelined in pieces of chunk_bytes_.
-    const std::uint32_t seq = ++seq_ag_;
-    const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
-    if (seq > static_cast<std::uint32_t>(cfg_.inter_slots))
-      for (int nn = 0; nn < N_; ++nn)
-        if (nn != n_) wait_flag(s_agsend_, nn * g_ + j_, kAgRxDone, seq - cfg_.inter_slots);
-    unsigned char* mine = shm_->slot(rank_, 0, idx);
+    // pipelined in pieces of chunk_bytes_.  Staging runs on s_agsend_ (which
+    // already waited on this event's deps in run()), so the receive side below
+    // overlaps with it.
     const std::size_t bt = wt ? l.my_real_t * C : 0, bf = wf ? l.my_real_f * C : 0;
     const Counter ctr = backward ? kTxBwdAg : kTxFwdAg;
-    // s_agsend_ already waited on this event's deps (run()); stage there so the
-    // receive side below overlaps with our own staging.
-    stage_pieces(0, s_agsend_, mine, param_t_ + l.off_t * C, bt, 0, N_ - 1, ctr);
-    stage_pieces(0, s_agsend_, mine, param_f_ + l.off_f * C, bf, bt, N_ - 1, ctr);
+    stage_pieces(0, s_agsend_, param_t_ + l.off_t * C, bt, N_ - 1, ctr);
+    stage_pieces(0, s_agsend_, param_f_ + l.off_f * C, bf, N_ - 1, ctr);
     std::uint64_t rx = 0;
     for (int nn = 0; nn < N_; ++nn) {
       const int src_rank = nn * g_ + j_;
       const int r = j_ * N_ + nn;
       const std::size_t rt = wt ? l.L.real_chunks(false, r) * C : 0, rf = wf ? l.L.real_chunks(true, r) * C : 0;
       const std::uint32_t base = recv_base_[0][src_rank];
-      recv_base_[0][src_rank] += static_cast<std::uint32_t>(pieces_of(rt) + pieces_of(rf));
+      const std::uint32_t pt = static_cast<std::uint32_t>(pieces_of(rt));
+      recv_base_[0][src_rank] += pt + static_cast<std::uint32_t>(pieces_of(rf));
       if (nn == n_) continue;
-      const unsigned char* src = shm_->slot(src_rank, 0, idx);
-      receive_pieces(0, s, src_rank, base + 1, src, 0, rt, X + nn * l.L.dev.shard_t * C);
-      receive_pieces(0, s, src_rank, base + 1 + static_cast<std::uint32_t>(pieces_of(rt)), src, rt, rf,
-                     Xf + nn * l.L.dev.shard_f * C);
+      receive_pieces(0, s, src_rank, base + 1, rt, X + nn * l.L.dev.shard_t * C);
+      receive_pieces(0, s, src_rank, base + 1 + pt, rf, Xf + nn * l.L.dev.shard_f * C);
       rx += rt + rf;
     }
-    write_flag(s, kAgRxDone, seq);
     shm_->add(rank_, backward ? kRxBwdAg : kRxFwdAg, rx);
   }
   finish_slice_fill(slot, q);
@@ -773,21 +780,14 @@ void Engine::ev_reduce_scatter(const Event& e) {
 
   // Inter-node reduce-scatter among {(n', j)}: partial sums of the other
   // nodes' shards cross the NIC in the parameter dtype (costmodel.cpp:86-88).
-  const std::uint32_t seq = ++seq_rs_;
-  const int idx = static_cast<int>(seq % static_cast<std::uint32_t>(cfg_.inter_slots));
-  // staging side (s_rssend_): after this slice's kernel, once receivers freed the slot
+  // staging side (s_rssend_): after this slice's kernel
   CK(cudaEventRecord(rs_kernel_done_[gs], s));
   CK(cudaStreamWaitEvent(s_rssend_, rs_kernel_done_[gs], 0));
-  if (seq > static_cast<std::uint32_t>(cfg_.inter_slots))
-    for (int nn = 0; nn < N_; ++nn)
-      if (nn != n_) wait_flag(s_rssend_, nn * g_ + j_, kRsRxDone, seq - cfg_.inter_slots);
-  // stage the slice with the own-shard hole: slot layout == slice layout;
-  // region m (partials of shard j*N+m) goes to node m only.
-  unsigned char* mine = shm_->slot(rank_, 1, idx);
+  // region m (partials of shard j*N+m) goes to node m only; regions in ascending m
   for (int nn = 0; nn < N_; ++nn) {
     if (nn == n_) continue;
     const std::size_t off = nn * l.L.dev.shard_t * C;
-    stage_pieces(1, s_rssend_, mine, wire_[gs] + off, l.L.real_chunks(false, j_ * N_ + nn) * C, off, 1, kTxRs);
+    stage_pieces(1, s_rssend_, wire_[gs] + off, l.L.real_chunks(false, j_ * N_ + nn) * C, 1, kTxRs);
   }
   CK(cudaEventRecord(rs_staged_[gs], s_rssend_));  // wire_[gs] may be rewritten after this
   std::uint64_t rx = 0;
@@ -803,12 +803,12 @@ void Engine::ev_reduce_scatter(const Event& e) {
       id += static_cast<std::uint32_t>(pieces_of(l.L.real_chunks(false, j_ * N_ + m) * C));
     }
     recv_base_[1][src_rank] = id;
+    mark_consumed(1, s, nn, mine_first - 1);  // pieces before our region are not ours to read
     const std::size_t my = l.my_real_t * C;
-    receive_pieces(1, s, src_rank, mine_first, shm_->slot(src_rank, 1, idx), n_ * l.L.dev.shard_t * C, my,
-                   rx_[gs] + nn * l.L.dev.shard_t * C);
+    receive_pieces(1, s, src_rank, mine_first, my, rx_[gs] + nn * l.L.dev.shard_t * C);
+    mark_consumed(1, s, nn, id);              // nor are the ones after it
     rx += my;
   }
-  write_flag(s, kRsRxDone, seq);
   shm_->add(rank_, kRxRs, rx);
   const std::uint64_t fin_elems = static_cast<std::uint64_t>(l.L.dev.shard_t) * V_;
   timed(2, s, fin_elems * (2 * sizeof(float) + static_cast<std::uint64_t>(N_ - 1) * eb_), [&] {
@@ -936,8 +936,8 @@ void Engine::sync() {
       if (q != cudaErrorNotReady) CK(q);
       if (std::chrono::steady_clock::now() > deadline) {
         std::string msg = "engine: rank " + std::to_string(rank_) + " stream did not drain within timeout; " +
-                          "seq q=" + std::to_string(q_) + " ag=" + std::to_string(seq_ag_) + " rs=" +
-                          std::to_string(seq_rs_) + " u=" + std::to_string(u_) + "; flags:";
+                          "seq q=" + std::to_string(q_) + " ag_pieces=" + std::to_string(sent_pieces_[0]) + " rs_pieces=" +
+                          std::to_string(sent_pieces_[1]) + " u=" + std::to_string(u_) + "; flags:";
         for (int r = 0; r < G_; ++r) {
           msg += " [r" + std::to_string(r);
           for (int f = 0; f < kNumFlags; ++f) msg += " " + std::to_string(*shm_->flag(r, static_cast<Flag>(f)));

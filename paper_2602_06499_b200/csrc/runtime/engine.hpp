@@ -112,10 +112,11 @@ class Engine {
   void wait_flag(cudaStream_t s, int rank, Flag f, std::uint32_t v);
   void write_flag(cudaStream_t s, Flag f, std::uint32_t v);
   std::int64_t pieces_of(std::size_t bytes) const;
-  void stage_pieces(int cls, cudaStream_t s, unsigned char* slot, const void* src, std::size_t bytes,
-                    std::size_t slot_off, std::uint64_t wire_mult, Counter counter);
-  void receive_pieces(int cls, cudaStream_t s, int src_rank, std::uint32_t first_id, const unsigned char* slot,
-                      std::size_t slot_off, std::size_t bytes, unsigned char* dst);
+  void stage_pieces(int cls, cudaStream_t s, const void* src, std::size_t bytes, std::uint64_t wire_mult,
+                    Counter counter);
+  void receive_pieces(int cls, cudaStream_t s, int src_rank, std::uint32_t first_id, std::size_t bytes,
+                      unsigned char* dst);
+  void mark_consumed(int cls, cudaStream_t s, int src_node, std::uint32_t id);
   bool is_peer_rank(int r) const { return r / g_ == n_; }
 
   fcdp_engine_config cfg_;
@@ -159,10 +160,11 @@ class Engine {
   cudaEvent_t join_[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
   // sequence counters (identical on every rank)
-  std::uint32_t q_ = 0, seq_ag_ = 0, seq_rs_ = 0, u_ = 0;
+  std::uint32_t q_ = 0, u_ = 0;
   std::int64_t chunk_bytes_ = 4ll << 20;          // inter-node wire piece size
   std::uint32_t sent_pieces_[2] = {0, 0};         // my cumulative staged pieces per class
   std::uint32_t recv_base_[2][64] = {};           // replica of every sender's piece counter
+  std::uint32_t consumed_[2][8] = {};             // last consumed marker written, per sender node
   std::uint64_t w_instances_ = 0;
   std::uint32_t grad_slot_seq_ = 0;
   int opt_steps_ = 0;

@@ -23,17 +23,19 @@ inline constexpr std::uint64_t kShmMagic = 0x46434450'42323030ull;  // "FCDPB200
 inline constexpr int kMaxRanks = 64;
 
 enum Flag : int {
-  kAgTxReady = 0,  // inter AG: my staged shard is on the wire up to seq
-  kAgRxDone,       // inter AG: I have copied in every peer shard up to seq
+  kAgTxReady = 0,  // inter AG: my staged piece <= id has crossed the emulated wire
   kRsTxReady,      // inter RS: same, reduce-scatter class
-  kRsRxDone,
   kSliceReady,     // intra gather: my slice buffer holds gather seq
   kSliceFree,      // intra gather: I finished pulling peers' slices of seq
   kGradReady,      // intra RS: my natural gradient buffer holds rs seq
   kGradFree,       // intra RS: I finished pulling peers' gradients of seq
-  kAgStaged,       // inter AG: my staging D2H of seq landed in host memory (for my NIC thread)
+  kAgStaged,       // inter AG: my staging D2H of piece id landed in host memory (for my NIC thread)
   kRsStaged,       // inter RS: same
-  kNumFlags
+  // consumed markers, one per SENDER node: "I no longer need any piece <= v of
+  // node n's sender" -> that sender may reuse the ring slots of those pieces
+  kAgConsumed0,
+  kRsConsumed0 = kAgConsumed0 + 8,
+  kNumFlags = kRsConsumed0 + 8
 };
 
 enum Counter : int {
@@ -91,7 +93,7 @@ class SharedBlock {
   void* base() const { return hdr_; }
   std::size_t bytes() const { return bytes_; }
   RankBlock& rank_block(int r) const { return hdr_->ranks[r]; }
-  // Staging slot of (rank, class 0 = AG / 1 = RS, slot index).
+  // Staging ring slot of (rank, class 0 = AG / 1 = RS, slot index).
   unsigned char* slot(int rank, int cls, int idx) const;
   volatile std::uint32_t* flag(int rank, Flag f) const { return &hdr_->ranks[rank].flags[f].v; }
   void add(int rank, Counter c, std::uint64_t v) const {

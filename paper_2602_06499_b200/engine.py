@@ -26,7 +26,7 @@ class Engine:
     def __init__(self, model: ModelSpec, topo: ClusterTopology, plan: StrategyPlan, *, rank: int,
                  world_size: int, device: int, shm_name: str,
                  chunk_masks: Optional[Sequence[Optional[np.ndarray]]] = None, nic_pacing: bool = True,
-                 use_copy_engine: bool = False, x_slots: int = 3, inter_slots: int = 2,
+                 use_copy_engine: bool = False, x_slots: int = 3, inter_slots: int = 16,
                  timeout_s: float = 300.0, inter_chunk_bytes: int = 0):
         self.model, self.topo, self.plan = model, topo, plan
         self.rank, self.world_size, self.device = rank, world_size, device
