@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--copy-engine", action="store_true")
-    p.add_argument("--watchdog", type=float, default=1200.0,
+    p.add_argument("--watchdog", type=float, default=900.0,
                    help="dump every thread's stack and exit if the run exceeds this many seconds")
     p.add_argument("--engine-timeout", type=float, default=300.0)
     p.add_argument("--no-pacing", action="store_true", help="do not throttle the emulated inter-node link")

@@ -499,28 +499,23 @@ std::int64_t Engine::pieces_of(std::size_t bytes) const {
   return bytes == 0 ? 0 : static_cast<std::int64_t>((bytes + ch - 1) / ch);
 }
 
-void Engine::stage_pieces(int cls, cudaStream_t s, const void* src, std::size_t bytes, std::uint64_t wire_mult,
-                          Counter counter) {
-  // Pipelined host-staged wire: each piece is staged into the next slot of
+void Engine::stage_one(int cls, cudaStream_t s, const void* src, std::size_t n, std::uint64_t wire_mult,
+                       Counter counter) {
+  // Pipelined host-staged wire: the piece is staged into the next slot of
   // this rank's ring, flagged, and handed to the NIC thread, which puts it on
   // the emulated wire as soon as it lands.  A ring slot is reused only once
   // every receiver has marked the piece it held as consumed.
-  const std::size_t ch = static_cast<std::size_t>(chunk_bytes_);
   const std::uint32_t ring = static_cast<std::uint32_t>(cfg_.inter_slots);
   const Flag consumed = static_cast<Flag>((cls == 0 ? kAgConsumed0 : kRsConsumed0) + n_);
-  for (std::size_t off = 0; off < bytes; off += ch) {
-    const std::size_t n = std::min(ch, bytes - off);
-    const std::uint32_t id = ++sent_pieces_[cls];
-    if (id > ring)
-      for (int nn = 0; nn < N_; ++nn)
-        if (nn != n_) wait_flag(s, nn * g_ + j_, consumed, id - ring);
-    CK(cudaMemcpyAsync(shm_->slot(rank_, cls, static_cast<int>(id % ring)), static_cast<const unsigned char*>(src) + off,
-                       n, cudaMemcpyDeviceToHost, s));
-    write_flag(s, cls == 0 ? kAgStaged : kRsStaged, id);
-    nic_->submit({cls, id, n * wire_mult, counter});
-    shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, id);
-  }
-  shm_->add(rank_, kStagingD2H, bytes);
+  const std::uint32_t id = ++sent_pieces_[cls];
+  if (id > ring)
+    for (int nn = 0; nn < N_; ++nn)
+      if (nn != n_) wait_flag(s, nn * g_ + j_, consumed, id - ring);
+  CK(cudaMemcpyAsync(shm_->slot(rank_, cls, static_cast<int>(id % ring)), src, n, cudaMemcpyDeviceToHost, s));
+  write_flag(s, cls == 0 ? kAgStaged : kRsStaged, id);
+  nic_->submit({cls, id, n * wire_mult, counter});
+  shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, id);
+  shm_->add(rank_, kStagingD2H, n);
 }
 
 void Engine::mark_consumed(int cls, cudaStream_t s, int src_node, std::uint32_t id) {
@@ -530,19 +525,56 @@ void Engine::mark_consumed(int cls, cudaStream_t s, int src_node, std::uint32_t 
   write_flag(s, static_cast<Flag>((cls == 0 ? kAgConsumed0 : kRsConsumed0) + src_node), id);
 }
 
-void Engine::receive_pieces(int cls, cudaStream_t s, int src_rank, std::uint32_t first_id, std::size_t bytes,
-                            unsigned char* dst) {
+void Engine::exchange(int cls, cudaStream_t send_s, const std::vector<SendSeg>& mine, std::uint64_t wire_mult,
+                      Counter counter, cudaStream_t recv_s, const std::vector<Inbound>& inbound) {
+  // Host enqueue order interleaves my k-th outgoing piece with every sender's
+  // k-th incoming piece.  A rank that must wait (host side) for a receiver to
+  // post consumption of its piece k - ring therefore never waits on a peer
+  // host that is itself stuck before enqueuing that receive: every rank posts
+  // piece k's consumption before it stages piece k + ring.
   const std::size_t ch = static_cast<std::size_t>(chunk_bytes_);
   const std::uint32_t ring = static_cast<std::uint32_t>(cfg_.inter_slots);
-  const int src_node = src_rank / g_;
-  std::uint32_t id = first_id;
-  for (std::size_t off = 0; off < bytes; off += ch, ++id) {
-    wait_flag(s, src_rank, cls == 0 ? kAgTxReady : kRsTxReady, id);
-    CK(cudaMemcpyAsync(dst + off, shm_->slot(src_rank, cls, static_cast<int>(id % ring)), std::min(ch, bytes - off),
-                       cudaMemcpyHostToDevice, s));
-    mark_consumed(cls, s, src_node, id);
+  struct P {
+    const unsigned char* src;
+    std::size_t n;
+  };
+  std::vector<P> out;
+  for (const SendSeg& sg : mine)
+    for (std::size_t off = 0; off < sg.bytes; off += ch)
+      out.push_back({static_cast<const unsigned char*>(sg.src) + off, std::min(ch, sg.bytes - off)});
+  struct R {
+    int src_rank;
+    std::uint32_t first;
+    std::vector<std::pair<std::size_t, unsigned char*>> pieces;  // (bytes, dst or null)
+  };
+  std::vector<R> in;
+  std::size_t kmax = out.size();
+  for (const Inbound& ib : inbound) {
+    R r{ib.src_rank, recv_base_[cls][ib.src_rank] + 1, {}};
+    for (const InSeg& sg : ib.segs)
+      for (std::size_t off = 0; off < sg.bytes; off += ch)
+        r.pieces.push_back({std::min(ch, sg.bytes - off), sg.dst ? sg.dst + off : nullptr});
+    recv_base_[cls][ib.src_rank] += static_cast<std::uint32_t>(r.pieces.size());
+    kmax = std::max(kmax, r.pieces.size());
+    in.push_back(std::move(r));
   }
-  shm_->add(rank_, kStagingH2D, bytes);
+  std::uint64_t rx = 0;
+  for (std::size_t k = 0; k < kmax; ++k) {
+    if (k < out.size()) stage_one(cls, send_s, out[k].src, out[k].n, wire_mult, counter);
+    for (R& r : in) {
+      if (k >= r.pieces.size()) continue;
+      const std::uint32_t id = r.first + static_cast<std::uint32_t>(k);
+      const auto [n, dst] = r.pieces[k];
+      if (dst) {
+        wait_flag(recv_s, r.src_rank, cls == 0 ? kAgTxReady : kRsTxReady, id);
+        CK(cudaMemcpyAsync(dst, shm_->slot(r.src_rank, cls, static_cast<int>(id % ring)), n,
+                           cudaMemcpyHostToDevice, recv_s));
+        rx += n;
+      }
+      mark_consumed(cls, recv_s, r.src_rank / g_, id);  // read it, or it was never ours to read
+    }
+  }
+  shm_->add(rank_, kStagingH2D, rx);
 }
 
 // ------------------------------------------------------------------ events
@@ -573,22 +605,17 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
     // already waited on this event's deps in run()), so the receive side below
     // overlaps with it.
     const std::size_t bt = wt ? l.my_real_t * C : 0, bf = wf ? l.my_real_f * C : 0;
-    const Counter ctr = backward ? kTxBwdAg : kTxFwdAg;
-    stage_pieces(0, s_agsend_, param_t_ + l.off_t * C, bt, N_ - 1, ctr);
-    stage_pieces(0, s_agsend_, param_f_ + l.off_f * C, bf, N_ - 1, ctr);
+    std::vector<Inbound> inbound;
     std::uint64_t rx = 0;
     for (int nn = 0; nn < N_; ++nn) {
-      const int src_rank = nn * g_ + j_;
+      if (nn == n_) continue;
       const int r = j_ * N_ + nn;
       const std::size_t rt = wt ? l.L.real_chunks(false, r) * C : 0, rf = wf ? l.L.real_chunks(true, r) * C : 0;
-      const std::uint32_t base = recv_base_[0][src_rank];
-      const std::uint32_t pt = static_cast<std::uint32_t>(pieces_of(rt));
-      recv_base_[0][src_rank] += pt + static_cast<std::uint32_t>(pieces_of(rf));
-      if (nn == n_) continue;
-      receive_pieces(0, s, src_rank, base + 1, rt, X + nn * l.L.dev.shard_t * C);
-      receive_pieces(0, s, src_rank, base + 1 + pt, rf, Xf + nn * l.L.dev.shard_f * C);
+      inbound.push_back({nn * g_ + j_, {{rt, X + nn * l.L.dev.shard_t * C}, {rf, Xf + nn * l.L.dev.shard_f * C}}});
       rx += rt + rf;
     }
+    exchange(0, s_agsend_, {{param_t_ + l.off_t * C, bt}, {param_f_ + l.off_f * C, bf}}, N_ - 1,
+             backward ? kTxBwdAg : kTxFwdAg, s, inbound);
     shm_->add(rank_, backward ? kRxBwdAg : kRxFwdAg, rx);
   }
   finish_slice_fill(slot, q);
@@ -784,31 +811,25 @@ void Engine::ev_reduce_scatter(const Event& e) {
   CK(cudaEventRecord(rs_kernel_done_[gs], s));
   CK(cudaStreamWaitEvent(s_rssend_, rs_kernel_done_[gs], 0));
   // region m (partials of shard j*N+m) goes to node m only; regions in ascending m
-  for (int nn = 0; nn < N_; ++nn) {
-    if (nn == n_) continue;
-    const std::size_t off = nn * l.L.dev.shard_t * C;
-    stage_pieces(1, s_rssend_, wire_[gs] + off, l.L.real_chunks(false, j_ * N_ + nn) * C, 1, kTxRs);
-  }
-  CK(cudaEventRecord(rs_staged_[gs], s_rssend_));  // wire_[gs] may be rewritten after this
+  std::vector<SendSeg> mine;
+  for (int nn = 0; nn < N_; ++nn)
+    if (nn != n_)
+      mine.push_back({wire_[gs] + nn * l.L.dev.shard_t * C, l.L.real_chunks(false, j_ * N_ + nn) * C});
+  std::vector<Inbound> inbound;
   std::uint64_t rx = 0;
   for (int nn = 0; nn < N_; ++nn) {
     if (nn == n_) continue;
-    const int src_rank = nn * g_ + j_;
-    // piece ids of sender (nn, j): its regions m != nn in ascending order; ours is m == n
-    std::uint32_t id = recv_base_[1][src_rank];
-    std::uint32_t mine_first = 0;
-    for (int m = 0; m < N_; ++m) {
+    Inbound ib{nn * g_ + j_, {}};
+    for (int m = 0; m < N_; ++m) {  // sender (nn, j)'s regions; only region n_ is ours
       if (m == nn) continue;
-      if (m == n_) mine_first = id + 1;
-      id += static_cast<std::uint32_t>(pieces_of(l.L.real_chunks(false, j_ * N_ + m) * C));
+      const std::size_t b = l.L.real_chunks(false, j_ * N_ + m) * C;
+      ib.segs.push_back({b, m == n_ ? rx_[gs] + nn * l.L.dev.shard_t * C : nullptr});
+      if (m == n_) rx += b;
     }
-    recv_base_[1][src_rank] = id;
-    mark_consumed(1, s, nn, mine_first - 1);  // pieces before our region are not ours to read
-    const std::size_t my = l.my_real_t * C;
-    receive_pieces(1, s, src_rank, mine_first, my, rx_[gs] + nn * l.L.dev.shard_t * C);
-    mark_consumed(1, s, nn, id);              // nor are the ones after it
-    rx += my;
+    inbound.push_back(std::move(ib));
   }
+  exchange(1, s_rssend_, mine, 1, kTxRs, s, inbound);
+  CK(cudaEventRecord(rs_staged_[gs], s_rssend_));  // wire_[gs] may be rewritten after this
   shm_->add(rank_, kRxRs, rx);
   const std::uint64_t fin_elems = static_cast<std::uint64_t>(l.L.dev.shard_t) * V_;
   timed(2, s, fin_elems * (2 * sizeof(float) + static_cast<std::uint64_t>(N_ - 1) * eb_), [&] {

@@ -112,11 +112,22 @@ class Engine {
   void wait_flag(cudaStream_t s, int rank, Flag f, std::uint32_t v);
   void write_flag(cudaStream_t s, Flag f, std::uint32_t v);
   std::int64_t pieces_of(std::size_t bytes) const;
-  void stage_pieces(int cls, cudaStream_t s, const void* src, std::size_t bytes, std::uint64_t wire_mult,
-                    Counter counter);
-  void receive_pieces(int cls, cudaStream_t s, int src_rank, std::uint32_t first_id, std::size_t bytes,
-                      unsigned char* dst);
+  struct SendSeg {
+    const void* src;
+    std::size_t bytes;
+  };
+  struct InSeg {
+    std::size_t bytes;
+    unsigned char* dst;  // null: part of the sender's message that is not for this rank
+  };
+  struct Inbound {
+    int src_rank;
+    std::vector<InSeg> segs;  // the sender's whole message, in its staging order
+  };
+  void stage_one(int cls, cudaStream_t s, const void* src, std::size_t n, std::uint64_t wire_mult, Counter counter);
   void mark_consumed(int cls, cudaStream_t s, int src_node, std::uint32_t id);
+  void exchange(int cls, cudaStream_t send_s, const std::vector<SendSeg>& mine, std::uint64_t wire_mult,
+                Counter counter, cudaStream_t recv_s, const std::vector<Inbound>& inbound);
   bool is_peer_rank(int r) const { return r / g_ == n_; }
 
   fcdp_engine_config cfg_;
