@@ -29,13 +29,15 @@ def main():
     ap.add_argument("--preset-model", default="gpt2-1.3b")
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--topologies", default="", help="comma list NxG (default: all with N*G == gpus)")
     ap.add_argument("--out", default="gpurun_out/sweep.jsonl")
     ap.add_argument("--per-run-timeout", type=int, default=240)
     a = ap.parse_args()
     out = Path(a.out)
     out.parent.mkdir(parents=True, exist_ok=True)
     port = 29600
-    for (N, g) in topologies(a.gpus):
+    topos = [tuple(int(x) for x in t.split("x")) for t in a.topologies.split(",")] if a.topologies else topologies(a.gpus)
+    for (N, g) in topos:
         for preset in a.presets.split(","):
             for strat in a.strategies.split(","):
                 port += 1
@@ -43,7 +45,7 @@ def main():
                        "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
                        "--gpus", str(a.gpus), "--topology", f"{N}x{g}", "--inter", preset, "--strategy", strat,
                        "--preset", a.preset_model, "--batch", str(a.batch), "--steps", str(a.steps),
-                       "--warmup", "1", "--no-zero3", "--no-e2e", "--no-cpu-baseline",
+                       "--warmup", "1", "--no-zero3", "--no-e2e", "--no-cpu-baseline", "--tau-variant", "0",
                        "--engine-timeout", "120", "--watchdog", str(a.per_run_timeout - 20)]
                 if a.gpus == 1:
                     cmd = [sys.executable, str(ROOT / "bench.py")] + cmd[cmd.index("--gpus"):]
