@@ -69,16 +69,20 @@ def env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """nvidia-smi clocks / throttle reasons during the timed region, for the GPUs this job uses."""
 
-    def __init__(self):
+    def __init__(self, world: int = 1):
         self.proc = None
         self.lines = []
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        ids = vis.split(",")[:world] if vis else [str(i) for i in range(world)]
+        self.ids = ",".join(ids)
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                ["nvidia-smi", "-i", self.ids,
+                 "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "200"],
@@ -114,7 +118,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "gpus": self.ids}
 
 
 def measured_peaks():
@@ -274,7 +278,7 @@ def main():
         tr.engine.kernel_stats(reset=True)
         tr.engine.set_timing(timing)
         barrier()
-        sampler = ClockSampler() if (rank == 0 and timing) else None
+        sampler = ClockSampler(world) if (rank == 0 and timing) else None
         if sampler:
             sampler.start()
         e0 = torch.cuda.Event(enable_timing=True)
