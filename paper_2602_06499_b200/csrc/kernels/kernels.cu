@@ -15,6 +15,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "kernels/kernels.hpp"
@@ -201,6 +203,17 @@ __global__ void __launch_bounds__(32) bulk_copy_kernel(BulkSegs segs) {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// TMA copies keep 128 KiB of shared memory per CTA, which cannot co-reside
+// with the driving model's GEMM CTAs; the SM copy (no smem, 32 registers)
+// slots in beside them.  FCDP_COPY=tma selects the TMA path.
+bool use_tma_copy() {
+  static const bool on = [] {
+    const char* v = std::getenv("FCDP_COPY");
+    return v && std::string(v) == "tma";
+  }();
+  return on;
 }
 
 cudaError_t launch_bulk(const BulkSegs& segs_in, cudaStream_t s) {
@@ -553,6 +566,11 @@ cudaError_t launch_expand(const Layout& L, const SlicePtrs& ts, const SlicePtrs&
     const bool tr = L.dense_trainable();
     if (tr ? !want_t : !want_f) return cudaSuccess;
     const std::int64_t per = tr ? L.dev.slice_t : L.dev.slice_f;
+    if (!use_tma_copy()) {
+      dim3 grid(std::max(1, grid_for(per, kThreads * kUnroll) / L.dev.local), L.dev.local);
+      concat_kernel<<<grid, kThreads, 0, s>>>(tr ? ts : fs, per, L.dev.chunks, out);
+      return cudaGetLastError();
+    }
     BulkSegs segs{};
     for (int j = 0; j < L.dev.local; ++j) {
       const std::int64_t lo = j * per;
@@ -666,7 +684,7 @@ cudaError_t launch_widen(std::int64_t n, const void* src, int elem_bytes, float*
 }
 
 cudaError_t launch_copy(const void* src, void* dst, std::int64_t bytes, cudaStream_t s) {
-  if (bytes % kChunkBytes == 0 && reinterpret_cast<std::uintptr_t>(src) % 16 == 0 &&
+  if (use_tma_copy() && bytes % kChunkBytes == 0 && reinterpret_cast<std::uintptr_t>(src) % 16 == 0 &&
       reinterpret_cast<std::uintptr_t>(dst) % 16 == 0) {
     BulkSegs segs{};
     segs.src[0] = static_cast<const unsigned char*>(src);
