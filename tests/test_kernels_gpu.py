@@ -184,3 +184,41 @@ def test_init_bit_exact(built, eb):
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), ref.view(np.uint8))
     lib.fcdp_layout_destroy(lay)
+
+
+_TMA_SCRIPT = r"""
+import ctypes as C, sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle as O
+from paper_2602_06499_b200 import _capi
+lib = _capi.lib()
+dev = torch.device("cuda", 0)
+rng = np.random.default_rng(3)
+for chunks, g in ((4099, 1), (100003, 4), (7, 2)):
+    m = np.ones(chunks, np.uint8)
+    geo = O.geom(chunks, m, 1, g)
+    lay = C.c_void_p()
+    _capi.check(lib.fcdp_layout_create(chunks, m.ctypes.data_as(C.POINTER(C.c_uint8)), 2, 1, g, C.byref(lay)))
+    ts = [rng.integers(0, 256, geo.slice_t * 16, dtype=np.uint8) for _ in range(g)]
+    ref = np.zeros(chunks * 16, np.uint8)
+    O.expand(geo, m, ts, [None] * g, ref, 0)
+    dts = [torch.from_numpy(x).to(dev) for x in ts]
+    out = torch.zeros(chunks * 16, dtype=torch.uint8, device=dev)
+    _capi.check(lib.fcdp_expand(lay, (C.c_void_p * g)(*[t.data_ptr() for t in dts]), None, C.c_void_p(out.data_ptr()), 0, None))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref), (chunks, g)
+print("tma-ok")
+"""
+
+
+def test_tma_bulk_copy_path(built):
+    """The TMA bulk-copy gather (FCDP_COPY=tma, read once per process) is bit-exact too."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    _dev()
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", _TMA_SCRIPT, root], env=dict(os.environ, FCDP_COPY="tma"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "tma-ok" in r.stdout, r.stdout + r.stderr
