@@ -56,10 +56,12 @@ def parse():
                    help="dump every thread's stack and exit if the run exceeds this many seconds")
     p.add_argument("--engine-timeout", type=float, default=300.0)
     p.add_argument("--no-pacing", action="store_true", help="do not throttle the emulated inter-node link")
-    p.add_argument("--tau", type=float, default=0.0,
-                   help="FCDP-Cache GPU-retention threshold of the headline run (0: pure host-cache path)")
-    p.add_argument("--tau-variant", type=float, default=0.9,
-                   help="also measure FCDP with adaptive GPU retention at this tau (0 disables)")
+    p.add_argument("--tau", type=float, default=0.9,
+                   help="FCDP-Cache adaptive GPU-retention threshold of the headline run (PAPER.md:455-462; "
+                        "capacity = this GPU's memory).  0 = every layer through the pinned host cache")
+    p.add_argument("--tau-variant", type=float, default=0.0,
+                   help="tau of the secondary FCDP run reported beside the headline (default 0: the pure "
+                        "host-cache path); negative disables")
     return p.parse_args()
 
 
@@ -173,6 +175,7 @@ def workload_config(args, mc, N, g, world, seq):
             "model": mc.name, "global_batch": args.batch * world, "seq_len": seq,
             "parallelism": f"{args.strategy} dp{world} ({N} emulated nodes x {g} GPUs)",
             "topology": f"{N}x{g}", "inter_link": args.inter, "strategy": args.strategy,
+            "fcdp_cache_tau": args.tau if args.strategy in ("fcdp", "fcdp-comm") else None,
             "l2": "inputs larger than L2 (layer params, host cache, optimizer state >> 126 MB)"}
 
 
@@ -332,9 +335,11 @@ def main():
 
     if args.batch <= 0:
         args.batch = zero3_max_batch()
+    if args.strategy not in ("fcdp", "fcdp-comm"):
+        args.tau = 0.0
     main_run = measure(args.strategy, args.steps, args.warmup, True, 0 if args.no_e2e else args.steps, args.tau)
     tau_run = None
-    if args.tau_variant > 0 and args.strategy in ("fcdp", "fcdp-comm") and args.tau == 0:
+    if args.tau_variant >= 0 and args.strategy in ("fcdp", "fcdp-comm") and args.tau_variant != args.tau:
         tau_run = measure(args.strategy, args.zero3_steps, 2, False, 0, args.tau_variant)
     z3 = None
     if not args.no_zero3 and args.strategy != "zero3":
@@ -399,7 +404,7 @@ def main():
                     "ag_inter_fwd_bwd": [zpp["node_tx"]["nic_tx_fwd_ag"], zpp["node_tx"]["nic_tx_bwd_ag"]]}
                    if zpp else None),
         "cache_bytes_per_step_per_node": main_run["cache"],
-        "fcdp_gpu_retention": ({"tau": args.tau_variant, "tokens_per_s": tokens_per_step / (tau_run["ms"] / args.zero3_steps / 1e3),
+        "fcdp_variant": ({"tau": args.tau_variant, "tokens_per_s": tokens_per_step / (tau_run["ms"] / args.zero3_steps / 1e3),
                                 "ms_per_step": tau_run["ms"] / args.zero3_steps, "cache": tau_run["cache"],
                                 "ag_inter_fwd_bwd": [tau_run["node_tx"]["nic_tx_fwd_ag"], tau_run["node_tx"]["nic_tx_bwd_ag"]]}
                                if tau_run else None),

@@ -37,7 +37,19 @@ class FcdpTrainer:
         self.batch, self.seq = batch_per_gpu, seq_len or cfg.seq
         self.dtype = torch.bfloat16 if cfg.dtype_bytes == 2 else torch.float32
         self.defs: List[LayerDef] = cfg.layer_defs()
-        layers = [S.LayerSpec(i, d.numel, d.trainable_params() / d.numel) for i, d in enumerate(self.defs)]
+        # activation bytes per sample feed the tau-admission projection
+        # (schedule.cpp:196-208); a bf16 transformer block with flash attention
+        # keeps about 34 * seq * hidden bytes, the head its logits (+ fp32 copy).
+        ffn = cfg.ffn or 4 * cfg.hidden
+
+        def act(d: LayerDef) -> int:
+            if d.kind == "head":
+                return self.seq * cfg.vocab_rows * 6
+            if d.kind == "embed":
+                return self.seq * cfg.hidden * 2
+            return int(self.seq * cfg.hidden * 34 * max(1.0, ffn / (4 * cfg.hidden)))
+        layers = [S.LayerSpec(i, d.numel, d.trainable_params() / d.numel, activation_bytes_per_sample=act(d))
+                  for i, d in enumerate(self.defs)]
         self.model = S.ModelSpec(layers, cfg.dtype_bytes, batch_per_gpu=batch_per_gpu)
         self.gpu_capacity_bytes = gpu_capacity_bytes
         self.engine = Engine(self.model, topo, plan, rank=rank, world_size=world_size, device=device,
