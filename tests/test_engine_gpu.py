@@ -155,9 +155,22 @@ def test_engine_even_shards_match_comm_volume(tmp_path, built):
     check_job(cfg, dumps)
 
 
-def test_engine_tau_retention(tmp_path, built):
-    """tau = 1, unlimited capacity: every layer retained, no backward reload."""
-    cfg, dumps = run_job(tmp_path, 1, 1, "fcdp", 2, "dense", tau=1.0)
+@pytest.mark.parametrize("N,g,strategy,kind", [(1, 1, "fcdp", "dense"), (2, 1, "fcdp-comm", "lora"),
+                                                (2, 2, "fcdp", "lora")])
+def test_engine_tau_retention(tmp_path, built, N, g, strategy, kind):
+    """tau = 1, unlimited capacity: every layer retained, no backward reload
+    (FCDP-Cache adaptive GPU caching; schedule.cpp:196-223)."""
+    if N * g > _ngpu():
+        pytest.skip(f"needs {N * g} GPUs")
+    cfg, dumps = run_job(tmp_path, N, g, strategy, 2, kind, tau=1.0)
     check_job(cfg, dumps)
     for d in dumps[0]:
         assert all(f & 1 for f in d["retained"])
+
+
+def test_engine_tau_partial_capacity(tmp_path, built):
+    """A capacity that admits only some layers: mixed retained / host-cache layers."""
+    cfg, dumps = run_job(tmp_path, 1, 1, "fcdp", 2, "dense", tau=0.5, capacity=900_000)  # retains the last layer only
+    check_job(cfg, dumps)
+    flags = dumps[0][-1]["retained"]
+    assert any(f & 1 for f in flags) and not all(f & 1 for f in flags), flags
