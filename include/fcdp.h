@@ -302,7 +302,6 @@ int fcdp_engine_read_shard(fcdp_engine* e, int32_t layer, int32_t frozen, void* 
 int fcdp_engine_read_master(fcdp_engine* e, int32_t layer, float* host, size_t count);
 int fcdp_engine_read_grad(fcdp_engine* e, int32_t layer, float* host, size_t count);
 int fcdp_engine_read_host_cache(fcdp_engine* e, int32_t layer, int32_t frozen, void* host, size_t bytes);
-int fcdp_engine_last_gathered(fcdp_engine* e, int32_t layer, void* host, size_t bytes);
 void fcdp_engine_destroy(fcdp_engine* e);
 
 /* Per-kernel-class launch counts, CUDA-event device time and algorithmic bytes

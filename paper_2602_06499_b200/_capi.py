@@ -162,7 +162,6 @@ SIGNATURES = {
     "fcdp_engine_read_master": (C.c_int, [P, i32, P, C.c_size_t]),
     "fcdp_engine_read_grad": (C.c_int, [P, i32, P, C.c_size_t]),
     "fcdp_engine_read_host_cache": (C.c_int, [P, i32, i32, P, C.c_size_t]),
-    "fcdp_engine_last_gathered": (C.c_int, [P, i32, P, C.c_size_t]),
     "fcdp_engine_destroy": (None, [P]),
     "fcdp_engine_set_timing": (C.c_int, [P, i32]),
     "fcdp_engine_kernel_stats": (C.c_int, [P, C.POINTER(KernelStats), i32]),

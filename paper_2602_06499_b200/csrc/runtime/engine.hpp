@@ -47,7 +47,6 @@ struct LayerRt {
   std::int64_t slice_real_t = 0, slice_real_f = 0;
   std::uint64_t shard_version_t = 0;          // version of this rank's trainable shard
   std::int64_t host_version_t = -1, host_version_f = -1;  // versions in the host cache (-1 none)
-  std::int8_t retained_slot = -1;
   std::int64_t replica_version_t = -1;   // ZeRO++: version in this GPU's HBM replica slice
   std::uint32_t last_replica_pull_q = 0; // ZeRO++: gather seq of the last backward pull
 };
@@ -128,7 +127,6 @@ class Engine {
   void mark_consumed(int cls, cudaStream_t s, int src_node, std::uint32_t id);
   void exchange(int cls, cudaStream_t send_s, const std::vector<SendSeg>& mine, std::uint64_t wire_mult,
                 Counter counter, cudaStream_t recv_s, const std::vector<Inbound>& inbound);
-  bool is_peer_rank(int r) const { return r / g_ == n_; }
 
   fcdp_engine_config cfg_;
   std::string shm_name_;
@@ -177,7 +175,6 @@ class Engine {
   std::uint32_t recv_base_[2][64] = {};           // replica of every sender's piece counter
   std::uint32_t consumed_[2][8] = {};             // last consumed marker written, per sender node
   std::uint64_t w_instances_ = 0;
-  std::uint32_t grad_slot_seq_ = 0;
   int opt_steps_ = 0;
 
   // per-iteration bookkeeping

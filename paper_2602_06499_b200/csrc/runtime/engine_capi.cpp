@@ -76,13 +76,6 @@ int fcdp_engine_read_host_cache(fcdp_engine* e, int32_t layer, int32_t frozen, v
   return guarded([&] { E(e).read_host_cache(layer, frozen != 0, host, bytes); });
 }
 
-int fcdp_engine_last_gathered(fcdp_engine* e, int32_t, void*, size_t) {
-  return guarded([&] {
-    E(e);
-    throw shardsim::ConfigError("engine: capture gathered layers in the compute callback instead");
-  });
-}
-
 int fcdp_engine_set_timing(fcdp_engine* e, int32_t on) { return guarded([&] { E(e).set_timing(on != 0); }); }
 
 int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t reset) {
