@@ -274,6 +274,7 @@ typedef struct fcdp_counters {
   uint64_t staging_h2d, staging_d2h;                   /* NIC-emulator host staging bytes */
   uint64_t ag_inter_events_fwd, ag_inter_events_bwd;
   uint64_t nic_busy_ns;                                /* paced wire time charged by this rank */
+  uint64_t resident_hits;  /* frozen reloads elided: portion already resident in a tau-retained buffer */
 } fcdp_counters;
 
 /* Compute callback: `kind` FCDP_EV_COMPUTE_FWD/BWD.  `weights` is the natural

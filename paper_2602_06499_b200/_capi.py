@@ -86,7 +86,7 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs", "nic_rx_fwd_ag", "nic_rx_bwd_ag", "nic_rx_rs",
         "nvlink_rx", "cache_h2d", "cache_d2h", "staging_h2d", "staging_d2h",
-        "ag_inter_events_fwd", "ag_inter_events_bwd", "nic_busy_ns")]
+        "ag_inter_events_fwd", "ag_inter_events_bwd", "nic_busy_ns", "resident_hits")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

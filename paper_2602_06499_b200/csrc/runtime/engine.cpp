@@ -39,6 +39,8 @@ using shardsim::Event;
 using shardsim::EventKind;
 using shardsim::ParamSet;
 
+constexpr int kElided = -2;  // PendingSlice::slot of an elided (resident) reload
+
 std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
 
 template <typename T>
@@ -647,6 +649,19 @@ void Engine::ev_h2d(const Event& e) {
   if (wf && l.host_version_f != 0)
     throw shardsim::ProtocolError("freshness: layer " + std::to_string(e.layer) +
                                   " frozen portion reloaded before it was cached");
+  // Frozen residency: a tau-retained layer whose retained buffer already holds
+  // the frozen portion (version 0 forever) needs no reload -
+  // the event's postcondition already holds.  Trainable data always moves.
+  if (!wt && wf && prog_->layer_retained[e.layer] && retained_[e.layer] &&
+      retained_content_[e.layer].layer == e.layer && retained_content_[e.layer].ver_f == 0) {
+    PendingSlice& p = pending_h2d_[e.layer];
+    p.slot = kElided;
+    p.t = false;
+    p.f = true;
+    p.ver_f = 0;
+    shm_->add(rank_, kResidentHits, 1);
+    return;
+  }
   const std::size_t C = kChunkBytes;
   const int slot = begin_slice_fill(e.layer);
   const std::uint32_t q = q_;
@@ -702,6 +717,11 @@ void Engine::ev_ag_intra(const Event& e) {
     return;
   }
   PendingSlice p = pending_h2d_[e.layer];
+  if (p.slot == kElided) {  // frozen portion already resident in the retained buffer
+    w_buffer(e.layer);
+    pending_h2d_[e.layer] = {};
+    return;
+  }
   if (p.slot < 0) throw shardsim::ProtocolError("ag_intra without a preceding h2d for layer " + std::to_string(e.layer));
   pull_expand(e.layer, p.slot, p.q, p.t, p.f, s_gather_);
   WContent& wc = w_of_layer_[e.layer] == 2 ? retained_content_[e.layer] : w_content_[w_of_layer_[e.layer]];
@@ -991,6 +1011,7 @@ void Engine::counters(int rank, fcdp_counters* o) const {
   o->ag_inter_events_fwd = shm_->counter(rank, kAgEventsFwd);
   o->ag_inter_events_bwd = shm_->counter(rank, kAgEventsBwd);
   o->nic_busy_ns = shm_->counter(rank, kNicBusyNs);
+  o->resident_hits = shm_->counter(rank, kResidentHits);
 }
 
 void Engine::reset_counters() { shm_->reset_counters(rank_); }

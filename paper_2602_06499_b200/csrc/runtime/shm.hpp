@@ -40,7 +40,7 @@ enum Flag : int {
 
 enum Counter : int {
   kTxFwdAg = 0, kTxBwdAg, kTxRs, kRxFwdAg, kRxBwdAg, kRxRs, kNvlinkRx, kCacheH2D, kCacheD2H,
-  kStagingH2D, kStagingD2H, kAgEventsFwd, kAgEventsBwd, kNicBusyNs, kNumCounters
+  kStagingH2D, kStagingD2H, kAgEventsFwd, kAgEventsBwd, kNicBusyNs, kResidentHits, kNumCounters
 };
 
 struct alignas(64) FlagLine {

@@ -63,6 +63,7 @@ class Sim:
                 self.m[r][l] = np.zeros_like(self.master[r][l])
                 self.v[r][l] = np.zeros_like(self.master[r][l])
         self.step = 0
+        self.prev_retained = [False] * self.L
 
     def shard_index(self, rank):
         n, j = divmod(rank, self.g)
@@ -100,6 +101,11 @@ class Sim:
                 "counters": {k: 0 for k in ("nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs", "cache_h2d",
                                             "cache_d2h", "nvlink_rx")}} for _ in range(self.G)]
         last_fwd = max(e.id for e in prog.events if e.kind == S.EventKind.ComputeFwd)
+        retained = [bool(f & 1) for f in prog.layer_flags(self.L)]
+
+        def resident(e):  # engine elides frozen-only reloads of layers retained twice in a row
+            frozen_only = e.param_set == S.ParamSet.FrozenOnly or (e.param_set == S.ParamSet.All and self.geo[e.layer].pt == 0)
+            return frozen_only and retained[e.layer] and self.prev_retained[e.layer]
         nat_now = [self.natural(l) for l in range(self.L)]
         grads = {}
         for e in prog.events:
@@ -134,6 +140,10 @@ class Sim:
                     key = "nic_tx_bwd_ag" if e.id > last_fwd else "nic_tx_fwd_ag"
                     exp[r]["counters"][key] += b * 16 * (self.N - 1)
                     exp[r]["counters"]["nvlink_rx"] += self._nvl(l, r, e.param_set)
+            elif e.kind == S.EventKind.H2D and resident(e):
+                pass
+            elif e.kind == S.EventKind.AgIntra and resident(e):
+                pass
             elif e.kind == S.EventKind.H2D:
                 for r in range(self.G):
                     j = r % self.g
@@ -164,6 +174,7 @@ class Sim:
                 exp[r]["shard_f"][l] = self.shard_f[r][l]
                 exp[r]["grad"][l] = self.grad[r][l] if hasattr(self, "grad") else None
         new_states = S.step_state(states, prog)
+        self.prev_retained = retained
         return exp, new_states, prog
 
     def _real(self, l, frozen, s):
