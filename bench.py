@@ -284,17 +284,18 @@ def main():
         sampler = ClockSampler(world) if (rank == 0 and timing) else None
         if sampler:
             sampler.start()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        e0, e1 = evs[0], evs[-1]
         e0.record(tr.stream)
         for i in range(steps):
             loss = tr.step(*batches[warmup + i])
-        e1.record(tr.stream)
+            evs[i + 1].record(tr.stream)
         tr.sync()
         torch.cuda.synchronize()
         barrier()
         clocks = sampler.stop() if sampler else None
         ms = max_over_ranks(e0.elapsed_time(e1))
+        per_step = [round(evs[i].elapsed_time(evs[i + 1]), 3) for i in range(steps)]
         counters = tr.engine.counters()
         kst = tr.engine.kernel_stats(reset=True)
         tr.engine.set_timing(False)
@@ -330,7 +331,7 @@ def main():
         tr.close()
         del tr
         torch.cuda.empty_cache()
-        return {"ms": ms, "counters": counters, "kernels": kst, "clocks": clocks, "loss": loss_v,
+        return {"ms": ms, "per_step": per_step, "counters": counters, "kernels": kst, "clocks": clocks, "loss": loss_v,
                 "node_tx": node_tx, "cache": cache, "vol": vol, "e2e": e2e}
 
     if args.batch <= 0:
@@ -408,7 +409,7 @@ def main():
                                 "ms_per_step": tau_run["ms"] / args.zero3_steps, "cache": tau_run["cache"],
                                 "ag_inter_fwd_bwd": [tau_run["node_tx"]["nic_tx_fwd_ag"], tau_run["node_tx"]["nic_tx_bwd_ag"]]}
                                if tau_run else None),
-        "kernels": kernels, "loss": main_run["loss"],
+        "kernels": kernels, "loss": main_run["loss"], "ms_each_step_rank0": main_run["per_step"],
     }
     print(json.dumps(line), flush=True)
     if world > 1:
