@@ -372,11 +372,20 @@ def main():
     d = kst[dom]
     per_launch_bytes = d["alg_bytes"] / max(d["launches"], 1)
     per_launch_ms = d["ms"] / max(d["timed_launches"], 1)
-    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": (achieved / hbm) if (achieved and hbm) else None,
-                "traffic": ncu_traffic(dom), "alg_bytes_per_launch": per_launch_bytes,
-                "ms_per_launch": per_launch_ms, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)",
+    nvlink_bound = d.get("link_bytes", 0) > 0 and g > 1
+    if nvlink_bound:
+        # an intra-node gather / pull-reduce: bounded by NVLink ingress, not HBM
+        link_per_launch = d["link_bytes"] / max(d["launches"], 1)
+        achieved = link_per_launch / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else None
+        peak, unit_peak, src = 770.0, "GB/s", ("B200_PROFILING.md measured NVLink peer copy, 770 GB/s per direction "
+                                               "(900 nominal); achieved = NVLink ingress bytes / launch time")
+    else:
+        achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else None
+        peak, unit_peak, src = hbm, "GB/s", "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    roofline = {"bound": "nvlink" if nvlink_bound else "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": unit_peak, "frac": (achieved / peak) if (achieved and peak) else None,
+                "traffic": ncu_traffic(dom) if not nvlink_bound else None, "alg_bytes_per_launch": per_launch_bytes,
+                "ms_per_launch": per_launch_ms, "peak_source": src,
                 "share_of_step": d["ms"] / main_run["ms"] if main_run["ms"] else None}
     gpu_launches = sum(v["launches"] for v in kst.values())
     ag = {"fcdp_fwd": main_run["node_tx"]["nic_tx_fwd_ag"], "fcdp_bwd": main_run["node_tx"]["nic_tx_bwd_ag"],

@@ -307,13 +307,16 @@ void fcdp_engine_destroy(fcdp_engine* e);
 
 /* Per-kernel-class launch counts, CUDA-event device time and algorithmic bytes
  * of the engine's own kernels.  Classes: 0 gather/expand (intra all-gather),
- * 1 reduce-scatter slice (pull-reduce), 2 reduce-scatter finalize, 3 AdamW. */
-#define FCDP_KCLASSES 4
+ * 1 reduce-scatter slice (pull-reduce), 2 reduce-scatter finalize, 3 AdamW,
+ * 4 local shard copies (pack into the slice buffer, ZeRO++ replica).
+ * link_bytes: the part of the traffic that crossed NVLink (peer reads). */
+#define FCDP_KCLASSES 5
 typedef struct fcdp_kernel_stats {
   uint64_t launches[FCDP_KCLASSES];
   double total_ms[FCDP_KCLASSES];  /* only while timing is on */
   uint64_t alg_bytes[FCDP_KCLASSES];
   uint64_t timed_launches[FCDP_KCLASSES];
+  uint64_t link_bytes[FCDP_KCLASSES];
 } fcdp_kernel_stats;
 int fcdp_engine_set_timing(fcdp_engine* e, int32_t on);
 int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t reset);

@@ -62,7 +62,7 @@ bool wants_f(ParamSet s) { return s != ParamSet::TrainableOnly; }
 }  // namespace
 
 template <typename F>
-void Engine::timed(int cls, cudaStream_t s, std::uint64_t alg_bytes, F&& launch) {
+void Engine::timed(int cls, cudaStream_t s, std::uint64_t alg_bytes, F&& launch, std::uint64_t link_bytes) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (timing_) {
     for (cudaEvent_t* e : {&a, &b}) {
@@ -78,6 +78,7 @@ void Engine::timed(int cls, cudaStream_t s, std::uint64_t alg_bytes, F&& launch)
   CK(launch());
   kstats_.launches[cls] += 1;
   kstats_.alg_bytes[cls] += alg_bytes;
+  kstats_.link_bytes[cls] += link_bytes;
   if (timing_) {
     CK(cudaEventRecord(b, s));
     timed_pending_.push_back({cls, a, b, alg_bytes});
@@ -469,6 +470,12 @@ void Engine::pull_expand(int layer, int slot, std::uint32_t q, bool want_t, bool
     fs.p[jj] = x_slot(jj, slot) + l.L.dev.slice_t * kChunkBytes;
   }
   const int set = want_t && want_f ? kSetAll : (want_t ? kSetTrainable : kSetFrozen);
+  std::uint64_t rx = 0;  // bytes this GPU pulls from its NVLink peers
+  for (int jj = 0; jj < g_; ++jj) {
+    if (jj == j_) continue;
+    if (want_t) rx += l.L.real_slice_chunks(false, jj) * kChunkBytes;
+    if (want_f) rx += l.L.real_slice_chunks(true, jj) * kChunkBytes;
+  }
   const bool dense = l.L.dense_trainable() || l.L.dense_frozen();
   if (use_ce_ && dense) {
     const bool tr = l.L.dense_trainable();
@@ -484,15 +491,9 @@ void Engine::pull_expand(int layer, int slot, std::uint32_t q, bool want_t, bool
     std::uint64_t out_bytes = 0;
     if (want_t) out_bytes += l.L.dev.pt * kChunkBytes;
     if (want_f) out_bytes += l.L.dev.pf * kChunkBytes;
-    timed(0, s, 2 * out_bytes, [&] { return launch_expand(l.L, ts, fs, W, set, s); });
+    timed(0, s, 2 * out_bytes, [&] { return launch_expand(l.L, ts, fs, W, set, s); }, rx);
   }
   write_flag(s, kSliceFree, q);
-  std::uint64_t rx = 0;
-  for (int jj = 0; jj < g_; ++jj) {
-    if (jj == j_) continue;
-    if (want_t) rx += l.L.real_slice_chunks(false, jj) * kChunkBytes;
-    if (want_f) rx += l.L.real_slice_chunks(true, jj) * kChunkBytes;
-  }
   shm_->add(rank_, kNvlinkRx, rx);
 }
 
@@ -594,11 +595,11 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
   // (an SM copy, not cudaMemcpy: the copy engines are busy with FCDP-Cache D2H
   //  and host-staged NIC traffic, and a D2D queued behind them stalls the gather)
   if (wt && l.my_real_t)
-    timed(0, s, 2 * l.my_real_t * C, [&] {
+    timed(4, s, 2 * l.my_real_t * C, [&] {
       return launch_copy(param_t_ + l.off_t * C, X + n_ * l.L.dev.shard_t * C, l.my_real_t * C, s);
     });
   if (wf && l.my_real_f)
-    timed(0, s, 2 * l.my_real_f * C, [&] {
+    timed(4, s, 2 * l.my_real_f * C, [&] {
       return launch_copy(param_f_ + l.off_f * C, Xf + n_ * l.L.dev.shard_f * C, l.my_real_f * C, s);
     });
   if (N_ > 1) {
@@ -634,7 +635,7 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
       for (int jj = 0; jj < g_; ++jj)
         if (jj != j_) wait_flag(s, n_ * g_ + jj, kSliceFree, l.last_replica_pull_q);
     const std::size_t bytes = (l.L.dev.slice_t + l.L.dev.slice_f) * C;
-    timed(0, s, 2 * bytes, [&] { return launch_copy(X, replica(j_, e.layer), bytes, s); });
+    timed(4, s, 2 * bytes, [&] { return launch_copy(X, replica(j_, e.layer), bytes, s); });
     l.replica_version_t = static_cast<std::int64_t>(l.shard_version_t);
   }
 }
@@ -704,8 +705,11 @@ void Engine::ev_ag_intra(const Event& e) {
       ts.p[jj] = replica(jj, e.layer);
       fs.p[jj] = replica(jj, e.layer) + l.L.dev.slice_t * kChunkBytes;
     }
+    std::uint64_t prx = 0;
+    for (int jj = 0; jj < g_; ++jj)
+      if (jj != j_) prx += (l.L.real_slice_chunks(false, jj) + l.L.real_slice_chunks(true, jj)) * kChunkBytes;
     timed(0, s_gather_, 2 * l.chunks * kChunkBytes,
-          [&] { return launch_expand(l.L, ts, fs, W, kSetAll, s_gather_); });
+          [&] { return launch_expand(l.L, ts, fs, W, kSetAll, s_gather_); }, prx);
     write_flag(s_gather_, kSliceFree, q);
     l.last_replica_pull_q = q;
     std::uint64_t rx = 0;
@@ -815,9 +819,11 @@ void Engine::ev_reduce_scatter(const Event& e) {
                                  static_cast<std::uint64_t>(l.my_real_t) * V_ * sizeof(float) +
                                  static_cast<std::uint64_t>(l.slice_real_t - l.my_real_t) * C;
   if (N_ == 1) {
-    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, 0, scale, true, final_out, wire_[gs], s); });
+    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, 0, scale, true, final_out, wire_[gs], s); },
+          static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
   } else {
-    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, n_, scale, false, own32_[gs], wire_[gs], s); });
+    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, n_, scale, false, own32_[gs], wire_[gs], s); },
+          static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
   }
   write_flag(s, kGradFree, u);
   CK(cudaEventRecord(rs_done_[gs], s));

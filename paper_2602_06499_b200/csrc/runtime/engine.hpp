@@ -202,7 +202,7 @@ class Engine {
 
   // kernel accounting (launch counts always, event timing when enabled)
   template <typename F>
-  void timed(int cls, cudaStream_t s, std::uint64_t alg_bytes, F&& launch);
+  void timed(int cls, cudaStream_t s, std::uint64_t alg_bytes, F&& launch, std::uint64_t link_bytes = 0);
   struct TimedLaunch {
     int cls;
     cudaEvent_t a, b;

@@ -121,7 +121,7 @@ class Engine:
     def reset_counters(self) -> None:
         check(lib().fcdp_engine_reset_counters(self._h))
 
-    KERNEL_CLASSES = ("gather_expand", "rs_slice", "rs_finalize", "adamw")
+    KERNEL_CLASSES = ("gather_expand", "rs_slice", "rs_finalize", "adamw", "shard_copy")
 
     def set_timing(self, on: bool) -> None:
         check(lib().fcdp_engine_set_timing(self._h, int(on)))
@@ -130,7 +130,8 @@ class Engine:
         k = _capi.KernelStats()
         check(lib().fcdp_engine_kernel_stats(self._h, C.byref(k), int(reset)))
         return {name: {"launches": int(k.launches[i]), "ms": float(k.total_ms[i]),
-                       "alg_bytes": int(k.alg_bytes[i]), "timed_launches": int(k.timed_launches[i])}
+                       "alg_bytes": int(k.alg_bytes[i]), "timed_launches": int(k.timed_launches[i]),
+                       "link_bytes": int(k.link_bytes[i])}
                 for i, name in enumerate(self.KERNEL_CLASSES)}
 
     def set_trace(self, on: bool) -> None:
