@@ -155,8 +155,9 @@ def test_engine_even_shards_match_comm_volume(tmp_path, built):
     check_job(cfg, dumps)
 
 
-@pytest.mark.parametrize("N,g,strategy,kind", [(1, 1, "fcdp", "dense"), (2, 1, "fcdp-comm", "lora"),
-                                                (2, 2, "fcdp", "lora")])
+@pytest.mark.parametrize("N,g,strategy,kind", [(1, 1, "fcdp", "dense"), (1, 1, "fcdp-comm", "lora"),
+                                                (2, 1, "fcdp-comm", "lora"), (2, 2, "fcdp", "lora"),
+                                                (2, 2, "fcdp-comm", "random")])
 def test_engine_tau_retention(tmp_path, built, N, g, strategy, kind):
     """tau = 1, unlimited capacity: every layer retained, no backward reload
     (FCDP-Cache adaptive GPU caching; schedule.cpp:196-223)."""
@@ -166,6 +167,10 @@ def test_engine_tau_retention(tmp_path, built, N, g, strategy, kind):
     check_job(cfg, dumps)
     for d in dumps[0]:
         assert all(f & 1 for f in d["retained"])
+    if strategy == "fcdp-comm":
+        # from iteration 2 on, every frozen reload is satisfied by the resident buffer
+        assert all(d["counters"]["resident_hits"] > 0 for d in dumps[0][1:])
+        assert all(d["counters"]["cache_h2d"] == 0 for d in dumps[0][1:])
 
 
 def test_engine_tau_partial_capacity(tmp_path, built):
