@@ -104,22 +104,26 @@ __global__ void __launch_bounds__(kThreads) expand_kernel(LayoutDev L, SlicePtrs
 // the real chunk count).  blockIdx.y selects the source slice.
 __global__ void __launch_bounds__(kThreads) concat_kernel(SlicePtrs src, std::int64_t per,
                                                           std::int64_t total, uint4* __restrict__ out) {
+  // Block-contiguous tiles of kThreads*kUnroll chunks (16 KiB): a warp's kUnroll
+  // loads hit consecutive 512 B segments of one tile, so DRAM pages stay open.
   const int j = blockIdx.y;
   const std::int64_t lo = j * per;
   if (lo >= total) return;
   const std::int64_t n = std::min(per, total - lo);
-  const uint4* s = pick(src, j);
-  uint4* d = out + lo;
-  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+  const uint4* __restrict__ s = pick(src, j);
+  uint4* __restrict__ d = out + lo;
+  constexpr std::int64_t kTile = static_cast<std::int64_t>(kThreads) * kUnroll;
+  const std::int64_t tiles = (n + kTile - 1) / kTile;
+  for (std::int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const std::int64_t base = t * kTile + threadIdx.x;
     uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = s[i + u * stride];
+    for (int u = 0; u < kUnroll; ++u)
+      if (base + u * kThreads < n) v[u] = __ldcs(s + base + u * kThreads);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) d[i + u * stride] = v[u];
+    for (int u = 0; u < kUnroll; ++u)
+      if (base + u * kThreads < n) d[base + u * kThreads] = v[u];
   }
-  for (; i < n; i += stride) d[i] = s[i];
 }
 
 // ---------------------------------------------------------- TMA bulk copy
@@ -523,16 +527,18 @@ __global__ void __launch_bounds__(kThreads) init_kernel(std::int64_t n, std::uin
 
 __global__ void __launch_bounds__(kThreads) copy_kernel(const uint4* __restrict__ s, uint4* __restrict__ d,
                                                         std::int64_t n) {
-  const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + (kUnroll - 1) * stride < n; i += kUnroll * stride) {
+  constexpr std::int64_t kTile = static_cast<std::int64_t>(kThreads) * kUnroll;
+  const std::int64_t tiles = (n + kTile - 1) / kTile;
+  for (std::int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const std::int64_t base = t * kTile + threadIdx.x;
     uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = s[i + u * stride];
+    for (int u = 0; u < kUnroll; ++u)
+      if (base + u * kThreads < n) v[u] = __ldcs(s + base + u * kThreads);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) d[i + u * stride] = v[u];
+    for (int u = 0; u < kUnroll; ++u)
+      if (base + u * kThreads < n) d[base + u * kThreads] = v[u];
   }
-  for (; i < n; i += stride) d[i] = s[i];
 }
 
 }  // namespace
