@@ -204,7 +204,19 @@ Engine::~Engine() {
     if (l.d_bits) cudaFree(l.d_bits);
     if (l.d_tpre) cudaFree(l.d_tpre);
   }
-  if (host_cache_) cudaFreeHost(host_cache_);
+  for (auto& ev : cache_staged_)
+    if (ev) cudaEventDestroy(ev);
+  for (int nn = 0; nn < kMaxNodes; ++nn)
+    if (hc_peer_[nn]) {
+      cudaHostUnregister(hc_peer_[nn]->base());
+      hc_peer_[nn].reset();
+    }
+  if (hc_own_) {
+    cudaHostUnregister(hc_own_->base());
+    hc_own_.reset();
+  } else if (host_cache_) {
+    cudaFreeHost(host_cache_);
+  }
   if (shm_) cudaHostUnregister(shm_->base());
   shm_.reset();
 }
@@ -296,13 +308,29 @@ void Engine::allocate() {
     wire_[i] = dalloc<unsigned char>(max_slice_t_ * C, "rs wire");
     rx_[i] = dalloc<unsigned char>(static_cast<std::size_t>(N_) * max_shard_t_ * C, "rs rx");
   }
-  const cudaError_t e = cudaHostAlloc(&host_cache_, std::max<std::size_t>(host_chunks_ * C, 4096),
-                                      cudaHostAllocPortable);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    throw OomError("cudaHostAlloc(host cache, " + std::to_string(host_chunks_ * C) + " B) failed");
+  shared_cache_ = N_ > 1 && (plan_.kind == shardsim::StrategyKind::Fcdp || plan_.kind == shardsim::StrategyKind::FcdpComm);
+  if (shared_cache_) {
+    hc_own_ = std::make_unique<ShmSegment>(shm_name_ + "_hc" + std::to_string(rank_), host_chunks_ * C, true,
+                                           cfg_.timeout_s);
+    host_cache_ = hc_own_->base();
+    CK(cudaHostRegister(host_cache_, hc_own_->bytes(), cudaHostRegisterPortable));
+  } else {
+    const cudaError_t e = cudaHostAlloc(&host_cache_, std::max<std::size_t>(host_chunks_ * C, 4096),
+                                        cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw OomError("cudaHostAlloc(host cache, " + std::to_string(host_chunks_ * C) + " B) failed");
+    }
   }
   std::memset(host_cache_, 0, host_chunks_ * C);
+  hc_base_[n_] = host_cache_;
+  const std::size_t L = layers_.size();
+  cache_stage_t_.assign(L, 0);
+  cache_stage_f_.assign(L, 0);
+  cache_last_id_t_.assign(L, 0);
+  cache_last_id_f_.assign(L, 0);
+  cache_staged_.assign(L, nullptr);
+  for (auto& ev : cache_staged_) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
 }
 
 void Engine::exchange_handles() {
@@ -327,6 +355,14 @@ void Engine::exchange_handles() {
     CK(cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess));
     peer_base_[jj] = static_cast<unsigned char*>(p);
   }
+  if (shared_cache_)
+    for (int nn = 0; nn < N_; ++nn) {
+      if (nn == n_) continue;
+      hc_peer_[nn] = std::make_unique<ShmSegment>(shm_name_ + "_hc" + std::to_string(nn * g_ + j_),
+                                                  host_chunks_ * kChunkBytes, false, cfg_.timeout_s);
+      hc_base_[nn] = hc_peer_[nn]->base();
+      CK(cudaHostRegister(hc_base_[nn], hc_peer_[nn]->bytes(), cudaHostRegisterPortable));
+    }
 }
 
 void Engine::init_params(std::uint64_t seed, const fcdp_init_range* const* ranges, const int32_t* num_ranges) {
@@ -503,7 +539,7 @@ std::int64_t Engine::pieces_of(std::size_t bytes) const {
 }
 
 void Engine::stage_one(int cls, cudaStream_t s, const void* src, std::size_t n, std::uint64_t wire_mult,
-                       Counter counter) {
+                       Counter counter, unsigned char* host_dst) {
   // Pipelined host-staged wire: the piece is staged into the next slot of
   // this rank's ring, flagged, and handed to the NIC thread, which puts it on
   // the emulated wire as soon as it lands.  A ring slot is reused only once
@@ -514,7 +550,8 @@ void Engine::stage_one(int cls, cudaStream_t s, const void* src, std::size_t n, 
   if (id > ring)
     for (int nn = 0; nn < N_; ++nn)
       if (nn != n_) wait_flag(s, nn * g_ + j_, consumed, id - ring);
-  CK(cudaMemcpyAsync(shm_->slot(rank_, cls, static_cast<int>(id % ring)), src, n, cudaMemcpyDeviceToHost, s));
+  unsigned char* dst = host_dst ? host_dst : shm_->slot(rank_, cls, static_cast<int>(id % ring));
+  CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s));
   write_flag(s, cls == 0 ? kAgStaged : kRsStaged, id);
   nic_->submit({cls, id, n * wire_mult, counter});
   shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, id);
@@ -540,15 +577,22 @@ void Engine::exchange(int cls, cudaStream_t send_s, const std::vector<SendSeg>& 
   struct P {
     const unsigned char* src;
     std::size_t n;
+    unsigned char* host_dst;
   };
   std::vector<P> out;
   for (const SendSeg& sg : mine)
     for (std::size_t off = 0; off < sg.bytes; off += ch)
-      out.push_back({static_cast<const unsigned char*>(sg.src) + off, std::min(ch, sg.bytes - off)});
+      out.push_back({static_cast<const unsigned char*>(sg.src) + off, std::min(ch, sg.bytes - off),
+                     sg.host_dst ? sg.host_dst + off : nullptr});
+  struct RP {
+    std::size_t n;
+    unsigned char* dst;             // null: not ours
+    const unsigned char* host_src;  // null: the sender's ring slot
+  };
   struct R {
     int src_rank;
     std::uint32_t first;
-    std::vector<std::pair<std::size_t, unsigned char*>> pieces;  // (bytes, dst or null)
+    std::vector<RP> pieces;
   };
   std::vector<R> in;
   std::size_t kmax = out.size();
@@ -556,22 +600,25 @@ void Engine::exchange(int cls, cudaStream_t send_s, const std::vector<SendSeg>& 
     R r{ib.src_rank, recv_base_[cls][ib.src_rank] + 1, {}};
     for (const InSeg& sg : ib.segs)
       for (std::size_t off = 0; off < sg.bytes; off += ch)
-        r.pieces.push_back({std::min(ch, sg.bytes - off), sg.dst ? sg.dst + off : nullptr});
+        r.pieces.push_back({std::min(ch, sg.bytes - off), sg.dst ? sg.dst + off : nullptr,
+                            sg.host_src ? sg.host_src + off : nullptr});
     recv_base_[cls][ib.src_rank] += static_cast<std::uint32_t>(r.pieces.size());
     kmax = std::max(kmax, r.pieces.size());
     in.push_back(std::move(r));
   }
   std::uint64_t rx = 0;
   for (std::size_t k = 0; k < kmax; ++k) {
-    if (k < out.size()) stage_one(cls, send_s, out[k].src, out[k].n, wire_mult, counter);
+    if (k < out.size()) stage_one(cls, send_s, out[k].src, out[k].n, wire_mult, counter, out[k].host_dst);
     for (R& r : in) {
       if (k >= r.pieces.size()) continue;
       const std::uint32_t id = r.first + static_cast<std::uint32_t>(k);
-      const auto [n, dst] = r.pieces[k];
+      const RP& pc = r.pieces[k];
+      const std::size_t n = pc.n;
+      unsigned char* dst = pc.dst;
       if (dst) {
         wait_flag(recv_s, r.src_rank, cls == 0 ? kAgTxReady : kRsTxReady, id);
-        CK(cudaMemcpyAsync(dst, shm_->slot(r.src_rank, cls, static_cast<int>(id % ring)), n,
-                           cudaMemcpyHostToDevice, recv_s));
+        const unsigned char* src = pc.host_src ? pc.host_src : shm_->slot(r.src_rank, cls, static_cast<int>(id % ring));
+        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, recv_s));
         rx += n;
       }
       mark_consumed(cls, recv_s, r.src_rank / g_, id);  // read it, or it was never ours to read
@@ -608,17 +655,44 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
     // already waited on this event's deps in run()), so the receive side below
     // overlaps with it.
     const std::size_t bt = wt ? l.my_real_t * C : 0, bf = wf ? l.my_real_f * C : 0;
+    // Write-once staging: portions the forward FCDP-Cache will store are staged
+    // straight into their host-cache position (slice j, shard n) and served to
+    // the wire from there.
+    const bool ct = !backward && wt && cache_stage_t_[e.layer], cf = !backward && wf && cache_stage_f_[e.layer];
+    const std::size_t t_off = (l.host_off + n_ * l.L.dev.shard_t) * C;
+    const std::size_t f_off = (l.host_off + l.L.dev.slice_t + n_ * l.L.dev.shard_f) * C;
+    if (ct || cf) {
+      // WAR: receivers must be done with last iteration's pieces from this region
+      const std::uint32_t last = std::max(ct ? cache_last_id_t_[e.layer] : 0u, cf ? cache_last_id_f_[e.layer] : 0u);
+      if (last)
+        for (int nn = 0; nn < N_; ++nn)
+          if (nn != n_) wait_flag(s_agsend_, nn * g_ + j_, static_cast<Flag>(kAgConsumed0 + n_), last);
+    }
     std::vector<Inbound> inbound;
     std::uint64_t rx = 0;
     for (int nn = 0; nn < N_; ++nn) {
       if (nn == n_) continue;
       const int r = j_ * N_ + nn;
       const std::size_t rt = wt ? l.L.real_chunks(false, r) * C : 0, rf = wf ? l.L.real_chunks(true, r) * C : 0;
-      inbound.push_back({nn * g_ + j_, {{rt, X + nn * l.L.dev.shard_t * C}, {rf, Xf + nn * l.L.dev.shard_f * C}}});
+      const unsigned char* hb = hc_base_[nn];
+      inbound.push_back({nn * g_ + j_,
+                         {{rt, X + nn * l.L.dev.shard_t * C,
+                           ct ? hb + (l.host_off + nn * l.L.dev.shard_t) * C : nullptr},
+                          {rf, Xf + nn * l.L.dev.shard_f * C,
+                           cf ? hb + (l.host_off + l.L.dev.slice_t + nn * l.L.dev.shard_f) * C : nullptr}}});
       rx += rt + rf;
     }
-    exchange(0, s_agsend_, {{param_t_ + l.off_t * C, bt}, {param_f_ + l.off_f * C, bf}}, N_ - 1,
-             backward ? kTxBwdAg : kTxFwdAg, s, inbound);
+    const std::uint32_t first_id = sent_pieces_[0] + 1;
+    exchange(0, s_agsend_,
+             {{param_t_ + l.off_t * C, bt, ct ? host_cache_ + t_off : nullptr},
+              {param_f_ + l.off_f * C, bf, cf ? host_cache_ + f_off : nullptr}},
+             N_ - 1, backward ? kTxBwdAg : kTxFwdAg, s, inbound);
+    if (ct || cf) {
+      const std::uint32_t pt = static_cast<std::uint32_t>(pieces_of(bt));
+      if (ct) cache_last_id_t_[e.layer] = first_id + pt - 1;
+      if (cf) cache_last_id_f_[e.layer] = sent_pieces_[0];
+      CK(cudaEventRecord(cache_staged_[e.layer], s_agsend_));
+    }
     shm_->add(rank_, backward ? kRxBwdAg : kRxFwdAg, rx);
   }
   finish_slice_fill(slot, q);
@@ -742,20 +816,39 @@ void Engine::ev_d2h(const Event& e) {
   unsigned char* H = host_cache_ + l.host_off * C;
   std::uint64_t bytes = 0;
   int slot_t = -1, slot_f = -1;
+  // Copy slice j of a portion from X to the host cache; when this GPU's own
+  // shard was staged there already (write-once staging), only the peers' shards.
+  auto store = [&](bool frozen, int slot) {
+    const std::int64_t shard = frozen ? l.L.dev.shard_f : l.L.dev.shard_t;
+    const std::size_t base = frozen ? l.L.dev.slice_t * C : 0;
+    const unsigned char* Xs = x_slot(j_, slot) + base;
+    const bool own_staged = frozen ? cache_stage_f_[e.layer] : cache_stage_t_[e.layer];
+    if (!own_staged || N_ == 1) {
+      const std::int64_t real = frozen ? l.slice_real_f : l.slice_real_t;
+      if (real) CK(cudaMemcpyAsync(H + base, Xs, real * C, cudaMemcpyDeviceToHost, s_cache_));
+      return;
+    }
+    for (int m = 0; m < N_; ++m) {
+      if (m == n_) continue;
+      const std::int64_t real = l.L.real_chunks(frozen, j_ * N_ + m);
+      if (real)
+        CK(cudaMemcpyAsync(H + base + m * shard * C, Xs + m * shard * C, real * C, cudaMemcpyDeviceToHost,
+                           s_cache_));
+    }
+  };
+  const bool staged_any = (wt && cache_stage_t_[e.layer]) || (wf && cache_stage_f_[e.layer]);
+  if (staged_any && N_ > 1) CK(cudaStreamWaitEvent(s_cache_, cache_staged_[e.layer], 0));
   if (wt) {
     slot_t = x_of_t_[e.layer];
     if (slot_t < 0) throw shardsim::ProtocolError("d2h of a trainable portion that was not gathered");
-    if (l.slice_real_t)
-      CK(cudaMemcpyAsync(H, x_slot(j_, slot_t), l.slice_real_t * C, cudaMemcpyDeviceToHost, s_cache_));
+    store(false, slot_t);
     bytes += l.slice_real_t * C;
     l.host_version_t = static_cast<std::int64_t>(l.shard_version_t);
   }
   if (wf) {
     slot_f = x_of_f_[e.layer];
     if (slot_f < 0) throw shardsim::ProtocolError("d2h of a frozen portion that was not gathered");
-    if (l.slice_real_f)
-      CK(cudaMemcpyAsync(H + l.L.dev.slice_t * C, x_slot(j_, slot_f) + l.L.dev.slice_t * C, l.slice_real_f * C,
-                         cudaMemcpyDeviceToHost, s_cache_));
+    store(true, slot_f);
     bytes += l.slice_real_f * C;
     l.host_version_f = 0;
   }
@@ -915,6 +1008,14 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
   }
   std::fill(x_of_t_.begin(), x_of_t_.end(), -1);
   std::fill(x_of_f_.begin(), x_of_f_.end(), -1);
+  std::fill(cache_stage_t_.begin(), cache_stage_t_.end(), 0);
+  std::fill(cache_stage_f_.begin(), cache_stage_f_.end(), 0);
+  if (shared_cache_)
+    for (const Event& e : prog.events)
+      if (e.kind == EventKind::D2H) {  // every D2H stores a forward-gathered layer
+        if (wants_t(e.param_set) && layers_[e.layer].has_t) cache_stage_t_[e.layer] = 1;
+        if (wants_f(e.param_set) && layers_[e.layer].has_f) cache_stage_f_[e.layer] = 1;
+      }
   std::fill(w_of_layer_.begin(), w_of_layer_.end(), -1);
 
   static const bool debug = std::getenv("FCDP_DEBUG") != nullptr;

@@ -114,16 +114,19 @@ class Engine {
   struct SendSeg {
     const void* src;
     std::size_t bytes;
+    unsigned char* host_dst = nullptr;  // stage into this host address (the host cache) instead of the ring
   };
   struct InSeg {
     std::size_t bytes;
     unsigned char* dst;  // null: part of the sender's message that is not for this rank
+    const unsigned char* host_src = nullptr;  // the sender staged this segment here (its host cache)
   };
   struct Inbound {
     int src_rank;
     std::vector<InSeg> segs;  // the sender's whole message, in its staging order
   };
-  void stage_one(int cls, cudaStream_t s, const void* src, std::size_t n, std::uint64_t wire_mult, Counter counter);
+  void stage_one(int cls, cudaStream_t s, const void* src, std::size_t n, std::uint64_t wire_mult, Counter counter,
+                 unsigned char* host_dst);
   void mark_consumed(int cls, cudaStream_t s, int src_node, std::uint32_t id);
   void exchange(int cls, cudaStream_t send_s, const std::vector<SendSeg>& mine, std::uint64_t wire_mult,
                 Counter counter, cudaStream_t recv_s, const std::vector<Inbound>& inbound);
@@ -155,6 +158,16 @@ class Engine {
   unsigned char* wire_[2] = {nullptr, nullptr};
   unsigned char* rx_[2] = {nullptr, nullptr};
   unsigned char* host_cache_ = nullptr;
+  // Shared host cache (N > 1, FCDP family): a forward AgInter stages this GPU's
+  // own shard straight into its host-cache position and the wire serves it from
+  // there, so FCDP-Cache's D2H only copies the peers' shards (write once).
+  bool shared_cache_ = false;
+  std::unique_ptr<ShmSegment> hc_own_;
+  std::unique_ptr<ShmSegment> hc_peer_[kMaxNodes];
+  unsigned char* hc_base_[kMaxNodes] = {};   // node -> host cache of (node, j_) in this process
+  std::vector<char> cache_stage_t_, cache_stage_f_;  // per layer, this iteration
+  std::vector<cudaEvent_t> cache_staged_;           // per layer: own shard landed in the host cache
+  std::vector<std::uint32_t> cache_last_id_t_, cache_last_id_f_;  // last piece id staged into each region
 
   cudaStream_t s_comp_ = nullptr, s_gather_ = nullptr, s_cache_ = nullptr, s_rs_ = nullptr;
   // staging (send) side of the NIC path, so a message's pieces are staged

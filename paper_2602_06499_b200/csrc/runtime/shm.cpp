@@ -90,6 +90,42 @@ SharedBlock::SharedBlock(const std::string& name, int rank, int world, int nodes
   hdr_->ranks[rank].attached.store(1, std::memory_order_release);
 }
 
+ShmSegment::ShmSegment(const std::string& name, std::size_t bytes, bool create, double timeout_s)
+    : name_(shm_path(name)), bytes_(round_up(bytes ? bytes : 4096, 4096)), owner_(create) {
+  int fd = -1;
+  if (create) {
+    shm_unlink(name_.c_str());
+    fd = shm_open(name_.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) throw std::runtime_error("shm_open(create " + name_ + ") failed: " + std::strerror(errno));
+    if (ftruncate(fd, static_cast<off_t>(bytes_)) != 0) {
+      close(fd);
+      throw std::runtime_error("ftruncate(" + name_ + ") failed: " + std::string(std::strerror(errno)));
+    }
+  } else {
+    const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
+    for (;;) {
+      fd = shm_open(name_.c_str(), O_RDWR, 0600);
+      if (fd >= 0) {
+        struct stat st {};
+        if (fstat(fd, &st) == 0 && static_cast<std::size_t>(st.st_size) >= bytes_) break;
+        close(fd);
+        fd = -1;
+      }
+      if (std::chrono::steady_clock::now() > deadline) throw TimeoutError("shm segment " + name_ + " did not appear");
+      std::this_thread::sleep_for(std::chrono::milliseconds(2));
+    }
+  }
+  void* p = mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) throw std::runtime_error("mmap(" + name_ + ") failed: " + std::string(std::strerror(errno)));
+  base_ = static_cast<unsigned char*>(p);
+}
+
+ShmSegment::~ShmSegment() {
+  if (base_) munmap(base_, bytes_);
+  if (owner_) shm_unlink(name_.c_str());
+}
+
 SharedBlock::~SharedBlock() {
   if (hdr_) munmap(hdr_, bytes_);
   if (rank_ == 0) shm_unlink(name_.c_str());

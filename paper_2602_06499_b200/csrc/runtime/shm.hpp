@@ -78,6 +78,25 @@ struct alignas(64) ShmHeader {
   NodeBlock node_blocks[kMaxRanks];
 };
 
+// A named POSIX shared-memory segment (one per rank) used for memory other
+// ranks must read directly, e.g. the FCDP-Cache host tier when staged shards
+// are served to the wire from it.
+class ShmSegment {
+ public:
+  ShmSegment(const std::string& name, std::size_t bytes, bool create, double timeout_s);
+  ~ShmSegment();
+  ShmSegment(const ShmSegment&) = delete;
+  ShmSegment& operator=(const ShmSegment&) = delete;
+  unsigned char* base() const { return base_; }
+  std::size_t bytes() const { return bytes_; }
+
+ private:
+  std::string name_;
+  unsigned char* base_ = nullptr;
+  std::size_t bytes_ = 0;
+  bool owner_ = false;
+};
+
 class SharedBlock {
  public:
   // Rank 0 creates (and later unlinks) the segment; others attach, waiting up
