@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--zero3-steps", type=int, default=3)
     p.add_argument("--no-zero3", action="store_true")
     p.add_argument("--zeropp", action="store_true", help="also measure ZeRO++ (GPU node replica) on the same executor")
+    p.add_argument("--mics", action="store_true", help="also measure MiCS (node-local shards + replica gradient sync)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--copy-engine", action="store_true")
@@ -298,10 +299,12 @@ def main():
         per_step = [round(evs[i].elapsed_time(evs[i + 1]), 3) for i in range(steps)]
         counters = tr.engine.counters()
         kst = tr.engine.kernel_stats(reset=True)
+        numa = tr.engine.numa()
         tr.engine.set_timing(False)
         loss_v = float(loss.item())
         # per-node inter-group bytes per step (sum over the node's ranks), from the NIC counters
-        node_tx = {k: sum_over_ranks(counters[k]) / N / steps for k in ("nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs")}
+        node_tx = {k: sum_over_ranks(counters[k]) / N / steps for k in ("nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs",
+                                                                       "nic_tx_grad_sync")}
         cache = {k: sum_over_ranks(counters[k]) / N / steps for k in ("cache_h2d", "cache_d2h")}
         vol = S.comm_volume(plan, tr.model, topo, warmup + steps)
         e2e = None
@@ -332,7 +335,7 @@ def main():
         del tr
         torch.cuda.empty_cache()
         return {"ms": ms, "per_step": per_step, "counters": counters, "kernels": kst, "clocks": clocks, "loss": loss_v,
-                "node_tx": node_tx, "cache": cache, "vol": vol, "e2e": e2e}
+                "node_tx": node_tx, "cache": cache, "vol": vol, "e2e": e2e, "numa": numa}
 
     if args.batch <= 0:
         args.batch = zero3_max_batch()
@@ -349,6 +352,9 @@ def main():
     zpp = None
     if args.zeropp and args.strategy != "zeropp":
         zpp = measure("zeropp", args.zero3_steps, 2, False, 0)
+    mics = None
+    if args.mics and args.strategy != "mics":
+        mics = measure("mics", args.zero3_steps, 2, False, 0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -413,12 +419,16 @@ def main():
                     "ms_per_step": zpp["ms"] / args.zero3_steps,
                     "ag_inter_fwd_bwd": [zpp["node_tx"]["nic_tx_fwd_ag"], zpp["node_tx"]["nic_tx_bwd_ag"]]}
                    if zpp else None),
+        "mics": ({"tokens_per_s": tokens_per_step / (mics["ms"] / args.zero3_steps / 1e3),
+                  "ms_per_step": mics["ms"] / args.zero3_steps,
+                  "ag_inter_fwd_bwd": [mics["node_tx"]["nic_tx_fwd_ag"], mics["node_tx"]["nic_tx_bwd_ag"]],
+                  "grad_sync_bytes_per_node": mics["node_tx"]["nic_tx_grad_sync"]} if mics else None),
         "cache_bytes_per_step_per_node": main_run["cache"],
         "fcdp_variant": ({"tau": args.tau_variant, "tokens_per_s": tokens_per_step / (tau_run["ms"] / args.zero3_steps / 1e3),
                                 "ms_per_step": tau_run["ms"] / args.zero3_steps, "cache": tau_run["cache"],
                                 "ag_inter_fwd_bwd": [tau_run["node_tx"]["nic_tx_fwd_ag"], tau_run["node_tx"]["nic_tx_bwd_ag"]]}
                                if tau_run else None),
-        "kernels": kernels, "loss": main_run["loss"], "ms_each_step_rank0": main_run["per_step"],
+        "host_numa": main_run["numa"], "kernels": kernels, "loss": main_run["loss"], "ms_each_step_rank0": main_run["per_step"],
     }
     print(json.dumps(line), flush=True)
     if world > 1:

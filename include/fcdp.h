@@ -275,6 +275,7 @@ typedef struct fcdp_counters {
   uint64_t ag_inter_events_fwd, ag_inter_events_bwd;
   uint64_t nic_busy_ns;                                /* paced wire time charged by this rank */
   uint64_t resident_hits;  /* frozen reloads elided: portion already resident in a tau-retained buffer */
+  uint64_t nic_tx_grad_sync, nic_rx_grad_sync;  /* MiCS: replica gradient all-reduce (not in comm_volume) */
 } fcdp_counters;
 
 /* Compute callback: `kind` FCDP_EV_COMPUTE_FWD/BWD.  `weights` is the natural
@@ -298,6 +299,12 @@ int fcdp_engine_barrier(fcdp_engine* e);
 int fcdp_engine_streams(fcdp_engine* e, void** compute_stream);
 int fcdp_engine_counters(fcdp_engine* e, int32_t rank, fcdp_counters* out);
 int fcdp_engine_reset_counters(fcdp_engine* e);
+/* NUMA placement of this rank's host side (multi-socket hosts): the GPU's
+ * node (-1 unknown), online memory nodes, whether the host + NIC threads were
+ * pinned to the GPU's node, and pinned host bytes given that node as preferred
+ * (the FCDP-Cache tier).  FCDP_NUMA=0 disables placement. */
+int fcdp_engine_numa(fcdp_engine* e, int32_t* gpu_node, int32_t* num_nodes, int32_t* cpus_bound,
+                     uint64_t* bytes_bound);
 /* Read back (device->host, synchronous) for tests: */
 int fcdp_engine_read_shard(fcdp_engine* e, int32_t layer, int32_t frozen, void* host, size_t bytes);
 int fcdp_engine_read_master(fcdp_engine* e, int32_t layer, float* host, size_t count);

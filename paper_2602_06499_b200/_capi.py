@@ -86,7 +86,8 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs", "nic_rx_fwd_ag", "nic_rx_bwd_ag", "nic_rx_rs",
         "nvlink_rx", "cache_h2d", "cache_d2h", "staging_h2d", "staging_d2h",
-        "ag_inter_events_fwd", "ag_inter_events_bwd", "nic_busy_ns", "resident_hits")]
+        "ag_inter_events_fwd", "ag_inter_events_bwd", "nic_busy_ns", "resident_hits",
+        "nic_tx_grad_sync", "nic_rx_grad_sync")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -158,6 +159,7 @@ SIGNATURES = {
     "fcdp_engine_streams": (C.c_int, [P, PP]),
     "fcdp_engine_counters": (C.c_int, [P, i32, C.POINTER(Counters)]),
     "fcdp_engine_reset_counters": (C.c_int, [P]),
+    "fcdp_engine_numa": (C.c_int, [P, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32), C.POINTER(u64)]),
     "fcdp_engine_read_shard": (C.c_int, [P, i32, i32, P, C.c_size_t]),
     "fcdp_engine_read_master": (C.c_int, [P, i32, P, C.c_size_t]),
     "fcdp_engine_read_grad": (C.c_int, [P, i32, P, C.c_size_t]),

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <thread>
+#include <sys/mman.h>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -107,10 +108,12 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   topo_.validate();
   plan_.validate(topo_);
   model_.validate();
-  if (plan_.kind != shardsim::StrategyKind::Zero3 && plan_.kind != shardsim::StrategyKind::Fcdp &&
-      plan_.kind != shardsim::StrategyKind::FcdpComm && plan_.kind != shardsim::StrategyKind::ZeroPP)
-    throw shardsim::ConfigError("engine: the B200 data plane executes zero3, zeropp, fcdp and fcdp-comm programs");
+  if (plan_.kind == shardsim::StrategyKind::Zero2)
+    throw shardsim::ConfigError("engine: the B200 data plane executes zero3, mics, zeropp, fcdp and fcdp-comm programs");
   zeropp_ = plan_.kind == shardsim::StrategyKind::ZeroPP;
+  mics_ = plan_.kind == shardsim::StrategyKind::MiCS;
+  if (mics_ && plan_.effective_subgroup(topo_) != topo_.gpus_per_node)
+    throw shardsim::ConfigError("engine: mics is executed with subgroup_size = gpus_per_node");
   if (shm_name_.empty()) throw shardsim::ConfigError("engine: shm_name is required");
   N_ = topo_.num_nodes;
   g_ = topo_.gpus_per_node;
@@ -120,6 +123,8 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   rank_ = cfg.rank;
   n_ = rank_ / g_;
   j_ = rank_ % g_;
+  Ns_ = mics_ ? 1 : N_;
+  ns_ = mics_ ? 0 : n_;
   eb_ = model_.param_bytes_per_element;
   V_ = kChunkBytes / eb_;
   if (cfg_.x_slots < 2) cfg_.x_slots = 3;
@@ -130,6 +135,13 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   chunk_bytes_ = (chunk_bytes_ + kChunkBytes - 1) / kChunkBytes * kChunkBytes;
 
   CK(cudaSetDevice(cfg_.device));
+  // NUMA: run this rank's host thread - and the NIC thread it starts - on the
+  // GPU's socket, and place its pinned host tiers there (multi-socket hosts).
+  numa_.num_nodes = numa_online_nodes();
+  numa_.gpu_node = numa_node_of_gpu(cfg_.device);
+  const char* numa_env = std::getenv("FCDP_NUMA");
+  if (numa_.num_nodes > 1 && numa_.gpu_node >= 0 && !(numa_env && std::strcmp(numa_env, "0") == 0))
+    numa_.cpus_bound = numa_pin_thread(numa_.gpu_node);
   build_layouts(chunk_masks);
 
   // staging ring: inter_slots pieces of chunk_bytes_ per class per rank
@@ -215,7 +227,8 @@ Engine::~Engine() {
     cudaHostUnregister(hc_own_->base());
     hc_own_.reset();
   } else if (host_cache_) {
-    cudaFreeHost(host_cache_);
+    cudaHostUnregister(host_cache_);
+    munmap(host_cache_, host_cache_map_bytes_);
   }
   if (shm_) cudaHostUnregister(shm_->base());
   shm_.reset();
@@ -226,7 +239,7 @@ Engine::~Engine() {
 void Engine::build_layouts(const std::uint8_t* const* masks) {
   const int L = model_.num_layers();
   layers_.resize(static_cast<std::size_t>(L));
-  const int r = j_ * N_ + n_;  // global shard index of this GPU
+  const int r = j_ * Ns_ + ns_;  // shard index of this GPU in its sharding scope
   for (int l = 0; l < L; ++l) {
     LayerRt& lr = layers_[l];
     const std::int64_t E = model_.layers[l].param_count;
@@ -246,7 +259,7 @@ void Engine::build_layouts(const std::uint8_t* const* masks) {
       std::fill_n(derived.begin(), trainable * eb_ / kChunkBytes, 1);
       mask = derived.data();
     }
-    lr.L = build_layout(lr.chunks, mask, eb_, N_, g_);
+    lr.L = build_layout(lr.chunks, mask, eb_, Ns_, g_);
     if (lr.L.dev.pt * V_ != trainable)
       throw shardsim::ConfigError("layer " + std::to_string(l) + ": chunk mask selects " +
                                   std::to_string(lr.L.dev.pt * V_) + " trainable params, trainable_fraction gives " +
@@ -313,16 +326,25 @@ void Engine::allocate() {
     hc_own_ = std::make_unique<ShmSegment>(shm_name_ + "_hc" + std::to_string(rank_), host_chunks_ * C, true,
                                            cfg_.timeout_s);
     host_cache_ = hc_own_->base();
-    CK(cudaHostRegister(host_cache_, hc_own_->bytes(), cudaHostRegisterPortable));
   } else {
-    const cudaError_t e = cudaHostAlloc(&host_cache_, std::max<std::size_t>(host_chunks_ * C, 4096),
-                                        cudaHostAllocPortable);
+    host_cache_map_bytes_ = std::max<std::size_t>(host_chunks_ * C, 4096);
+    void* p = mmap(nullptr, host_cache_map_bytes_, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) {
+      host_cache_map_bytes_ = 0;
+      throw OomError("mmap(host cache, " + std::to_string(host_chunks_ * C) + " B) failed");
+    }
+    host_cache_ = static_cast<unsigned char*>(p);
+  }
+  const std::size_t hc_bytes = hc_own_ ? hc_own_->bytes() : host_cache_map_bytes_;
+  if (numa_.cpus_bound && numa_prefer(host_cache_, hc_bytes, numa_.gpu_node)) numa_.bytes_bound += hc_bytes;
+  std::memset(host_cache_, 0, host_chunks_ * C);  // first touch: pages land on the preferred node
+  {
+    const cudaError_t e = cudaHostRegister(host_cache_, hc_bytes, cudaHostRegisterPortable);
     if (e != cudaSuccess) {
       cudaGetLastError();
-      throw OomError("cudaHostAlloc(host cache, " + std::to_string(host_chunks_ * C) + " B) failed");
+      throw OomError("cudaHostRegister(host cache, " + std::to_string(hc_bytes) + " B) failed");
     }
   }
-  std::memset(host_cache_, 0, host_chunks_ * C);
   hc_base_[n_] = host_cache_;
   const std::size_t L = layers_.size();
   cache_stage_t_.assign(L, 0);
@@ -371,8 +393,8 @@ void Engine::init_params(std::uint64_t seed, const fcdp_init_range* const* range
   unsigned char* nat = dalloc<unsigned char>(max_chunks_ * C, "init natural");
   std::int64_t max_t = 0, max_f = 0;
   for (const LayerRt& l : layers_) {
-    max_t = std::max(max_t, l.L.dev.shard_t * G_);
-    max_f = std::max(max_f, l.L.dev.shard_f * G_);
+    max_t = std::max(max_t, l.L.dev.shard_t * Ns_ * g_);
+    max_f = std::max(max_f, l.L.dev.shard_f * Ns_ * g_);
   }
   unsigned char* tv = dalloc<unsigned char>(max_t * C, "init t");
   unsigned char* fv = dalloc<unsigned char>(max_f * C, "init f");
@@ -380,15 +402,15 @@ void Engine::init_params(std::uint64_t seed, const fcdp_init_range* const* range
   int max_r = 1;
   for (std::size_t l = 0; l < layers_.size(); ++l) max_r = std::max(max_r, num_ranges ? num_ranges[l] : 0);
   d_ranges = dalloc<InitRange>(sizeof(InitRange) * max_r, "init ranges");
-  const int r = j_ * N_ + n_;
+  const int r = j_ * Ns_ + ns_;
   try {
     for (std::size_t li = 0; li < layers_.size(); ++li) {
       LayerRt& l = layers_[li];
       const int nr = num_ranges ? num_ranges[li] : 0;
       if (nr > 0) CK(cudaMemcpy(d_ranges, ranges[li], sizeof(InitRange) * nr, cudaMemcpyHostToDevice));
       CK(launch_init_natural(l.elems, eb_, seed, static_cast<int>(li), d_ranges, nr, nat, s));
-      CK(cudaMemsetAsync(tv, 0, l.L.dev.shard_t * G_ * C, s));
-      CK(cudaMemsetAsync(fv, 0, l.L.dev.shard_f * G_ * C, s));
+      CK(cudaMemsetAsync(tv, 0, l.L.dev.shard_t * Ns_ * g_ * C, s));
+      CK(cudaMemsetAsync(fv, 0, l.L.dev.shard_f * Ns_ * g_ * C, s));
       CK(launch_partition(l.L, nat, tv, fv, s));
       if (l.has_t)
         CK(cudaMemcpyAsync(param_t_ + l.off_t * C, tv + r * l.L.dev.shard_t * C, l.L.dev.shard_t * C,
@@ -643,13 +665,13 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
   //  and host-staged NIC traffic, and a D2D queued behind them stalls the gather)
   if (wt && l.my_real_t)
     timed(4, s, 2 * l.my_real_t * C, [&] {
-      return launch_copy(param_t_ + l.off_t * C, X + n_ * l.L.dev.shard_t * C, l.my_real_t * C, s);
+      return launch_copy(param_t_ + l.off_t * C, X + ns_ * l.L.dev.shard_t * C, l.my_real_t * C, s);
     });
   if (wf && l.my_real_f)
     timed(4, s, 2 * l.my_real_f * C, [&] {
-      return launch_copy(param_f_ + l.off_f * C, Xf + n_ * l.L.dev.shard_f * C, l.my_real_f * C, s);
+      return launch_copy(param_f_ + l.off_f * C, Xf + ns_ * l.L.dev.shard_f * C, l.my_real_f * C, s);
     });
-  if (N_ > 1) {
+  if (Ns_ > 1) {
     // Inter-node all-gather among {(n', j)} through the host-staged NIC path,
     // pipelined in pieces of chunk_bytes_.  Staging runs on s_agsend_ (which
     // already waited on this event's deps in run()), so the receive side below
@@ -702,7 +724,7 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
   if (wc.layer != e.layer) wc = WContent{e.layer, -1, -1};
   if (wt) wc.ver_t = static_cast<std::int64_t>(l.shard_version_t), x_of_t_[e.layer] = slot;
   if (wf) wc.ver_f = 0, x_of_f_[e.layer] = slot;
-  shm_->add(rank_, backward ? kAgEventsBwd : kAgEventsFwd, 1);
+  if (!mics_) shm_->add(rank_, backward ? kAgEventsBwd : kAgEventsFwd, 1);
   if (zeropp_ && !backward) {
     // keep slice j on the GPU for the backward intra-node gather (ZeRO++ hpZ)
     if (l.last_replica_pull_q)
@@ -763,7 +785,11 @@ void Engine::ev_h2d(const Event& e) {
   p.ver_f = wf ? 0 : -1;
 }
 
-void Engine::ev_ag_intra(const Event& e) {
+void Engine::ev_ag_intra(const Event& e, bool backward) {
+  if (mics_) {  // MiCS within a node: gather the layer from the node's g shards over NVLink
+    ev_ag_inter(e, backward);
+    return;
+  }
   if (zeropp_) {
     // backward reconstruction from the GPU replicas of the node (no PCIe, no NIC)
     LayerRt& l = layers_[e.layer];
@@ -902,7 +928,7 @@ void Engine::ev_reduce_scatter(const Event& e) {
   write_flag(s, kGradReady, u);
   for (int jj = 0; jj < g_; ++jj)
     if (jj != j_) wait_flag(s, n_ * g_ + jj, kGradReady, u);
-  if (N_ > 1) CK(cudaStreamWaitEvent(s, rs_staged_[gs], 0));  // wire_[gs] staged out (use u-2)
+  if (N_ > 1) CK(cudaStreamWaitEvent(s, rs_staged_[gs], 0));  // wire/rx [gs] staged out (use u-2)
   GradPtrs gp{};
   for (int jj = 0; jj < g_; ++jj) gp.p[jj] = grad_slot(jj, gs);
   const float scale = 1.0f / static_cast<float>(G_);
@@ -911,7 +937,13 @@ void Engine::ev_reduce_scatter(const Event& e) {
   const std::uint64_t rs_bytes = static_cast<std::uint64_t>(g_) * l.slice_real_t * C +
                                  static_cast<std::uint64_t>(l.my_real_t) * V_ * sizeof(float) +
                                  static_cast<std::uint64_t>(l.slice_real_t - l.my_real_t) * C;
-  if (N_ == 1) {
+  if (mics_ && N_ > 1) {
+    // every contribution (this node's included) in the wire dtype, so all
+    // replicas sum identical values in the same order
+    timed(1, s, static_cast<std::uint64_t>(g_ + 1) * l.slice_real_t * C, [&] {
+      return launch_rs_slice(l.L, gp, j_, -1, scale, false, nullptr, rx_[gs] + n_ * l.L.dev.shard_t * C, s);
+    }, static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
+  } else if (N_ == 1) {
     timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, 0, scale, true, final_out, wire_[gs], s); },
           static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
   } else {
@@ -923,6 +955,10 @@ void Engine::ev_reduce_scatter(const Event& e) {
   shm_->add(rank_, kNvlinkRx, static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
   grad_slot_of_layer_[li] = -1;
   if (N_ == 1) return;
+  if (mics_) {
+    mics_grad_sync(l, gs, scale, final_out);
+    return;
+  }
 
   // Inter-node reduce-scatter among {(n', j)}: partial sums of the other
   // nodes' shards cross the NIC in the parameter dtype (costmodel.cpp:86-88).
@@ -953,6 +989,31 @@ void Engine::ev_reduce_scatter(const Event& e) {
   const std::uint64_t fin_elems = static_cast<std::uint64_t>(l.L.dev.shard_t) * V_;
   timed(2, s, fin_elems * (2 * sizeof(float) + static_cast<std::uint64_t>(N_ - 1) * eb_), [&] {
     return launch_rs_finalize(l.L.dev.shard_t * V_, N_, n_, eb_, own32_[gs], rx_[gs], l.L.dev.shard_t * V_, scale,
+                              final_out, s);
+  });
+}
+
+void Engine::mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out) {
+  // MiCS replicas: all-reduce slice j over the N nodes' GPUs j through the
+  // NIC path (each sends its whole node-reduced slice to every other node),
+  // then one fixed-order sum of the N contributions.  The reference's cost
+  // model books no bytes for this sync (costmodel.cpp:39-43, scope = 1 node),
+  // so it has its own counter.
+  cudaStream_t s = s_rs_;
+  const std::size_t C = kChunkBytes;
+  const std::size_t stride = static_cast<std::size_t>(l.L.dev.shard_t) * C;
+  CK(cudaEventRecord(rs_kernel_done_[gs], s));
+  CK(cudaStreamWaitEvent(s_rssend_, rs_kernel_done_[gs], 0));
+  const std::size_t b = static_cast<std::size_t>(l.slice_real_t) * C;
+  std::vector<Inbound> inbound;
+  for (int nn = 0; nn < N_; ++nn)
+    if (nn != n_) inbound.push_back({nn * g_ + j_, {{b, rx_[gs] + nn * stride}}});
+  exchange(1, s_rssend_, {{rx_[gs] + n_ * stride, b}}, N_ - 1, kTxGradSync, s, inbound);
+  CK(cudaEventRecord(rs_staged_[gs], s_rssend_));
+  shm_->add(rank_, kRxGradSync, static_cast<std::uint64_t>(N_ - 1) * b);
+  const std::uint64_t fin_elems = static_cast<std::uint64_t>(l.L.dev.shard_t) * V_;
+  timed(2, s, fin_elems * (sizeof(float) + static_cast<std::uint64_t>(N_) * eb_), [&] {
+    return launch_rs_finalize(l.L.dev.shard_t * V_, N_, -1, eb_, nullptr, rx_[gs], l.L.dev.shard_t * V_, scale,
                               final_out, s);
   });
 }
@@ -1033,7 +1094,7 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     switch (e.kind) {
       case EventKind::AgInter: ev_ag_inter(e, bwd); break;
       case EventKind::H2D: ev_h2d(e); break;
-      case EventKind::AgIntra: ev_ag_intra(e); break;
+      case EventKind::AgIntra: ev_ag_intra(e, bwd); break;
       case EventKind::D2H: ev_d2h(e); break;
       case EventKind::ComputeFwd: ev_compute(e, false); break;
       case EventKind::ComputeBwd: ev_compute(e, true); break;
@@ -1119,6 +1180,8 @@ void Engine::counters(int rank, fcdp_counters* o) const {
   o->ag_inter_events_bwd = shm_->counter(rank, kAgEventsBwd);
   o->nic_busy_ns = shm_->counter(rank, kNicBusyNs);
   o->resident_hits = shm_->counter(rank, kResidentHits);
+  o->nic_tx_grad_sync = shm_->counter(rank, kTxGradSync);
+  o->nic_rx_grad_sync = shm_->counter(rank, kRxGradSync);
 }
 
 void Engine::reset_counters() { shm_->reset_counters(rank_); }

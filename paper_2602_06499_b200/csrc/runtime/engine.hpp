@@ -30,6 +30,7 @@
 #include "fcdp.h"
 #include "kernels/kernels.hpp"
 #include "runtime/nic.hpp"
+#include "runtime/numa.hpp"
 #include "runtime/shm.hpp"
 #include "shardsim/schedule.hpp"
 
@@ -58,6 +59,7 @@ struct WContent {
 
 class Engine {
  public:
+  const NumaPlacement& numa() const { return numa_; }
   Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
          const shardsim::ClusterTopology& topo, const shardsim::StrategyPlan& plan,
          const std::uint8_t* const* chunk_masks);
@@ -94,7 +96,8 @@ class Engine {
   // ---- events
   void ev_ag_inter(const shardsim::Event& e, bool backward);
   void ev_h2d(const shardsim::Event& e);
-  void ev_ag_intra(const shardsim::Event& e);
+  void ev_ag_intra(const shardsim::Event& e, bool backward);
+  void mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out);
   void ev_d2h(const shardsim::Event& e);
   void ev_compute(const shardsim::Event& e, bool backward);
   void ev_reduce_scatter(const shardsim::Event& e);
@@ -137,6 +140,12 @@ class Engine {
   shardsim::ClusterTopology topo_;
   shardsim::StrategyPlan plan_;
   int N_, g_, G_, n_, j_, rank_, eb_, V_;
+  // Sharding scope: the nodes one parameter shard set spans.  Every strategy
+  // but MiCS shards over the whole job (Ns_ = N_, ns_ = n_); MiCS with
+  // subgroup = gpus_per_node shards inside each node (Ns_ = 1) and keeps a
+  // replica per node, whose gradients are summed over the NIC after the RS.
+  int Ns_ = 1, ns_ = 0;
+  bool mics_ = false;
   std::vector<LayerRt> layers_;
   std::int64_t max_chunks_ = 0, max_slice_ = 0, max_shard_t_ = 0, max_slice_t_ = 0;
   std::int64_t arena_t_ = 0, arena_f_ = 0, host_chunks_ = 0;
@@ -158,6 +167,8 @@ class Engine {
   unsigned char* wire_[2] = {nullptr, nullptr};
   unsigned char* rx_[2] = {nullptr, nullptr};
   unsigned char* host_cache_ = nullptr;
+  std::size_t host_cache_map_bytes_ = 0;  // anonymous mapping (non-shared cache)
+  NumaPlacement numa_;
   // Shared host cache (N > 1, FCDP family): a forward AgInter stages this GPU's
   // own shard straight into its host-cache position and the wire serves it from
   // there, so FCDP-Cache's D2H only copies the peers' shards (write once).

@@ -58,6 +58,17 @@ int fcdp_engine_counters(fcdp_engine* e, int32_t rank, fcdp_counters* out) {
   return guarded([&] { E(e).counters(rank, out); });
 }
 
+int fcdp_engine_numa(fcdp_engine* e, int32_t* gpu_node, int32_t* num_nodes, int32_t* cpus_bound,
+                     uint64_t* bytes_bound) {
+  return guarded([&] {
+    const fcdp::NumaPlacement& p = E(e).numa();
+    if (gpu_node) *gpu_node = p.gpu_node;
+    if (num_nodes) *num_nodes = p.num_nodes;
+    if (cpus_bound) *cpus_bound = p.cpus_bound ? 1 : 0;
+    if (bytes_bound) *bytes_bound = p.bytes_bound;
+  });
+}
+
 int fcdp_engine_reset_counters(fcdp_engine* e) { return guarded([&] { E(e).reset_counters(); }); }
 
 int fcdp_engine_read_shard(fcdp_engine* e, int32_t layer, int32_t frozen, void* host, size_t bytes) {

@@ -40,7 +40,8 @@ enum Flag : int {
 
 enum Counter : int {
   kTxFwdAg = 0, kTxBwdAg, kTxRs, kRxFwdAg, kRxBwdAg, kRxRs, kNvlinkRx, kCacheH2D, kCacheD2H,
-  kStagingH2D, kStagingD2H, kAgEventsFwd, kAgEventsBwd, kNicBusyNs, kResidentHits, kNumCounters
+  kStagingH2D, kStagingD2H, kAgEventsFwd, kAgEventsBwd, kNicBusyNs, kResidentHits, kTxGradSync, kRxGradSync,
+  kNumCounters
 };
 
 struct alignas(64) FlagLine {

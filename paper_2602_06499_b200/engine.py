@@ -110,6 +110,12 @@ class Engine:
         check(lib().fcdp_engine_counters(self._h, self.rank if rank is None else rank, C.byref(c)))
         return c.as_dict()
 
+    def numa(self) -> Dict[str, int]:
+        """NUMA placement of this rank's host side (fcdp_engine_numa)."""
+        gn, nn, cb, bb = C.c_int32(), C.c_int32(), C.c_int32(), C.c_uint64()
+        check(lib().fcdp_engine_numa(self._h, C.byref(gn), C.byref(nn), C.byref(cb), C.byref(bb)))
+        return {"gpu_node": gn.value, "num_nodes": nn.value, "cpus_bound": bool(cb.value), "bytes_bound": bb.value}
+
     def node_counters(self, node: int) -> Dict[str, int]:
         g = self.topo.gpus_per_node
         tot: Dict[str, int] = {}

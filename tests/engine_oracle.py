@@ -11,6 +11,11 @@ import numpy as np
 from oracle import oracle as O
 
 
+def scope_nodes(cfg):
+    """Nodes one shard set spans: MiCS (subgroup = g) shards inside a node."""
+    return 1 if cfg["strategy"] == "mics" else cfg["N"]
+
+
 def grad_coeff(rank):
     return (1 + rank) / 8.0
 
@@ -34,12 +39,15 @@ class Sim:
         self.cfg = cfg
         self.N, self.g = cfg["N"], cfg["g"]
         self.G = self.N * self.g
+        self.Ns = scope_nodes(cfg)
+        self.Gs = self.Ns * self.g  # shards per portion
+        self.mics = cfg["strategy"] == "mics"
         self.eb = cfg["eb"]
         self.V = 16 // self.eb
         self.masks = [np.array(m, np.uint8) for m in cfg["masks"]]
         self.E = cfg["params"]
         self.L = len(self.E)
-        self.geo = [O.geom(len(m), m, self.N, self.g) for m in self.masks]
+        self.geo = [O.geom(len(m), m, self.Ns, self.g) for m in self.masks]
         layers = [S.LayerSpec(i, E, float(int(m.sum()) * self.V) / E) for i, (E, m) in enumerate(zip(self.E, self.masks))]
         self.model = S.ModelSpec(layers, self.eb)
         self.topo = S.make_topology(self.N, self.g, inter_preset=cfg.get("inter", "ib100-rdma-measured"))
@@ -67,22 +75,22 @@ class Sim:
 
     def shard_index(self, rank):
         n, j = divmod(rank, self.g)
-        return j * self.N + n
+        return j * self.Ns + (n if self.Ns > 1 else 0)
 
     def _padded_portions(self, l, nat):
         geo = self.geo[l]
         t, f = O.partition(nat.view(np.uint8), self.masks[l])
-        tp = np.zeros(geo.shard_t * self.G * 16, np.uint8)
+        tp = np.zeros(geo.shard_t * self.Gs * 16, np.uint8)
         tp[:t.size] = t
-        fp = np.zeros(geo.shard_f * self.G * 16, np.uint8)
+        fp = np.zeros(geo.shard_f * self.Gs * 16, np.uint8)
         fp[:f.size] = f
         return tp, fp
 
     def portions(self, l):
         geo = self.geo[l]
-        t = np.zeros(geo.shard_t * self.G * 16, np.uint8)
-        f = np.zeros(geo.shard_f * self.G * 16, np.uint8)
-        for r in range(self.G):
+        t = np.zeros(geo.shard_t * self.Gs * 16, np.uint8)
+        f = np.zeros(geo.shard_f * self.Gs * 16, np.uint8)
+        for r in range(self.Gs):  # one shard set (the first replica for MiCS)
             s = self.shard_index(r)
             t[s * geo.shard_t * 16:(s + 1) * geo.shard_t * 16] = self.shard_t[r][l]
             f[s * geo.shard_f * 16:(s + 1) * geo.shard_f * 16] = self.shard_f[r][l]
@@ -99,7 +107,7 @@ class Sim:
                                  gpu_capacity_bytes=self.cfg.get("capacity", 0))
         exp = [{"captures": [], "host": {}, "grad": {}, "master": {}, "shard_t": {}, "shard_f": {},
                 "counters": {k: 0 for k in ("nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs", "cache_h2d",
-                                            "cache_d2h", "nvlink_rx")}} for _ in range(self.G)]
+                                            "cache_d2h", "nvlink_rx", "nic_tx_grad_sync")}} for _ in range(self.G)]
         last_fwd = max(e.id for e in prog.events if e.kind == S.EventKind.ComputeFwd)
         retained = [bool(f & 1) for f in prog.layer_flags(self.L)]
 
@@ -183,7 +191,7 @@ class Sim:
         return max(0, min(per, tot - s * per))
 
     def _real_slice(self, l, frozen, j):
-        return sum(self._real(l, frozen, j * self.N + n) for n in range(self.N))
+        return sum(self._real(l, frozen, j * self.Ns + n) for n in range(self.Ns))
 
     def _nvl(self, l, r, pset):
         S = self.S
@@ -211,8 +219,8 @@ class Sim:
         for r in range(self.G):
             n, j = divmod(r, g)
             local = [g_all[n * g + jj] for jj in range(g)]
-            own[r], wire[r] = O.rs_slice(geo, self.masks[l], self.eb, local, j, n if N > 1 else 0,
-                                         float(scale), N == 1)
+            own_idx = (-1 if self.mics else n) if N > 1 else 0  # MiCS: whole slice on the wire
+            own[r], wire[r] = O.rs_slice(geo, self.masks[l], self.eb, local, j, own_idx, float(scale), N == 1)
             exp[r]["counters"]["nvlink_rx"] += (g - 1) * self._real_slice(l, False, j) * 16
         for r in range(self.G):
             n, j = divmod(r, g)
@@ -221,6 +229,12 @@ class Sim:
                 continue
             sh = geo.shard_t * self.V
             rx = np.zeros(N * sh, _elem(self.eb))
+            if self.mics:  # replica all-reduce: every node's whole slice, fixed node order
+                for nn in range(N):
+                    rx[nn * sh:(nn + 1) * sh] = wire[nn * g + j]
+                exp[r]["counters"]["nic_tx_grad_sync"] += (N - 1) * self._real_slice(l, False, j) * 16
+                self.grad[r][l] = O.rs_finalize(np.zeros(sh, np.float32), rx, N, -1, self.eb, sh, float(scale))
+                continue
             for nn in range(N):
                 if nn == n:
                     continue

@@ -28,6 +28,7 @@ def main():
     from paper_2602_06499_b200.engine import Engine, BWD
     from paper_2602_06499_b200.tensors import device_view
     from oracle import oracle as O
+    from tests.engine_oracle import scope_nodes
 
     rank, world = cfg["rank"], cfg["world"]
     N, g = cfg["N"], cfg["g"]
@@ -82,7 +83,7 @@ def main():
              "retained": prog.layer_flags(model.num_layers())}
         captures.clear()
         for l in range(model.num_layers()):
-            geo = O.geom(len(masks[l]), masks[l], N, g)
+            geo = O.geom(len(masks[l]), masks[l], scope_nodes(cfg), g)
             j = rank % g
             st, sf = geo.slice_t * 16, geo.slice_f * 16
             d["host"][l] = (eng.read_host_cache(l, False, st), eng.read_host_cache(l, True, sf))

@@ -133,9 +133,10 @@ CASES_1 = [(1, 1, "zeropp", 2, "dense"), (1, 1, "zero3", 2, "dense"), (1, 1, "fc
            (1, 1, "fcdp-comm", 4, "random"), (1, 1, "fcdp", 4, "lora")]
 CASES_2 = [(2, 1, "zero3", 2, "dense"), (2, 1, "fcdp", 2, "dense"), (2, 1, "fcdp-comm", 2, "lora"),
            (1, 2, "fcdp", 2, "dense"), (1, 2, "fcdp-comm", 2, "random"), (2, 1, "fcdp-comm", 4, "random"),
-           (1, 2, "zeropp", 2, "lora")]
+           (1, 2, "zeropp", 2, "lora"), (2, 1, "mics", 2, "dense"), (1, 2, "mics", 4, "random")]
 CASES_4 = [(2, 2, "zeropp", 2, "dense"), (2, 2, "zero3", 2, "dense"), (2, 2, "fcdp", 2, "dense"), (2, 2, "fcdp-comm", 2, "lora"),
-           (4, 1, "fcdp-comm", 2, "random"), (1, 4, "fcdp", 4, "lora")]
+           (4, 1, "fcdp-comm", 2, "random"), (1, 4, "fcdp", 4, "lora"), (2, 2, "mics", 2, "lora"),
+           (4, 1, "mics", 4, "dense")]
 
 
 @pytest.mark.parametrize("N,g,strategy,eb,kind", CASES_1 + CASES_2 + CASES_4)
