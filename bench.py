@@ -402,6 +402,15 @@ def main():
                    "oracle_zero3": z3["vol"].fwd_ag_inter + z3["vol"].bwd_ag_inter})
         tot_z = ag["zero3_fwd"] + ag["zero3_bwd"]
         ag["eliminated_frac"] = (1 - (ag["fcdp_fwd"] + ag["fcdp_bwd"]) / tot_z) if tot_z else None
+    # Step-level link roofline (N > 1): the NIC bytes a node must move per step at
+    # the preset's bandwidth, against the measured step (costmodel.cpp:100-129 shape).
+    link_bound = None
+    if N > 1:
+        nic_b = sum(main_run["node_tx"][k] for k in ("nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs", "nic_tx_grad_sync"))
+        bw = topo.inter_node.bandwidth_bytes_per_s
+        t_nic = nic_b / bw * 1e3
+        link_bound = {"nic_bytes_per_node_per_step": nic_b, "nic_gbs": bw / 1e9, "nic_time_ms": t_nic,
+                      "step_ms": ms_step, "frac": t_nic / ms_step if ms_step else None}
     kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
                    "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None} for k, v in kst.items()}
     line = {
@@ -410,7 +419,7 @@ def main():
         "vs_baseline": None, "dtype": "bf16" if mc.dtype_bytes == 2 else "fp32",
         "data": "synthetic (counter-based token ids, random-init weights of the named architecture)",
         "config": workload_config(args, mc, N, g, world, seq),
-        "e2e": main_run["e2e"], "gpu_launches": gpu_launches, "roofline": roofline,
+        "e2e": main_run["e2e"], "gpu_launches": gpu_launches, "roofline": roofline, "link_bound": link_bound,
         "cpu_baseline": cpu, "clocks": main_run["clocks"],
         "ag_inter_bytes_per_step_per_node": ag,
         "zero3": ({"tokens_per_s": tokens_per_step / (z3["ms"] / z3_steps(args) / 1e3), "ms_per_step": z3["ms"] / z3_steps(args)}

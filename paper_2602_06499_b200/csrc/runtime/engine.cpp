@@ -160,6 +160,8 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   CK(cudaStreamCreateWithPriority(&s_rs_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_agsend_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_rssend_, cudaStreamNonBlocking, hi));
+  CK(cudaStreamCreateWithPriority(&s_rsrecv_, cudaStreamNonBlocking, hi));
+  for (auto& e : fin_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_staged_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   x_reader_.assign(static_cast<std::size_t>(cfg_.x_slots), nullptr);
@@ -201,7 +203,9 @@ Engine::~Engine() {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : rs_staged_)
     if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_})
+  for (cudaEvent_t e : fin_done_)
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_})
     if (s) cudaStreamDestroy(s);
   for (void* p : {static_cast<void*>(param_t_), static_cast<void*>(param_f_), static_cast<void*>(master_),
                   static_cast<void*>(adam_m_), static_cast<void*>(adam_v_), static_cast<void*>(grad32_),
@@ -928,7 +932,10 @@ void Engine::ev_reduce_scatter(const Event& e) {
   write_flag(s, kGradReady, u);
   for (int jj = 0; jj < g_; ++jj)
     if (jj != j_) wait_flag(s, n_ * g_ + jj, kGradReady, u);
-  if (N_ > 1) CK(cudaStreamWaitEvent(s, rs_staged_[gs], 0));  // wire/rx [gs] staged out (use u-2)
+  if (N_ > 1) {
+    CK(cudaStreamWaitEvent(s, rs_staged_[gs], 0));  // wire/rx [gs] staged out (use u-2)
+    CK(cudaStreamWaitEvent(s, fin_done_[gs], 0));   // own32/rx [gs] consumed by epilogue u-2
+  }
   GradPtrs gp{};
   for (int jj = 0; jj < g_; ++jj) gp.p[jj] = grad_slot(jj, gs);
   const float scale = 1.0f / static_cast<float>(G_);
@@ -983,14 +990,18 @@ void Engine::ev_reduce_scatter(const Event& e) {
     }
     inbound.push_back(std::move(ib));
   }
-  exchange(1, s_rssend_, mine, 1, kTxRs, s, inbound);
+  cudaStream_t r = s_rsrecv_;
+  CK(cudaStreamWaitEvent(r, rs_kernel_done_[gs], 0));
+  exchange(1, s_rssend_, mine, 1, kTxRs, r, inbound);
   CK(cudaEventRecord(rs_staged_[gs], s_rssend_));  // wire_[gs] may be rewritten after this
   shm_->add(rank_, kRxRs, rx);
   const std::uint64_t fin_elems = static_cast<std::uint64_t>(l.L.dev.shard_t) * V_;
-  timed(2, s, fin_elems * (2 * sizeof(float) + static_cast<std::uint64_t>(N_ - 1) * eb_), [&] {
+  timed(2, r, fin_elems * (2 * sizeof(float) + static_cast<std::uint64_t>(N_ - 1) * eb_), [&] {
     return launch_rs_finalize(l.L.dev.shard_t * V_, N_, n_, eb_, own32_[gs], rx_[gs], l.L.dev.shard_t * V_, scale,
-                              final_out, s);
+                              final_out, r);
   });
+  CK(cudaEventRecord(fin_done_[gs], r));
+  done_s_ = r;
 }
 
 void Engine::mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out) {
@@ -999,11 +1010,12 @@ void Engine::mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out) {
   // then one fixed-order sum of the N contributions.  The reference's cost
   // model books no bytes for this sync (costmodel.cpp:39-43, scope = 1 node),
   // so it has its own counter.
-  cudaStream_t s = s_rs_;
   const std::size_t C = kChunkBytes;
   const std::size_t stride = static_cast<std::size_t>(l.L.dev.shard_t) * C;
-  CK(cudaEventRecord(rs_kernel_done_[gs], s));
+  CK(cudaEventRecord(rs_kernel_done_[gs], s_rs_));
   CK(cudaStreamWaitEvent(s_rssend_, rs_kernel_done_[gs], 0));
+  cudaStream_t s = s_rsrecv_;
+  CK(cudaStreamWaitEvent(s, rs_kernel_done_[gs], 0));
   const std::size_t b = static_cast<std::size_t>(l.slice_real_t) * C;
   std::vector<Inbound> inbound;
   for (int nn = 0; nn < N_; ++nn)
@@ -1016,6 +1028,8 @@ void Engine::mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out) {
     return launch_rs_finalize(l.L.dev.shard_t * V_, N_, -1, eb_, nullptr, rx_[gs], l.L.dev.shard_t * V_, scale,
                               final_out, s);
   });
+  CK(cudaEventRecord(fin_done_[gs], s));
+  done_s_ = s;
 }
 
 void Engine::ev_optimizer(const Event&) {
@@ -1049,7 +1063,8 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     stream_of[e.id] = stream_for(e.kind);
     if (e.kind == EventKind::ComputeFwd) last_fwd = e.id;
   }
-  for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_}) CK(cudaStreamWaitEvent(s, iter_done_, 0));
+  for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_})
+    CK(cudaStreamWaitEvent(s, iter_done_, 0));
   if (trace_) {
     auto grow = [&](std::vector<cudaEvent_t>& v) {
       while (v.size() < n_ev) {
@@ -1062,7 +1077,8 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     grow(trace_end_);
     if (!trace_start_) CK(cudaEventCreate(&trace_start_));
     CK(cudaEventRecord(trace_start_, s_comp_));
-    for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_}) CK(cudaStreamWaitEvent(s, trace_start_, 0));
+    for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_})
+      CK(cudaStreamWaitEvent(s, trace_start_, 0));
     traced_events_ = static_cast<std::uint32_t>(n_ev);
   } else {
     traced_events_ = 0;
@@ -1087,8 +1103,10 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
                    static_cast<unsigned long long>(prog.iteration_index), e.id, shardsim::to_string(e.kind), e.layer);
     for (shardsim::EventId d : e.deps)
       if (stream_of[d] != s) CK(cudaStreamWaitEvent(s, ev_done_[d], 0));
-    if (e.kind == EventKind::AgInter && N_ > 1)
-      for (shardsim::EventId d : e.deps) CK(cudaStreamWaitEvent(s_agsend_, ev_done_[d], 0));
+    // (the staging side s_agsend_ needs none of the program's deps: its source,
+    //  the own shard, is final since the previous iteration joined, and buffer
+    //  reuse on it is guarded by the receivers' consumed markers - so the NIC
+    //  keeps streaming the next layers while this one is expanded)
     const bool bwd = e.id > last_fwd;
     if (trace_) CK(cudaEventRecord(trace_begin_[e.id], s));
     switch (e.kind) {
@@ -1104,12 +1122,15 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
       case EventKind::Broadcast:
         throw shardsim::ConfigError("engine: broadcast events (zero2) are not part of this data plane");
     }
-    CK(cudaEventRecord(ev_done_[e.id], s));
-    if (trace_) CK(cudaEventRecord(trace_end_[e.id], s));
+    const cudaStream_t ds = done_s_ ? done_s_ : s;
+    done_s_ = nullptr;
+    stream_of[e.id] = ds;
+    CK(cudaEventRecord(ev_done_[e.id], ds));
+    if (trace_) CK(cudaEventRecord(trace_end_[e.id], ds));
   }
   // join: the next iteration starts after everything of this one
-  const cudaStream_t side[5] = {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_};
-  for (int i = 0; i < 5; ++i) {
+  const cudaStream_t side[6] = {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_};
+  for (int i = 0; i < 6; ++i) {
     CK(cudaEventRecord(join_[i], side[i]));
     CK(cudaStreamWaitEvent(s_comp_, join_[i], 0));
   }
@@ -1137,7 +1158,7 @@ void Engine::sync() {
   // Poll instead of blocking so a cross-rank wait that can never be satisfied
   // (a peer died, a protocol bug) ends in a diagnosable TimeoutError.
   const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(cfg_.timeout_s);
-  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_}) {
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_}) {
     if (!s) continue;
     for (int spin = 0;; ++spin) {
       const cudaError_t q = cudaStreamQuery(s);

@@ -184,13 +184,18 @@ class Engine {
   // staging (send) side of the NIC path, so a message's pieces are staged
   // while the same layer's incoming pieces are already being received
   cudaStream_t s_agsend_ = nullptr, s_rssend_ = nullptr;
+  // inter-node RS receive + epilogue: off s_rs_, so the next layer's intra RS
+  // kernel and staging start while this layer's pieces are still on the wire
+  cudaStream_t s_rsrecv_ = nullptr;
+  cudaStream_t done_s_ = nullptr;      // set by a handler whose event completes on another stream
+  cudaEvent_t fin_done_[2] = {nullptr, nullptr};  // RS epilogue of grad slot gs finished
   cudaEvent_t rs_kernel_done_[2] = {nullptr, nullptr};
   cudaEvent_t rs_staged_[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_done_;
   std::vector<cudaEvent_t> x_reader_;  // last local reader of each X slot
   cudaEvent_t rs_done_[2] = {nullptr, nullptr};
   cudaEvent_t iter_done_ = nullptr;
-  cudaEvent_t join_[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t join_[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, u_ = 0;

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--out", default="gpurun_out/trace.json")
     ap.add_argument("--copy-engine", action="store_true")
+    ap.add_argument("--tau", type=float, default=0.0, help="FCDP-Cache retention threshold (capacity = GPU memory)")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -43,8 +44,9 @@ def main():
         dist.broadcast_object_list(name, src=0)
     mc = PRESETS[a.preset]
     tr = FcdpTrainer(mc, S.make_topology(N, g, inter_preset=a.inter),
-                     S.StrategyPlan(S.StrategyKind.from_string(a.strategy)), rank=rank, world_size=world,
-                     device=local, shm_name=name[0], batch_per_gpu=a.batch, use_copy_engine=a.copy_engine)
+                     S.StrategyPlan(S.StrategyKind.from_string(a.strategy), tau=a.tau), rank=rank, world_size=world,
+                     device=local, shm_name=name[0], batch_per_gpu=a.batch, use_copy_engine=a.copy_engine,
+                     gpu_capacity_bytes=torch.cuda.get_device_properties(local).total_memory if a.tau > 0 else 0)
     dev = torch.device("cuda", local)
     for i in range(a.steps):
         if i == a.steps - 1:
