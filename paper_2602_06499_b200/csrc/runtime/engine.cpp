@@ -222,6 +222,8 @@ Engine::~Engine() {
   }
   for (auto& ev : cache_staged_)
     if (ev) cudaEventDestroy(ev);
+  for (auto& ev : ag_staged_)
+    if (ev) cudaEventDestroy(ev);
   for (int nn = 0; nn < kMaxNodes; ++nn)
     if (hc_peer_[nn]) {
       cudaHostUnregister(hc_peer_[nn]->base());
@@ -357,6 +359,10 @@ void Engine::allocate() {
   cache_last_id_f_.assign(L, 0);
   cache_staged_.assign(L, nullptr);
   for (auto& ev : cache_staged_) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  ag_staged_.assign(L, nullptr);
+  for (auto& ev : ag_staged_) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  ag_staged_valid_.assign(L, 0);
+  stepped_.assign(L, 0);
 }
 
 void Engine::exchange_handles() {
@@ -713,6 +719,8 @@ void Engine::ev_ag_inter(const Event& e, bool backward) {
              {{param_t_ + l.off_t * C, bt, ct ? host_cache_ + t_off : nullptr},
               {param_f_ + l.off_f * C, bf, cf ? host_cache_ + f_off : nullptr}},
              N_ - 1, backward ? kTxBwdAg : kTxFwdAg, s, inbound);
+    CK(cudaEventRecord(ag_staged_[e.layer], s_agsend_));
+    ag_staged_valid_[e.layer] = 1;
     if (ct || cf) {
       const std::uint32_t pt = static_cast<std::uint32_t>(pieces_of(bt));
       if (ct) cache_last_id_t_[e.layer] = first_id + pt - 1;
@@ -961,9 +969,13 @@ void Engine::ev_reduce_scatter(const Event& e) {
   CK(cudaEventRecord(rs_done_[gs], s));
   shm_->add(rank_, kNvlinkRx, static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
   grad_slot_of_layer_[li] = -1;
-  if (N_ == 1) return;
+  if (N_ == 1) {
+    if (early_opt_) adam_layer(li, s);
+    return;
+  }
   if (mics_) {
     mics_grad_sync(l, gs, scale, final_out);
+    if (early_opt_) adam_layer(li, s_rsrecv_);
     return;
   }
 
@@ -1002,6 +1014,7 @@ void Engine::ev_reduce_scatter(const Event& e) {
   });
   CK(cudaEventRecord(fin_done_[gs], r));
   done_s_ = r;
+  if (early_opt_) adam_layer(li, r);
 }
 
 void Engine::mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out) {
@@ -1032,7 +1045,32 @@ void Engine::mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out) {
   done_s_ = s;
 }
 
+void Engine::adam_layer(int li, cudaStream_t s) {
+  LayerRt& l = layers_[li];
+  const int step = opt_steps_ + 1;  // the step the program's OptimizerStep will complete
+  AdamParams p{adam_.lr, adam_.beta1, adam_.beta2, adam_.eps, adam_.weight_decay,
+               static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta1), step)),
+               static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta2), step))};
+  // the own shard must have left for the NIC before it is overwritten
+  if (ag_staged_valid_[li]) CK(cudaStreamWaitEvent(s, ag_staged_[li], 0));
+  const std::int64_t n = l.L.dev.shard_t * V_;
+  const std::size_t o = static_cast<std::size_t>(l.off_t) * V_;
+  timed(3, s, static_cast<std::uint64_t>(n) * (7 * sizeof(float) + eb_), [&] {
+    return launch_adam(n, p, master_ + o, adam_m_ + o, adam_v_ + o, grad32_ + o, param_t_ + l.off_t * kChunkBytes,
+                       eb_, s);
+  });
+  stepped_[li] = 1;
+}
+
 void Engine::ev_optimizer(const Event&) {
+  if (early_opt_) {
+    for (std::size_t li = 0; li < layers_.size(); ++li)
+      if (layers_[li].has_t && !stepped_[li]) adam_layer(static_cast<int>(li), s_comp_);
+    ++opt_steps_;
+    for (LayerRt& l : layers_)
+      if (l.has_t) ++l.shard_version_t;
+    return;
+  }
   ++opt_steps_;
   AdamParams p{adam_.lr, adam_.beta1, adam_.beta2, adam_.eps, adam_.weight_decay,
                static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta1), opt_steps_)),
@@ -1086,6 +1124,14 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
   std::fill(x_of_t_.begin(), x_of_t_.end(), -1);
   std::fill(x_of_f_.begin(), x_of_f_.end(), -1);
   std::fill(cache_stage_t_.begin(), cache_stage_t_.end(), 0);
+  std::fill(stepped_.begin(), stepped_.end(), 0);
+  std::fill(ag_staged_valid_.begin(), ag_staged_valid_.end(), 0);
+  {
+    static const char* eo = std::getenv("FCDP_EARLY_OPT");
+    bool has_opt = false;
+    for (const Event& e : prog.events) has_opt |= e.kind == EventKind::OptimizerStep;
+    early_opt_ = has_opt && !(eo && std::strcmp(eo, "0") == 0);
+  }
   std::fill(cache_stage_f_.begin(), cache_stage_f_.end(), 0);
   if (shared_cache_)
     for (const Event& e : prog.events)

@@ -205,6 +205,14 @@ class Engine {
   std::uint32_t consumed_[2][8] = {};             // last consumed marker written, per sender node
   std::uint64_t w_instances_ = 0;
   int opt_steps_ = 0;
+  // Early optimizer: AdamW of a layer's shard runs as soon as its gradient is
+  // final (after its RS), overlapping later layers' backward instead of one
+  // launch after the last RS.  Elementwise, so results are identical.
+  bool early_opt_ = false;
+  std::vector<char> stepped_;                 // per layer: updated early this iteration
+  std::vector<cudaEvent_t> ag_staged_;        // per layer: own shard staged for the NIC (s_agsend_)
+  std::vector<char> ag_staged_valid_;
+  void adam_layer(int li, cudaStream_t s);
 
   // per-iteration bookkeeping
   struct PendingSlice {
