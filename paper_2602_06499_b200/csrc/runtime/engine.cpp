@@ -1130,7 +1130,10 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     static const char* eo = std::getenv("FCDP_EARLY_OPT");
     bool has_opt = false;
     for (const Event& e : prog.events) has_opt |= e.kind == EventKind::OptimizerStep;
-    early_opt_ = has_opt && !(eo && std::strcmp(eo, "0") == 0);
+    // Worth it only where an inter-node RS tail follows the last backward
+    // compute (N > 1); at N = 1 the update would just contend with the
+    // backward GEMMs for HBM (measured: no gain).  FCDP_EARLY_OPT=0/1 forces.
+    early_opt_ = has_opt && (eo ? std::strcmp(eo, "0") != 0 : N_ > 1);
   }
   std::fill(cache_stage_f_.begin(), cache_stage_f_.end(), 0);
   if (shared_cache_)

@@ -207,7 +207,8 @@ class Engine {
   int opt_steps_ = 0;
   // Early optimizer: AdamW of a layer's shard runs as soon as its gradient is
   // final (after its RS), overlapping later layers' backward instead of one
-  // launch after the last RS.  Elementwise, so results are identical.
+  // launch after the last RS.  Elementwise, so results are identical.  On
+  // by default when N > 1.
   bool early_opt_ = false;
   std::vector<char> stepped_;                 // per layer: updated early this iteration
   std::vector<cudaEvent_t> ag_staged_;        // per layer: own shard staged for the NIC (s_agsend_)
