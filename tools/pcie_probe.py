@@ -26,13 +26,41 @@ def bw(fn, nbytes, reps=8):
     return nbytes * reps / dt / 1e9
 
 
+def registered(n, kind, tag):
+    """Host buffer from a POSIX shm segment or an anonymous mapping, registered
+    with cudaHostRegister (what the engine's host-cache tier uses)."""
+    import mmap
+    if kind == "shm":
+        path = f"/dev/shm/pcie_probe_{os.getpid()}_{tag}"
+        fd = os.open(path, os.O_CREAT | os.O_RDWR, 0o600)
+        os.ftruncate(fd, n)
+        m = mmap.mmap(fd, n)
+        os.close(fd)
+        os.unlink(path)
+    else:
+        m = mmap.mmap(-1, n)
+    t = torch.frombuffer(m, dtype=torch.uint8)
+    t.fill_(0)
+    err = torch.cuda.cudart().cudaHostRegister(t.data_ptr(), n, 1)
+    assert int(err) == 0, err
+    registered.keep.append(m)
+    return t
+
+
+registered.keep = []
+
+
 def main():
+    src = sys.argv[1] if len(sys.argv) > 1 else "torch"
     dist.init_process_group("gloo")
     r, w = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(r)
     n = 512 << 20
-    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    if src == "torch":
+        h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    else:
+        h, h2 = registered(n, src, "a"), registered(n, src, "b")
     d = torch.empty(n, dtype=torch.uint8, device="cuda")
     d2 = torch.empty(n, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
@@ -49,7 +77,7 @@ def main():
     out = [None] * w
     dist.all_gather_object(out, res)
     if r == 0:
-        print(json.dumps({"world": w, "per_gpu": out}))
+        print(json.dumps({"world": w, "src": src, "per_gpu": out}))
     dist.barrier()
 
 
