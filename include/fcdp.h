@@ -294,6 +294,16 @@ int fcdp_engine_set_compute(fcdp_engine* e, fcdp_compute_fn fn, void* user);
 /* Execute one program (built for this engine's plan/model/topology) and apply
  * step_state.  Asynchronous: returns once every event is enqueued. */
 int fcdp_engine_run(fcdp_engine* e, const fcdp_program* program, fcdp_states* states);
+/* The same, driven event by event by an external executor that walks
+ * EventProgram.events in id order (SURVEY §8(b) caller): begin, then exec for
+ * ids 0..n-1, then end (which applies step_state).  Each exec enqueues that
+ * event's data movement - AgInter (pack + NIC + NVLink gather/unpack), AgIntra,
+ * D2H (FCDP-Cache store), H2D (cache reload), ReduceScatter (fused cast/scale),
+ * OptimizerStep (AdamW) - honouring its deps with stream waits.  Out-of-order
+ * ids -> FCDP_ERR_PROTOCOL.  `program` must stay alive until end. */
+int fcdp_engine_begin(fcdp_engine* e, const fcdp_program* program);
+int fcdp_engine_exec(fcdp_engine* e, uint32_t event_id);
+int fcdp_engine_end(fcdp_engine* e, fcdp_states* states);
 int fcdp_engine_sync(fcdp_engine* e);
 int fcdp_engine_barrier(fcdp_engine* e);
 int fcdp_engine_streams(fcdp_engine* e, void** compute_stream);

@@ -154,6 +154,9 @@ SIGNATURES = {
     "fcdp_engine_set_adam": (C.c_int, [P, C.POINTER(AdamConfig)]),
     "fcdp_engine_set_compute": (C.c_int, [P, COMPUTE_FN, P]),
     "fcdp_engine_run": (C.c_int, [P, P, P]),
+    "fcdp_engine_begin": (C.c_int, [P, P]),
+    "fcdp_engine_exec": (C.c_int, [P, u32]),
+    "fcdp_engine_end": (C.c_int, [P, P]),
     "fcdp_engine_sync": (C.c_int, [P]),
     "fcdp_engine_barrier": (C.c_int, [P]),
     "fcdp_engine_streams": (C.c_int, [P, PP]),

@@ -1085,6 +1085,18 @@ void Engine::ev_optimizer(const Event&) {
 // --------------------------------------------------------------------- run
 
 void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::ParamState>& states) {
+  begin(prog);
+  try {
+    for (const Event& e : prog.events) exec(e.id);
+  } catch (...) {
+    prog_ = nullptr;  // the enqueued prefix still drains; the program is abandoned
+    throw;
+  }
+  end(states);
+}
+
+void Engine::begin(const shardsim::EventProgram& prog) {
+  if (prog_) throw shardsim::ProtocolError("engine: a program is already in progress (missing end)");
   if (prog.strategy != plan_.kind) throw shardsim::ConfigError("engine: program strategy differs from the engine plan");
   if (prog.layer_retained.size() != layers_.size()) throw shardsim::ConfigError("engine: program is for another model");
   CK(cudaSetDevice(cfg_.device));
@@ -1095,12 +1107,15 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ev_done_.push_back(e);
   }
-  std::vector<cudaStream_t> stream_of(n_ev);
-  std::uint32_t last_fwd = 0;
+  for (std::size_t i = 0; i < n_ev; ++i)
+    if (prog.events[i].id != i) throw shardsim::ConfigError("engine: event ids must be 0..n-1 in order");
+  stream_of_.assign(n_ev, nullptr);
+  last_fwd_ = 0;
   for (const Event& e : prog.events) {
-    stream_of[e.id] = stream_for(e.kind);
-    if (e.kind == EventKind::ComputeFwd) last_fwd = e.id;
+    stream_of_[e.id] = stream_for(e.kind);
+    if (e.kind == EventKind::ComputeFwd) last_fwd_ = e.id;
   }
+  next_event_ = 0;
   for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_})
     CK(cudaStreamWaitEvent(s, iter_done_, 0));
   if (trace_) {
@@ -1143,9 +1158,19 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
         if (wants_f(e.param_set) && layers_[e.layer].has_f) cache_stage_f_[e.layer] = 1;
       }
   std::fill(w_of_layer_.begin(), w_of_layer_.end(), -1);
+}
 
+void Engine::exec(std::uint32_t event_id) {
+  if (!prog_) throw shardsim::ProtocolError("engine: exec outside begin/end");
+  const shardsim::EventProgram& prog = *prog_;
+  if (event_id != next_event_ || event_id >= prog.events.size())
+    throw shardsim::ProtocolError("engine: events must be executed once each, in id order (expected " +
+                                  std::to_string(next_event_) + ", got " + std::to_string(event_id) + ")");
+  std::vector<cudaStream_t>& stream_of = stream_of_;
+  const std::uint32_t last_fwd = last_fwd_;
   static const bool debug = std::getenv("FCDP_DEBUG") != nullptr;
-  for (const Event& e : prog.events) {
+  {
+    const Event& e = prog.events[event_id];
     cudaStream_t s = stream_of[e.id];
     if (debug)
       std::fprintf(stderr, "[fcdp r%d] it=%llu enqueue ev %u %s layer %d\n", rank_,
@@ -1177,6 +1202,15 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
     CK(cudaEventRecord(ev_done_[e.id], ds));
     if (trace_) CK(cudaEventRecord(trace_end_[e.id], ds));
   }
+  ++next_event_;
+}
+
+void Engine::end(std::vector<shardsim::ParamState>& states) {
+  if (!prog_) throw shardsim::ProtocolError("engine: end without begin");
+  const shardsim::EventProgram& prog = *prog_;
+  if (next_event_ != prog.events.size())
+    throw shardsim::ProtocolError("engine: end after " + std::to_string(next_event_) + " of " +
+                                  std::to_string(prog.events.size()) + " events");
   // join: the next iteration starts after everything of this one
   const cudaStream_t side[6] = {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_};
   for (int i = 0; i < 6; ++i) {

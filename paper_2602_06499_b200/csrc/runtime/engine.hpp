@@ -72,6 +72,11 @@ class Engine {
     compute_user_ = user;
   }
   void run(const shardsim::EventProgram& prog, std::vector<shardsim::ParamState>& states);
+  // The same, one event at a time: an external executor walking the program
+  // in id order (begin, exec(0..n-1), end).  `prog` must outlive end().
+  void begin(const shardsim::EventProgram& prog);
+  void exec(std::uint32_t event_id);
+  void end(std::vector<shardsim::ParamState>& states);
   void sync();
   void barrier();
   cudaStream_t compute_stream() const { return s_comp_; }
@@ -230,6 +235,8 @@ class Engine {
   std::vector<int> grad_slot_of_layer_;
   std::vector<std::uint32_t> u_of_layer_;
   const shardsim::EventProgram* prog_ = nullptr;
+  std::vector<cudaStream_t> stream_of_;  // per event: stream its completion is recorded on
+  std::uint32_t last_fwd_ = 0, next_event_ = 0;
 
   fcdp_adam_config adam_{1e-4f, 0.9f, 0.95f, 1e-8f, 0.0f, 0};
   fcdp_compute_fn compute_fn_ = nullptr;

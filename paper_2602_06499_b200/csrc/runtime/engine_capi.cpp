@@ -47,6 +47,16 @@ int fcdp_engine_run(fcdp_engine* e, const fcdp_program* program, fcdp_states* st
   return guarded([&] { E(e).run(fcdp::program_from_c(program), fcdp::states_from_c(states)); });
 }
 
+int fcdp_engine_begin(fcdp_engine* e, const fcdp_program* program) {
+  return guarded([&] { E(e).begin(fcdp::program_from_c(program)); });
+}
+
+int fcdp_engine_exec(fcdp_engine* e, uint32_t event_id) { return guarded([&] { E(e).exec(event_id); }); }
+
+int fcdp_engine_end(fcdp_engine* e, fcdp_states* states) {
+  return guarded([&] { E(e).end(fcdp::states_from_c(states)); });
+}
+
 int fcdp_engine_sync(fcdp_engine* e) { return guarded([&] { E(e).sync(); }); }
 int fcdp_engine_barrier(fcdp_engine* e) { return guarded([&] { E(e).barrier(); }); }
 

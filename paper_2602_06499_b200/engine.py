@@ -94,6 +94,16 @@ class Engine:
         check(lib().fcdp_engine_run(self._h, program.ptr, s.ptr))
         return s.to_list()
 
+    def run_stepwise(self, program: EventProgram, states: Sequence[ParamState]) -> List[ParamState]:
+        """run(), driven the way an external executor would: begin, one exec
+        per event in id order, end (fcdp_engine_begin/exec/end)."""
+        s = _States.from_list(states)
+        check(lib().fcdp_engine_begin(self._h, program.ptr))
+        for e in program.events:
+            check(lib().fcdp_engine_exec(self._h, e.id))
+        check(lib().fcdp_engine_end(self._h, s.ptr))
+        return s.to_list()
+
     def sync(self) -> None:
         check(lib().fcdp_engine_sync(self._h))
 

@@ -73,7 +73,7 @@ def main():
                                  gpu_capacity_bytes=cfg.get("capacity", 0))
         eng.reset_counters()
         eng.barrier()
-        states = eng.run(prog, states)
+        states = eng.run_stepwise(prog, states) if cfg.get("stepwise") else eng.run(prog, states)
         eng.sync()
         eng.barrier()
         torch.cuda.synchronize()

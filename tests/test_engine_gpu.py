@@ -48,12 +48,13 @@ def _masks(chunks_list, kind, seed=0):
 
 
 def run_job(tmp_path, N, g, strategy, eb=2, kind="dense", iters=3, chunks=(1000, 1537, 777), pacing=False,
-            use_ce=False, tau=0.0, capacity=0):
+            use_ce=False, tau=0.0, capacity=0, stepwise=False):
     world = N * g
     V = 16 // eb
     cfg = {"N": N, "g": g, "world": world, "strategy": strategy, "eb": eb, "iters": iters, "seed": 0x5EED,
            "params": [c * V for c in chunks], "masks": _masks(chunks, kind), "shm": f"fcdp_test_{uuid.uuid4().hex[:12]}",
-           "out": str(tmp_path), "pacing": pacing, "use_ce": use_ce, "tau": tau, "capacity": capacity}
+           "out": str(tmp_path), "pacing": pacing, "use_ce": use_ce, "tau": tau, "capacity": capacity,
+           "stepwise": stepwise}
     procs = []
     for r in range(world):
         c = dict(cfg, rank=r)
@@ -180,3 +181,14 @@ def test_engine_tau_partial_capacity(tmp_path, built):
     check_job(cfg, dumps)
     flags = dumps[0][-1]["retained"]
     assert any(f & 1 for f in flags) and not all(f & 1 for f in flags), flags
+
+
+@pytest.mark.parametrize("N,g,strategy,kind", [(1, 1, "fcdp-comm", "lora"), (2, 1, "fcdp", "random")])
+def test_engine_stepwise_executor(tmp_path, built, N, g, strategy, kind):
+    """fcdp_engine_begin / exec (one event at a time, id order) / end gives the
+    same bit-exact results as fcdp_engine_run (the caller is an
+    executor walking EventProgram.events)."""
+    if N * g > _ngpu():
+        pytest.skip(f"needs {N * g} GPUs")
+    cfg, dumps = run_job(tmp_path, N, g, strategy, 2, kind, stepwise=True)
+    check_job(cfg, dumps)
