@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--topologies", default="", help="comma list NxG (default: all with N*G == gpus)")
     ap.add_argument("--out", default="gpurun_out/sweep.jsonl")
     ap.add_argument("--per-run-timeout", type=int, default=240)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--tau-variant", default="-1", help="also time this tau (bench --tau-variant); -1 = no")
     a = ap.parse_args()
     out = Path(a.out)
     out.parent.mkdir(parents=True, exist_ok=True)
@@ -45,7 +47,8 @@ def main():
                        "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
                        "--gpus", str(a.gpus), "--topology", f"{N}x{g}", "--inter", preset, "--strategy", strat,
                        "--preset", a.preset_model, "--batch", str(a.batch), "--steps", str(a.steps),
-                       "--warmup", "1", "--no-zero3", "--no-e2e", "--no-cpu-baseline", "--tau-variant", "0",
+                       "--warmup", str(a.warmup), "--no-zero3", "--no-e2e", "--no-cpu-baseline",
+                       "--tau-variant", a.tau_variant,
                        "--engine-timeout", "120", "--watchdog", str(a.per_run_timeout - 20)]
                 if a.gpus == 1:
                     cmd = [sys.executable, str(ROOT / "bench.py")] + cmd[cmd.index("--gpus"):]
