@@ -56,40 +56,63 @@ __device__ __forceinline__ const uint4* pick(const SlicePtrs& s, int j) {
 // Intra-node all-gather fused with the PEFT expansion: natural chunk c takes
 // its value from rank k of its portion, which lives in slice k / slice_size
 // (that GPU's memory, local or NVLink peer).
-template <bool kWriteT, bool kWriteF>
+// Slice lookup with the local GPU count as a compile-time constant: for g = 1
+// it vanishes, for g > 1 it is g - 1 predicated compares (no division).
+template <int kG>
+__device__ __forceinline__ int slice_of_g(int k, int per) {
+  int j = 0;
+#pragma unroll
+  for (int i = 1; i < kG; ++i) j += k >= i * per ? 1 : 0;
+  return j;
+}
+
+template <int kG>
+__device__ __forceinline__ const uint4* pick_g(const SlicePtrs& s, int j) {
+  const void* p = s.p[0];
+#pragma unroll
+  for (int i = 1; i < kG; ++i)
+    if (j == i) p = s.p[i];
+  return static_cast<const uint4*>(p);
+}
+
+// 32-bit chunk indices (the launcher rejects layers of >= 2^31 chunks, 32 GiB):
+// this loop is issue-bound as much as memory-bound, and 64-bit index math
+// doubled its instruction count.
+template <bool kWriteT, bool kWriteF, int kG>
 __global__ void __launch_bounds__(kThreads) expand_kernel(LayoutDev L, SlicePtrs ts, SlicePtrs fs,
                                                           uint4* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const std::int64_t warp = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int warp = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = static_cast<int>((gridDim.x * blockDim.x) >> 5);
   const unsigned below = (1u << lane) - 1u;
-  for (std::int64_t w0 = warp; w0 < L.words; w0 += nwarps * kUnroll) {
+  const int words = static_cast<int>(L.words), chunks = static_cast<int>(L.chunks);
+  const int per_t = static_cast<int>(L.slice_t), per_f = static_cast<int>(L.slice_f);
+  for (int w0 = warp; w0 < words; w0 += nwarps * kUnroll) {
     // phase 1: the mask words and prefixes of all kUnroll groups (independent loads)
     unsigned bits[kUnroll];
-    std::uint32_t pre[kUnroll];
+    int pre[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const std::int64_t w = w0 + u * nwarps;
-      bits[u] = w < L.words ? __ldg(L.bits + w) : 0u;
-      pre[u] = w < L.words ? __ldg(L.tpre + w) : 0u;
+      const int w = w0 + u * nwarps;
+      bits[u] = w < words ? __ldg(L.bits + w) : 0u;
+      pre[u] = w < words ? static_cast<int>(__ldg(L.tpre + w)) : 0;
     }
     // phase 2: ranks -> source addresses; phase 3: all data loads in flight
     uint4 v[kUnroll];
-    std::int64_t dst[kUnroll];
+    int dst[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const std::int64_t c = (w0 + u * nwarps) * 32 + lane;
-      const bool valid = c < L.chunks;
+      const int c = (w0 + u * nwarps) * 32 + lane;
+      const bool valid = c < chunks;
       const bool tr = valid && ((bits[u] >> lane) & 1u);
-      // ballot over the lanes' trainable predicates == the mask word for full groups
-      const unsigned ballot = __ballot_sync(kFull, tr);
-      const std::int64_t kt = static_cast<std::int64_t>(pre[u]) + __popc(ballot & below);
+      // the mask word's own bits are the ballot of the lanes' predicates
+      const int kt = pre[u] + __popc(bits[u] & below);
       dst[u] = -1;
       if (valid && (tr ? kWriteT : kWriteF)) {
-        const std::int64_t k = tr ? kt : c - kt;
-        const std::int64_t per = tr ? L.slice_t : L.slice_f;
-        const int j = slice_of(k, per, L.local);
-        v[u] = pick(tr ? ts : fs, j)[k - j * per];
+        const int k = tr ? kt : c - kt;
+        const int per = tr ? per_t : per_f;
+        const int j = slice_of_g<kG>(k, per);
+        v[u] = pick_g<kG>(tr ? ts : fs, j)[k - j * per];
         dst[u] = c;
       }
     }
@@ -588,13 +611,28 @@ cudaError_t launch_expand(const Layout& L, const SlicePtrs& ts, const SlicePtrs&
     }
     return launch_bulk(segs, s);
   }
+  if (L.dev.words * 32 >= (std::int64_t{1} << 31) - (std::int64_t{1} << 24))
+    return cudaErrorInvalidValue;  // 32-bit chunk indices (+ grid-stride headroom)
   const int grid = grid_for(L.dev.words * 32, kThreads * kUnroll);
-  if (want_t && want_f)
-    expand_kernel<true, true><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
-  else if (want_t)
-    expand_kernel<true, false><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
-  else
-    expand_kernel<false, true><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
+  auto go = [&](auto tag_g) {
+    constexpr int G = decltype(tag_g)::value;
+    if (want_t && want_f)
+      expand_kernel<true, true, G><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
+    else if (want_t)
+      expand_kernel<true, false, G><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
+    else
+      expand_kernel<false, true, G><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
+  };
+  switch (L.dev.local) {
+    case 1: go(std::integral_constant<int, 1>{}); break;
+    case 2: go(std::integral_constant<int, 2>{}); break;
+    case 3: go(std::integral_constant<int, 3>{}); break;
+    case 4: go(std::integral_constant<int, 4>{}); break;
+    case 5: go(std::integral_constant<int, 5>{}); break;
+    case 6: go(std::integral_constant<int, 6>{}); break;
+    case 7: go(std::integral_constant<int, 7>{}); break;
+    default: go(std::integral_constant<int, 8>{}); break;
+  }
   return cudaGetLastError();
 }
 
