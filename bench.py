@@ -234,6 +234,27 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    def pcie_peak() -> dict:
+        """Pinned host <-> this GPU copy rate, all ranks at once (the host link
+        peak the engine's copies are judged against), measured in this run."""
+        n = 256 << 20
+        h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        d = torch.empty(n, dtype=torch.uint8, device=dev)
+        out = {}
+        for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+            fn()
+            torch.cuda.synchronize()
+            barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(4):
+                fn()
+            b.record()
+            b.synchronize()
+            out[name] = 4 * n / (a.elapsed_time(b) / 1e3) / 1e9
+        del h, d
+        return out
+
     def zero3_max_batch() -> int:
         """strategy.cpp:116-137 with a measured activation coefficient."""
         plan = S.StrategyPlan(S.StrategyKind.Zero3)
@@ -337,6 +358,7 @@ def main():
         return {"ms": ms, "per_step": per_step, "counters": counters, "kernels": kst, "clocks": clocks, "loss": loss_v,
                 "node_tx": node_tx, "cache": cache, "vol": vol, "e2e": e2e, "numa": numa}
 
+    pcie = pcie_peak()
     if args.batch <= 0:
         args.batch = zero3_max_batch()
     if args.strategy not in ("fcdp", "fcdp-comm"):
@@ -373,7 +395,10 @@ def main():
     value = tokens_per_step / (ms_step / 1e3)
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs")
-    kst = main_run["kernels"]
+    from paper_2602_06499_b200.engine import Engine as _E
+    allst = main_run["kernels"]
+    kst = {k: v for k, v in allst.items() if k in _E.KERNEL_CLASSES}
+    cst = {k: v for k, v in allst.items() if k in _E.COPY_CLASSES}
     dom = max(kst, key=lambda k: kst[k]["ms"]) if any(v["ms"] for v in kst.values()) else "adamw"
     d = kst[dom]
     per_launch_bytes = d["alg_bytes"] / max(d["launches"], 1)
@@ -392,7 +417,10 @@ def main():
                 "unit": unit_peak, "frac": (achieved / peak) if (achieved and peak) else None,
                 "traffic": ncu_traffic(dom) if not nvlink_bound else None, "alg_bytes_per_launch": per_launch_bytes,
                 "ms_per_launch": per_launch_ms, "peak_source": src,
-                "share_of_step": d["ms"] / main_run["ms"] if main_run["ms"] else None}
+                "share_of_step": d["ms"] / main_run["ms"] if main_run["ms"] else None,
+                # north_star's nominal denominators (B200: ~8 TB/s HBM3e, 900 GB/s NVLink per direction)
+                "peak_nominal": 900.0 if nvlink_bound else 8000.0,
+                "frac_of_nominal": (achieved / (900.0 if nvlink_bound else 8000.0)) if achieved else None}
     gpu_launches = sum(v["launches"] for v in kst.values())
     ag = {"fcdp_fwd": main_run["node_tx"]["nic_tx_fwd_ag"], "fcdp_bwd": main_run["node_tx"]["nic_tx_bwd_ag"],
           "fcdp_rs": main_run["node_tx"]["nic_tx_rs"],
@@ -411,6 +439,17 @@ def main():
         t_nic = nic_b / bw * 1e3
         link_bound = {"nic_bytes_per_node_per_step": nic_b, "nic_gbs": bw / 1e9, "nic_time_ms": t_nic,
                       "step_ms": ms_step, "frac": t_nic / ms_step if ms_step else None}
+    # host-link copies (FCDP-Cache and NIC staging): achieved GB/s of the copies
+    # themselves (bytes / their CUDA-event durations) against the PCIe rate
+    # measured in this run with every rank copying at once
+    copies = {}
+    for k, v in cst.items():
+        if not v["launches"]:
+            continue
+        gbs = v["alg_bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None
+        peak_c = pcie["d2h"] if k.endswith("d2h") else pcie["h2d"]
+        copies[k] = {"bytes_per_step": v["alg_bytes"] / args.steps, "copies_per_step": v["launches"] / args.steps,
+                     "GBps": gbs, "pcie_peak_gbps": peak_c, "frac": gbs / peak_c if gbs else None}
     kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
                    "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None} for k, v in kst.items()}
     line = {
@@ -420,6 +459,7 @@ def main():
         "data": "synthetic (counter-based token ids, random-init weights of the named architecture)",
         "config": workload_config(args, mc, N, g, world, seq),
         "e2e": main_run["e2e"], "gpu_launches": gpu_launches, "roofline": roofline, "link_bound": link_bound,
+        "copies": copies, "pcie_peak_gbps": pcie,
         "cpu_baseline": cpu, "clocks": main_run["clocks"],
         "ag_inter_bytes_per_step_per_node": ag,
         "zero3": ({"tokens_per_s": tokens_per_step / (z3["ms"] / z3_steps(args) / 1e3), "ms_per_step": z3["ms"] / z3_steps(args)}

@@ -325,9 +325,12 @@ void fcdp_engine_destroy(fcdp_engine* e);
 /* Per-kernel-class launch counts, CUDA-event device time and algorithmic bytes
  * of the engine's own kernels.  Classes: 0 gather/expand (intra all-gather),
  * 1 reduce-scatter slice (pull-reduce), 2 reduce-scatter finalize, 3 AdamW,
- * 4 local shard copies (pack into the slice buffer, ZeRO++ replica).
- * link_bytes: the part of the traffic that crossed NVLink (peer reads). */
-#define FCDP_KCLASSES 5
+ * 4 local shard copies (pack into the slice buffer, ZeRO++ replica); and the
+ * host-link copies: 5 FCDP-Cache D2H, 6 FCDP-Cache H2D, 7 NIC staging D2H,
+ * 8 NIC receive H2D (cudaMemcpyAsync, not kernels).
+ * link_bytes: the part of the traffic that crossed NVLink (peer reads) for
+ * classes 0-4, the PCIe bytes for classes 5-8. */
+#define FCDP_KCLASSES 9
 typedef struct fcdp_kernel_stats {
   uint64_t launches[FCDP_KCLASSES];
   double total_ms[FCDP_KCLASSES];  /* only while timing is on */

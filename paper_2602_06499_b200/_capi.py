@@ -94,8 +94,8 @@ class Counters(C.Structure):
 
 
 class KernelStats(C.Structure):
-    _fields_ = [("launches", C.c_uint64 * 5), ("total_ms", C.c_double * 5), ("alg_bytes", C.c_uint64 * 5),
-                ("timed_launches", C.c_uint64 * 5), ("link_bytes", C.c_uint64 * 5)]
+    _fields_ = [("launches", C.c_uint64 * 9), ("total_ms", C.c_double * 9), ("alg_bytes", C.c_uint64 * 9),
+                ("timed_launches", C.c_uint64 * 9), ("link_bytes", C.c_uint64 * 9)]
 
 
 COMPUTE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p)

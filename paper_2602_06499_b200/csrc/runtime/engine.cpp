@@ -583,7 +583,7 @@ void Engine::stage_one(int cls, cudaStream_t s, const void* src, std::size_t n, 
     for (int nn = 0; nn < N_; ++nn)
       if (nn != n_) wait_flag(s, nn * g_ + j_, consumed, id - ring);
   unsigned char* dst = host_dst ? host_dst : shm_->slot(rank_, cls, static_cast<int>(id % ring));
-  CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s));
+  timed(7, s, n, [&] { return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, s); }, n);
   write_flag(s, cls == 0 ? kAgStaged : kRsStaged, id);
   nic_->submit({cls, id, n * wire_mult, counter});
   shm_->post(rank_, cls == 0 ? kAgTxReady : kRsTxReady, id);
@@ -650,7 +650,7 @@ void Engine::exchange(int cls, cudaStream_t send_s, const std::vector<SendSeg>& 
       if (dst) {
         wait_flag(recv_s, r.src_rank, cls == 0 ? kAgTxReady : kRsTxReady, id);
         const unsigned char* src = pc.host_src ? pc.host_src : shm_->slot(r.src_rank, cls, static_cast<int>(id % ring));
-        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, recv_s));
+        timed(8, recv_s, n, [&] { return cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, recv_s); }, n);
         rx += n;
       }
       mark_consumed(cls, recv_s, r.src_rank / g_, id);  // read it, or it was never ours to read
@@ -778,12 +778,15 @@ void Engine::ev_h2d(const Event& e) {
   const unsigned char* H = host_cache_ + l.host_off * C;
   std::uint64_t bytes = 0;
   if (wt && l.slice_real_t) {
-    CK(cudaMemcpyAsync(X, H, l.slice_real_t * C, cudaMemcpyHostToDevice, s_gather_));
+    const std::size_t b = l.slice_real_t * C;
+    timed(6, s_gather_, b, [&] { return cudaMemcpyAsync(X, H, b, cudaMemcpyHostToDevice, s_gather_); }, b);
     bytes += l.slice_real_t * C;
   }
   if (wf && l.slice_real_f) {
-    CK(cudaMemcpyAsync(X + l.L.dev.slice_t * C, H + l.L.dev.slice_t * C, l.slice_real_f * C,
-                       cudaMemcpyHostToDevice, s_gather_));
+    const std::size_t b = l.slice_real_f * C;
+    timed(6, s_gather_, b, [&] {
+      return cudaMemcpyAsync(X + l.L.dev.slice_t * C, H + l.L.dev.slice_t * C, b, cudaMemcpyHostToDevice, s_gather_);
+    }, b);
     bytes += l.slice_real_f * C;
   }
   shm_->add(rank_, kCacheH2D, bytes);
@@ -863,15 +866,18 @@ void Engine::ev_d2h(const Event& e) {
     const bool own_staged = frozen ? cache_stage_f_[e.layer] : cache_stage_t_[e.layer];
     if (!own_staged || N_ == 1) {
       const std::int64_t real = frozen ? l.slice_real_f : l.slice_real_t;
-      if (real) CK(cudaMemcpyAsync(H + base, Xs, real * C, cudaMemcpyDeviceToHost, s_cache_));
+      const std::size_t b = static_cast<std::size_t>(real) * C;
+      if (real) timed(5, s_cache_, b, [&] { return cudaMemcpyAsync(H + base, Xs, b, cudaMemcpyDeviceToHost, s_cache_); }, b);
       return;
     }
     for (int m = 0; m < N_; ++m) {
       if (m == n_) continue;
       const std::int64_t real = l.L.real_chunks(frozen, j_ * N_ + m);
       if (real)
-        CK(cudaMemcpyAsync(H + base + m * shard * C, Xs + m * shard * C, real * C, cudaMemcpyDeviceToHost,
-                           s_cache_));
+        timed(5, s_cache_, static_cast<std::uint64_t>(real) * C, [&] {
+          return cudaMemcpyAsync(H + base + m * shard * C, Xs + m * shard * C, real * C, cudaMemcpyDeviceToHost,
+                                 s_cache_);
+        }, static_cast<std::uint64_t>(real) * C);
     }
   };
   const bool staged_any = (wt && cache_stage_t_[e.layer]) || (wf && cache_stage_f_[e.layer]);

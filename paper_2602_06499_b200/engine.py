@@ -138,6 +138,7 @@ class Engine:
         check(lib().fcdp_engine_reset_counters(self._h))
 
     KERNEL_CLASSES = ("gather_expand", "rs_slice", "rs_finalize", "adamw", "shard_copy")
+    COPY_CLASSES = ("cache_d2h", "cache_h2d", "staging_d2h", "staging_h2d")  # cudaMemcpyAsync, host link
 
     def set_timing(self, on: bool) -> None:
         check(lib().fcdp_engine_set_timing(self._h, int(on)))
@@ -148,7 +149,7 @@ class Engine:
         return {name: {"launches": int(k.launches[i]), "ms": float(k.total_ms[i]),
                        "alg_bytes": int(k.alg_bytes[i]), "timed_launches": int(k.timed_launches[i]),
                        "link_bytes": int(k.link_bytes[i])}
-                for i, name in enumerate(self.KERNEL_CLASSES)}
+                for i, name in enumerate(self.KERNEL_CLASSES + self.COPY_CLASSES)}
 
     def set_trace(self, on: bool) -> None:
         check(lib().fcdp_engine_set_trace(self._h, int(on)))
