@@ -140,6 +140,74 @@ def ncu_traffic(kernel_class: str):
         return None
 
 
+def isolated_rate(kernel_class: str, alg_bytes: float, eb: int, dev):
+    """The dominant kernel re-timed alone (after the timed region) at the live
+    per-launch size: stateless C-ABI launch on synthetic buffers, L2 flushed
+    between reps, CUDA events, median.  The live number in `roofline` includes
+    any time the kernel spent sharing SMs / HBM with concurrent work (the
+    driving model's backward GEMMs at N > 1); this one is the kernel itself."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2602_06499_b200 import _capi
+    lib = _capi.lib()
+    P = lambda t: C.c_void_p(t.data_ptr())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    keep = []
+
+    def dense_layout(chunks):
+        m = np.ones(chunks, np.uint8)
+        out = C.c_void_p()
+        _capi.check(lib.fcdp_layout_create(chunks, m.ctypes.data_as(C.POINTER(C.c_uint8)), eb, 1, 1, C.byref(out)))
+        return out
+
+    V = 16 // eb
+    if kernel_class == "adamw":
+        n = int(alg_bytes // (7 * 4 + eb)) // 4 * 4
+        w, m_, v_, g_ = (torch.zeros(n, dtype=torch.float32, device=dev) for _ in range(4))
+        par = torch.empty(n * eb, dtype=torch.uint8, device=dev)
+        cfg = _capi.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0, 1)
+        keep += [w, m_, v_, g_, par]
+        fn = lambda: _capi.check(lib.fcdp_adam_step(n, C.byref(cfg), P(w), P(m_), P(v_), P(g_), P(par), eb, None))
+    elif kernel_class in ("gather_expand", "shard_copy"):
+        chunks = int(alg_bytes // 32)
+        lay = dense_layout(chunks)
+        x = torch.empty(chunks * 16, dtype=torch.uint8, device=dev)
+        y = torch.empty_like(x)
+        keep += [x, y]
+        fn = lambda: _capi.check(lib.fcdp_expand(lay, (C.c_void_p * 1)(x.data_ptr()), None, P(y), 0, None))
+    elif kernel_class == "rs_slice":
+        chunks = int(alg_bytes // (16 + 16 * 4 // eb))  # dtype grads in, fp32 shard out
+        lay = dense_layout(chunks)
+        gbuf = torch.empty(chunks * 16, dtype=torch.uint8, device=dev)
+        own = torch.empty(chunks * V, dtype=torch.float32, device=dev)
+        wire = torch.empty(chunks * 16, dtype=torch.uint8, device=dev)
+        keep += [gbuf, own, wire]
+        fn = lambda: _capi.check(lib.fcdp_rs_slice(lay, (C.c_void_p * 1)(gbuf.data_ptr()), 0, 0, 1.0, 1, P(own),
+                                                   P(wire), None))
+    elif kernel_class == "rs_finalize":
+        n = int(alg_bytes // (2 * 4 + eb)) // 4 * 4
+        own, out = (torch.zeros(n, dtype=torch.float32, device=dev) for _ in range(2))
+        wire = torch.zeros(2 * n * eb, dtype=torch.uint8, device=dev)
+        keep += [own, out, wire]
+        fn = lambda: _capi.check(lib.fcdp_rs_finalize(n, 2, 0, eb, P(own), P(wire), n, 0.5, P(out), None))
+    else:
+        return None
+    ts = []
+    for i in range(7):
+        flush.fill_(i & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        if i >= 2:
+            ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    del keep
+    return {"ms_per_launch": ms, "achieved": alg_bytes / (ms / 1e3) / 1e9}
+
+
 def run_reference(args, world_n):
     """--impl reference: the oracle port of the path on the host cores (rank 0)."""
     rank, world, _ = env_rank()
@@ -415,12 +483,17 @@ def main():
         peak, unit_peak, src = hbm, "GB/s", "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     roofline = {"bound": "nvlink" if nvlink_bound else "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": unit_peak, "frac": (achieved / peak) if (achieved and peak) else None,
-                "traffic": ncu_traffic(dom) if not nvlink_bound else None, "alg_bytes_per_launch": per_launch_bytes,
+                "traffic": ncu_traffic(dom) if (not nvlink_bound and world == 1) else None,  # the ncu capture is the N=1 run "alg_bytes_per_launch": per_launch_bytes,
                 "ms_per_launch": per_launch_ms, "peak_source": src,
                 "share_of_step": d["ms"] / main_run["ms"] if main_run["ms"] else None,
                 # north_star's nominal denominators (B200: ~8 TB/s HBM3e, 900 GB/s NVLink per direction)
                 "peak_nominal": 900.0 if nvlink_bound else 8000.0,
                 "frac_of_nominal": (achieved / (900.0 if nvlink_bound else 8000.0)) if achieved else None}
+    if roofline["bound"] == "hbm":
+        iso = isolated_rate(dom, per_launch_bytes, mc.dtype_bytes, dev)
+        if iso:
+            iso["frac"] = iso["achieved"] / peak if peak else None
+            roofline["isolated"] = iso
     gpu_launches = sum(v["launches"] for v in kst.values())
     ag = {"fcdp_fwd": main_run["node_tx"]["nic_tx_fwd_ag"], "fcdp_bwd": main_run["node_tx"]["nic_tx_bwd_ag"],
           "fcdp_rs": main_run["node_tx"]["nic_tx_rs"],
