@@ -164,7 +164,9 @@ def isolated_rate(kernel_class: str, alg_bytes: float, eb: int, dev):
     V = 16 // eb
     if kernel_class == "adamw":
         n = int(alg_bytes // (7 * 4 + eb)) // 4 * 4
-        w, m_, v_, g_ = (torch.zeros(n, dtype=torch.float32, device=dev) for _ in range(4))
+        # real-valued inputs: an all-zero gradient sends the IEEE divisions down their slow path
+        w, g_ = torch.randn(n, device=dev), torch.randn(n, device=dev).mul_(1e-3)
+        m_, v_ = torch.zeros(n, device=dev), torch.zeros(n, device=dev)
         par = torch.empty(n * eb, dtype=torch.uint8, device=dev)
         cfg = _capi.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0, 1)
         keep += [w, m_, v_, g_, par]
@@ -187,7 +189,7 @@ def isolated_rate(kernel_class: str, alg_bytes: float, eb: int, dev):
                                                    P(wire), None))
     elif kernel_class == "rs_finalize":
         n = int(alg_bytes // (2 * 4 + eb)) // 4 * 4
-        own, out = (torch.zeros(n, dtype=torch.float32, device=dev) for _ in range(2))
+        own, out = torch.randn(n, device=dev), torch.empty(n, device=dev)
         wire = torch.zeros(2 * n * eb, dtype=torch.uint8, device=dev)
         keep += [own, out, wire]
         fn = lambda: _capi.check(lib.fcdp_rs_finalize(n, 2, 0, eb, P(own), P(wire), n, 0.5, P(out), None))
