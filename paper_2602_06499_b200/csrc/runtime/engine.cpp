@@ -41,6 +41,8 @@ using shardsim::EventKind;
 using shardsim::ParamSet;
 
 constexpr int kElided = -2;  // PendingSlice::slot of an elided (resident) reload
+constexpr int kAliasW = 3;   // w_of_layer_: the layer is read in place from this GPU's shard (G = 1)
+constexpr int kAliasX = -4;  // x_of_t_/x_of_f_: the gathered portion is the shard itself
 
 std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
 
@@ -168,6 +170,7 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   for (auto& e : x_reader_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&iter_done_, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&alias_fence_, cudaEventDisableTiming));
   for (auto& e : join_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
   exchange_handles();
@@ -197,6 +200,7 @@ Engine::~Engine() {
     cudaEventDestroy(t.b);
   }
   if (iter_done_) cudaEventDestroy(iter_done_);
+  if (alias_fence_) cudaEventDestroy(alias_fence_);
   for (cudaEvent_t e : join_)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : rs_kernel_done_)
@@ -363,6 +367,7 @@ void Engine::allocate() {
   for (auto& ev : ag_staged_) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   ag_staged_valid_.assign(L, 0);
   stepped_.assign(L, 0);
+  prev_retained_.assign(L, 0);
 }
 
 void Engine::exchange_handles() {
@@ -661,9 +666,40 @@ void Engine::exchange(int cls, cudaStream_t send_s, const std::vector<SendSeg>& 
 
 // ------------------------------------------------------------------ events
 
+bool Engine::alias_gather(const Event& e, bool wt, bool wf) {
+  // One GPU holding the whole model (G = 1) and a single-portion layer (dense
+  // trainable, or frozen-only): the shard IS the natural layer, so the gather
+  // is the identity and compute reads the shard in place - no copy.
+  static const char* env = std::getenv("FCDP_ALIAS");
+  if (G_ != 1 || zeropp_ || (env && std::strcmp(env, "0") == 0)) return false;
+  LayerRt& l = layers_[e.layer];
+  if (!((wt && !l.has_f) || (wf && !l.has_t))) return false;
+  w_of_layer_[e.layer] = kAliasW;
+  if (wt) x_of_t_[e.layer] = kAliasX;
+  if (wf) x_of_f_[e.layer] = kAliasX;
+  alias_used_ = true;
+  return true;
+}
+
+unsigned char* Engine::alias_ptr(int li) const {
+  const LayerRt& l = layers_[li];
+  return l.has_t ? param_t_ + l.off_t * kChunkBytes : param_f_ + l.off_f * kChunkBytes;
+}
+
+void Engine::fence_alias_reads(cudaStream_t s) {
+  // FCDP-Cache D2H of an aliased layer reads the shard that AdamW rewrites
+  if (!alias_used_) return;
+  CK(cudaEventRecord(alias_fence_, s_cache_));
+  CK(cudaStreamWaitEvent(s, alias_fence_, 0));
+}
+
 void Engine::ev_ag_inter(const Event& e, bool backward) {
   LayerRt& l = layers_[e.layer];
   const bool wt = wants_t(e.param_set) && l.has_t, wf = wants_f(e.param_set) && l.has_f;
+  if (alias_gather(e, wt, wf)) {
+    if (!mics_) shm_->add(rank_, backward ? kAgEventsBwd : kAgEventsFwd, 1);
+    return;
+  }
   cudaStream_t s = s_gather_;
   const std::size_t C = kChunkBytes;
   const int slot = begin_slice_fill(e.layer);
@@ -761,10 +797,17 @@ void Engine::ev_h2d(const Event& e) {
   // Frozen residency: a tau-retained layer whose retained buffer already holds
   // the frozen portion (version 0 forever) needs no reload -
   // the event's postcondition already holds.  Trainable data always moves.
-  if (!wt && wf && prog_->layer_retained[e.layer] && retained_[e.layer] &&
-      retained_content_[e.layer].layer == e.layer && retained_content_[e.layer].ver_f == 0) {
+  // At G = 1 a frozen-only layer retained in this and the previous iteration is
+  // resident as the shard itself (read in place, see alias_gather).
+  static const char* alias_env = std::getenv("FCDP_ALIAS");
+  const bool alias_resident = !wt && wf && !l.has_t && G_ == 1 && !zeropp_ &&
+                              !(alias_env && std::strcmp(alias_env, "0") == 0) &&
+                              prog_->layer_retained[e.layer] && prev_retained_[e.layer];
+  if (alias_resident || (!wt && wf && prog_->layer_retained[e.layer] && retained_[e.layer] &&
+                         retained_content_[e.layer].layer == e.layer && retained_content_[e.layer].ver_f == 0)) {
     PendingSlice& p = pending_h2d_[e.layer];
     p.slot = kElided;
+    p.alias = alias_resident;
     p.t = false;
     p.f = true;
     p.ver_f = 0;
@@ -837,7 +880,12 @@ void Engine::ev_ag_intra(const Event& e, bool backward) {
   }
   PendingSlice p = pending_h2d_[e.layer];
   if (p.slot == kElided) {  // frozen portion already resident in the retained buffer
-    w_buffer(e.layer);
+    if (p.alias) {
+      w_of_layer_[e.layer] = kAliasW;
+      x_of_f_[e.layer] = kAliasX;
+    } else {
+      w_buffer(e.layer);
+    }
     pending_h2d_[e.layer] = {};
     return;
   }
@@ -862,7 +910,8 @@ void Engine::ev_d2h(const Event& e) {
   auto store = [&](bool frozen, int slot) {
     const std::int64_t shard = frozen ? l.L.dev.shard_f : l.L.dev.shard_t;
     const std::size_t base = frozen ? l.L.dev.slice_t * C : 0;
-    const unsigned char* Xs = x_slot(j_, slot) + base;
+    const unsigned char* Xs = slot == kAliasX ? (frozen ? param_f_ + l.off_f * C : param_t_ + l.off_t * C)
+                                              : x_slot(j_, slot) + base;
     const bool own_staged = frozen ? cache_stage_f_[e.layer] : cache_stage_t_[e.layer];
     if (!own_staged || N_ == 1) {
       const std::int64_t real = frozen ? l.slice_real_f : l.slice_real_t;
@@ -884,14 +933,16 @@ void Engine::ev_d2h(const Event& e) {
   if (staged_any && N_ > 1) CK(cudaStreamWaitEvent(s_cache_, cache_staged_[e.layer], 0));
   if (wt) {
     slot_t = x_of_t_[e.layer];
-    if (slot_t < 0) throw shardsim::ProtocolError("d2h of a trainable portion that was not gathered");
+    if (slot_t < 0 && slot_t != kAliasX)
+      throw shardsim::ProtocolError("d2h of a trainable portion that was not gathered");
     store(false, slot_t);
     bytes += l.slice_real_t * C;
     l.host_version_t = static_cast<std::int64_t>(l.shard_version_t);
   }
   if (wf) {
     slot_f = x_of_f_[e.layer];
-    if (slot_f < 0) throw shardsim::ProtocolError("d2h of a frozen portion that was not gathered");
+    if (slot_f < 0 && slot_f != kAliasX)
+      throw shardsim::ProtocolError("d2h of a frozen portion that was not gathered");
     store(true, slot_f);
     bytes += l.slice_real_f * C;
     l.host_version_f = 0;
@@ -905,12 +956,17 @@ void Engine::ev_compute(const Event& e, bool backward) {
   const int li = e.layer;
   LayerRt& l = layers_[li];
   if (w_of_layer_[li] < 0) throw shardsim::ProtocolError("freshness: layer " + std::to_string(li) + " computed without a gather");
-  const WContent& wc = w_of_layer_[li] == 2 ? retained_content_[li] : w_content_[w_of_layer_[li]];
+  const WContent alias_wc{li, l.has_t ? static_cast<std::int64_t>(l.shard_version_t) : -1, l.has_f ? 0 : -1};
+  const WContent& wc = w_of_layer_[li] == kAliasW ? alias_wc
+                       : w_of_layer_[li] == 2    ? retained_content_[li]
+                                                 : w_content_[w_of_layer_[li]];
   if (wc.layer != li || (l.has_t && wc.ver_t != static_cast<std::int64_t>(l.shard_version_t)) ||
       (l.has_f && wc.ver_f != 0))
     throw shardsim::ProtocolError("freshness: layer " + std::to_string(li) +
                                   " would compute on parameters that are not at their current version");
-  unsigned char* W = w_of_layer_[li] == 2 ? retained_[li] : w_slots_[w_of_layer_[li]];
+  unsigned char* W = w_of_layer_[li] == kAliasW ? alias_ptr(li)
+                     : w_of_layer_[li] == 2    ? retained_[li]
+                                               : w_slots_[w_of_layer_[li]];
   void* grad = nullptr;
   if (backward && l.has_t) {
     const std::uint32_t u = ++u_;
@@ -931,7 +987,8 @@ void Engine::ev_compute(const Event& e, bool backward) {
   } else if (grad) {
     CK(cudaMemsetAsync(grad, 0, l.chunks * kChunkBytes, s_comp_));  // data-plane-only mode
   }
-  if (!backward && w_of_layer_[li] != 2) w_of_layer_[li] = -1;  // the slot is free for the backward re-gather
+  if (!backward && w_of_layer_[li] != 2 && !(w_of_layer_[li] == kAliasW && prog_->layer_retained[li]))
+    w_of_layer_[li] = -1;  // the slot is free for the backward re-gather
 }
 
 void Engine::ev_reduce_scatter(const Event& e) {
@@ -1059,6 +1116,7 @@ void Engine::adam_layer(int li, cudaStream_t s) {
                static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta2), step))};
   // the own shard must have left for the NIC before it is overwritten
   if (ag_staged_valid_[li]) CK(cudaStreamWaitEvent(s, ag_staged_[li], 0));
+  fence_alias_reads(s);
   const std::int64_t n = l.L.dev.shard_t * V_;
   const std::size_t o = static_cast<std::size_t>(l.off_t) * V_;
   timed(3, s, static_cast<std::uint64_t>(n) * (7 * sizeof(float) + eb_), [&] {
@@ -1069,6 +1127,7 @@ void Engine::adam_layer(int li, cudaStream_t s) {
 }
 
 void Engine::ev_optimizer(const Event&) {
+  fence_alias_reads(s_comp_);
   if (early_opt_) {
     for (std::size_t li = 0; li < layers_.size(); ++li)
       if (layers_[li].has_t && !stepped_[li]) adam_layer(static_cast<int>(li), s_comp_);
@@ -1146,6 +1205,7 @@ void Engine::begin(const shardsim::EventProgram& prog) {
   std::fill(x_of_f_.begin(), x_of_f_.end(), -1);
   std::fill(cache_stage_t_.begin(), cache_stage_t_.end(), 0);
   std::fill(stepped_.begin(), stepped_.end(), 0);
+  alias_used_ = false;
   std::fill(ag_staged_valid_.begin(), ag_staged_valid_.end(), 0);
   {
     static const char* eo = std::getenv("FCDP_EARLY_OPT");
@@ -1224,11 +1284,13 @@ void Engine::end(std::vector<shardsim::ParamState>& states) {
     CK(cudaStreamWaitEvent(s_comp_, join_[i], 0));
   }
   CK(cudaEventRecord(iter_done_, s_comp_));
-  for (std::size_t li = 0; li < layers_.size(); ++li)
+  for (std::size_t li = 0; li < layers_.size(); ++li) {
     if (!prog.layer_retained[li] && retained_[li]) {
       // retention is per iteration; the buffer stays allocated for reuse
       retained_content_[li] = {};
     }
+    prev_retained_[li] = prog.layer_retained[li] ? 1 : 0;
+  }
   states = shardsim::step_state(std::move(states), prog);
   prog_ = nullptr;
 }

@@ -219,6 +219,13 @@ class Engine {
   std::vector<cudaEvent_t> ag_staged_;        // per layer: own shard staged for the NIC (s_agsend_)
   std::vector<char> ag_staged_valid_;
   void adam_layer(int li, cudaStream_t s);
+  // G = 1: gathers of single-portion layers alias the shard (no copy)
+  bool alias_used_ = false;
+  std::vector<char> prev_retained_;  // per layer: retained in the previous executed program
+  cudaEvent_t alias_fence_ = nullptr;
+  bool alias_gather(const shardsim::Event& e, bool wt, bool wf);
+  unsigned char* alias_ptr(int li) const;
+  void fence_alias_reads(cudaStream_t s);
 
   // per-iteration bookkeeping
   struct PendingSlice {
@@ -226,6 +233,7 @@ class Engine {
     std::uint32_t q = 0;
     bool t = false, f = false;
     std::int64_t ver_t = -1, ver_f = -1;
+    bool alias = false;  // elided reload served by the shard itself (G = 1)
   };
   std::vector<PendingSlice> pending_h2d_;             // per layer (H2D -> AgIntra)
   std::vector<int> x_of_t_, x_of_f_;                  // per layer: X slot holding fresh gather
