@@ -3,15 +3,18 @@
 // Event semantics follow the reference builder (proj/src/schedule.cpp:107-292)
 // and Algorithm 1; the data layout is the one in
 // common/layout.hpp.  Cross-rank ordering uses monotone 32-bit flags in the
-// shared control block:
+// shared control block, written and awaited by the GPU streams themselves
+// (cuStreamWriteValue32 / cuStreamWaitValue32):
 //   slice fill q :  [wait peers SliceFree >= q-K] fill X[q%K] [SliceReady=q]
 //   pull       q :  [wait peers SliceReady >= q] expand/gather -> W [SliceFree=q]
-//   inter send s :  [wait receivers RxDone >= s-K] D2H -> staging slot
-//                   -> NIC thread paces, then TxReady=s
-//   inter recv s :  [wait senders TxReady >= s] H2D from their slots [RxDone=s]
+//   NIC piece  p :  [wait receivers Consumed >= p-ring] D2H into ring slot (or
+//                   straight into the host cache: write-once staging) [Staged=p]
+//                   -> NIC thread paces the wire, then TxReady=p
+//   receive    p :  [wait sender TxReady >= p] H2D from its slot [Consumed=p]
 //   rs         u :  [GradReady=u] [wait peers GradReady >= u] pull-reduce [GradFree=u]
-// Every rank walks the same program, so sequence numbers agree and no wait
-// can close a cycle (each rank publishes before it waits on the same index).
+// Every rank walks the same program, so sequence numbers agree, and a rank
+// enqueues a wait only after the producing write was posted by its peer's host
+// (SharedBlock::await_posted), so no wait can close a cycle.
 #include "runtime/engine.hpp"
 
 #include <algorithm>
@@ -19,11 +22,12 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
-#include <thread>
-#include <sys/mman.h>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
+
+#include <sys/mman.h>
 
 #include "capi_util.hpp"
 #include "runtime/streamops.hpp"
