@@ -27,6 +27,7 @@
 #include <string>
 #include <thread>
 
+#include <nvtx3/nvToolsExt.h>
 #include <sys/mman.h>
 
 #include "capi_util.hpp"
@@ -62,6 +63,31 @@ T* dalloc(std::size_t bytes, const char* what) {
   check_cuda(cudaMemset(p, 0, std::max<std::size_t>(bytes, 256)), what);
   return static_cast<T*>(p);
 }
+
+// NVTX: one host range per executed program event ("fcdp" domain, message
+// "<kind> L<layer>"), so ncu can select an event's kernels
+// (--nvtx --nvtx-include "fcdp@reduce_scatter*").  Header-only NVTX3: free when
+// no tool is attached.
+nvtxDomainHandle_t nvtx_domain() {
+  static nvtxDomainHandle_t d = nvtxDomainCreateA("fcdp");
+  return d;
+}
+
+struct NvtxRange {
+  explicit NvtxRange(const shardsim::Event& e) {
+    char msg[64];
+    std::snprintf(msg, sizeof(msg), "%s L%d", shardsim::to_string(e.kind), e.layer);
+    nvtxEventAttributes_t a{};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = msg;
+    nvtxDomainRangePushEx(nvtx_domain(), &a);
+  }
+  ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 bool wants_t(ParamSet s) { return s != ParamSet::FrozenOnly; }
 bool wants_f(ParamSet s) { return s != ParamSet::TrainableOnly; }
@@ -1241,6 +1267,7 @@ void Engine::exec(std::uint32_t event_id) {
   static const bool debug = std::getenv("FCDP_DEBUG") != nullptr;
   {
     const Event& e = prog.events[event_id];
+    const NvtxRange nvtx_range(e);
     cudaStream_t s = stream_of[e.id];
     if (debug)
       std::fprintf(stderr, "[fcdp r%d] it=%llu enqueue ev %u %s layer %d\n", rank_,
