@@ -66,6 +66,36 @@ def test_rs_slice_against_numpy():
                     assert np.array_equal(ownf[:(hi - lo) * 8], (tvec[lo * 8:hi * 8] * np.float32(0.125)))
 
 
+def test_mics_replica_sum_against_numpy():
+    """MiCS replica gradient sync (engine mics_grad_sync): rs_slice with no own
+    shard puts the whole node-reduced slice on the wire; rs_finalize with
+    node = -1 sums every node's wire contribution in node order, so all
+    replicas produce identical bits."""
+    chunks, N, g = 200, 3, 2
+    rng = np.random.default_rng(4)
+    m = np.ones(chunks, np.uint8)
+    geo = O.geom(chunks, m, 1, g)  # MiCS: shards over the node's g GPUs only
+    per_node = [[O.f32_to_bf16(rng.standard_normal(chunks * 8).astype(np.float32)) for _ in range(g)]
+                for _ in range(N)]
+    sh = geo.shard_t * 8
+    for j in range(g):
+        wires = []
+        for n in range(N):
+            own, wire = O.rs_slice(geo, m, 2, per_node[n], j, -1, 1.0 / (N * g), False)
+            assert not own.any()  # nothing kept back in fp32
+            acc = np.zeros(chunks * 8, np.float32)
+            for x in per_node[n]:
+                acc = (acc + O.bf16_to_f32(x)).astype(np.float32)
+            assert np.array_equal(wire[:sh], O.f32_to_bf16(acc[j * sh:(j + 1) * sh]))
+            wires.append(wire[:sh])
+        rx = np.concatenate(wires)
+        got = O.rs_finalize(np.zeros(sh, np.float32), rx, N, -1, 2, sh, 1.0 / (N * g))
+        exp = np.zeros(sh, np.float32)
+        for w in wires:
+            exp = (exp + O.bf16_to_f32(w)).astype(np.float32)
+        assert np.array_equal(got, (exp * np.float32(1.0 / (N * g))).astype(np.float32))
+
+
 def test_adam_against_numpy():
     rng = np.random.default_rng(2)
     n = 1000
