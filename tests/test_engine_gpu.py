@@ -192,3 +192,43 @@ def test_engine_stepwise_executor(tmp_path, built, N, g, strategy, kind):
         pytest.skip(f"needs {N * g} GPUs")
     cfg, dumps = run_job(tmp_path, N, g, strategy, 2, kind, stepwise=True)
     check_job(cfg, dumps)
+
+
+_ORDER_SCRIPT = r"""
+import sys, uuid
+sys.path.insert(0, sys.argv[1])
+from paper_2602_06499_b200 import shardsim as S
+from paper_2602_06499_b200.engine import Engine, _States
+from paper_2602_06499_b200._capi import lib
+PROTOCOL = -2  # FCDP_ERR_PROTOCOL
+model = S.ModelSpec([S.LayerSpec(i, 8 * 64, 1.0) for i in range(3)], 2)
+topo = S.make_topology(1, 1)
+plan = S.StrategyPlan(S.StrategyKind.Fcdp)
+eng = Engine(model, topo, plan, rank=0, world_size=1, device=0, shm_name=f"fcdp_order_{uuid.uuid4().hex[:10]}",
+             timeout_s=60.0)
+eng.init_params(1, [])
+states = S.init_param_states(model)
+prog = S.build_iteration(plan, model, topo, states, 1)
+assert lib().fcdp_engine_exec(eng._h, 0) == PROTOCOL        # exec outside begin/end
+assert lib().fcdp_engine_begin(eng._h, prog.ptr) == 0
+assert lib().fcdp_engine_exec(eng._h, 1) == PROTOCOL        # id 0 must come first
+assert lib().fcdp_engine_begin(eng._h, prog.ptr) == PROTOCOL  # a program is already in progress
+st = _States.from_list(states)
+assert lib().fcdp_engine_end(eng._h, st.ptr) == PROTOCOL     # end before every event ran
+for e in prog.events:
+    assert lib().fcdp_engine_exec(eng._h, e.id) == 0
+assert lib().fcdp_engine_exec(eng._h, len(prog.events)) == PROTOCOL  # past the end
+assert lib().fcdp_engine_end(eng._h, st.ptr) == 0
+eng.sync()
+assert all(p.version == 1 and p.host_cached_version == 0 for p in st.to_list())  # step_state applied
+print("order-ok")
+"""
+
+
+def test_engine_exec_order_enforced(tmp_path, built):
+    """fcdp_engine_exec rejects out-of-order / repeated / past-the-end ids and a
+    second begin with FCDP_ERR_PROTOCOL (the stepwise executor contract)."""
+    if _ngpu() < 1:
+        pytest.skip("needs a GPU")
+    r = subprocess.run([sys.executable, "-c", _ORDER_SCRIPT, str(ROOT)], capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and "order-ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
