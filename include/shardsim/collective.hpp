@@ -1,8 +1,8 @@
-// Byte-splitting rules for evenly sharded bulk-synchronous collectives.
-//
-// Reference: proj/include/shardsim/collective.hpp:8-33.  Every byte count the
-// cost model reports - and every byte counter the B200 NIC emulator keeps -
-// is defined through these two helpers, so parity is integer equality.
+// How many bytes an evenly sharded all-gather / reduce-scatter moves - the
+// unit of every count in this project (cost model, NIC emulator counters,
+// bench).  Same two functions and constants as the reference header
+// (proj/include/shardsim/collective.hpp:8-33), so byte parity is an integer
+// comparison.
 #pragma once
 
 #include <cassert>
@@ -10,29 +10,28 @@
 
 namespace shardsim {
 
-inline constexpr std::uint64_t kKiB = std::uint64_t{1} << 10;
-inline constexpr std::uint64_t kMiB = std::uint64_t{1} << 20;
-inline constexpr std::uint64_t kGiB = std::uint64_t{1} << 30;
+inline constexpr std::uint64_t kKiB = 1024ull;
+inline constexpr std::uint64_t kMiB = 1024ull * kKiB;
+inline constexpr std::uint64_t kGiB = 1024ull * kMiB;
 
 namespace detail {
-// floor(x * (k - 1) / k) without forming the (possibly overflowing) product.
-inline std::uint64_t all_but_one_share(std::uint64_t x, std::uint64_t k) {
-  const std::uint64_t q = x / k, r = x % k;
-  return q * (k - 1) + (r * (k - 1)) / k;
+// (k - 1) / k of x, rounded down, computed without x * (k - 1) overflowing.
+inline std::uint64_t share_of_peers(std::uint64_t x, std::uint64_t k) {
+  return (x / k) * (k - 1) + ((x % k) * (k - 1)) / k;
 }
 }  // namespace detail
 
-/// Bytes through one node's NIC when `payload` bytes, sharded over
-/// `scope_nodes` nodes, are all-gathered (or reduce-scattered).
-inline std::uint64_t ag_inter_bytes(std::uint64_t payload, int scope_nodes) {
-  assert(scope_nodes >= 1);
-  return scope_nodes > 1 ? detail::all_but_one_share(payload, std::uint64_t(scope_nodes)) : 0;
+// One node's NIC bytes for a collective over `nodes` nodes of a `bytes` payload
+// (zero for a single node).
+inline std::uint64_t ag_inter_bytes(std::uint64_t bytes, int nodes) {
+  assert(nodes >= 1);
+  return nodes <= 1 ? 0 : detail::share_of_peers(bytes, static_cast<std::uint64_t>(nodes));
 }
 
-/// Bytes each GPU moves in a ring all-gather of `payload` over `ring_gpus`.
-inline std::uint64_t ring_intra_bytes(std::uint64_t payload, int ring_gpus) {
-  assert(ring_gpus >= 1);
-  return ring_gpus > 1 ? detail::all_but_one_share(payload, std::uint64_t(ring_gpus)) : 0;
+// One GPU's bytes in a ring all-gather of `bytes` over `gpus` GPUs.
+inline std::uint64_t ring_intra_bytes(std::uint64_t bytes, int gpus) {
+  assert(gpus >= 1);
+  return gpus <= 1 ? 0 : detail::share_of_peers(bytes, static_cast<std::uint64_t>(gpus));
 }
 
 }  // namespace shardsim
