@@ -140,6 +140,28 @@ def ncu_traffic(kernel_class: str):
         return None
 
 
+def control_plane_timing(mc, strategy: str, N: int, g: int, iters: int = 1000):
+    """BASELINE.md §3 "Timing 1": build_iteration + step_state + comm_volume per
+    step on the host, through the compiled reference (oracle/_ref/time_ref, built
+    from /root/reference's own sources) and through this project's libfcdp
+    (time_ours), same driver source (tests/cpp/control_plane_timer.cpp)."""
+    params = [str(d.numel) for d in mc.layer_defs()]
+    out = {}
+    for key, exe in (("reference_us_per_step", "time_ref"), ("ours_us_per_step", "time_ours")):
+        path = ROOT / "oracle" / "_ref" / exe
+        if not path.exists():
+            continue
+        try:
+            r = subprocess.run([str(path), strategy, str(N), str(g), str(iters), str(mc.dtype_bytes)] + params,
+                               capture_output=True, text=True, timeout=60)
+            out[key] = json.loads(r.stdout)["us_per_step"]
+        except Exception:
+            pass
+    if out:
+        out["note"] = "host CPU, 1 thread; model = the bench's explicit layer list"
+    return out or None
+
+
 def isolated_rate(kernel_class: str, alg_bytes: float, eb: int, dev):
     """The dominant kernel re-timed alone (after the timed region) at the live
     per-launch size: stateless C-ABI launch on synthetic buffers, L2 flushed
@@ -242,7 +264,7 @@ def run_reference(args, world_n):
             "dtype": "bf16" if mc.dtype_bytes == 2 else "fp32", "data": "synthetic",
             "config": workload_config(args, mc, N, g, world_n, seq),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-                             "sample": r["sample"]},
+                             "sample": r["sample"], "control_plane": control_plane_timing(mc, args.strategy, N, g)},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -460,7 +482,7 @@ def main():
         from oracle.cpu_step import cpu_step_sample
         r = cpu_step_sample(args.preset, batch=args.batch, seq=seq, repeats=2)
         cpu = {"value": r["tokens_per_s_per_gpu"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-               "sample": r["sample"]}
+               "sample": r["sample"], "control_plane": control_plane_timing(mc, args.strategy, N, g)}
 
     if rank != 0:
         if world > 1:

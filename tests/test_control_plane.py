@@ -129,3 +129,20 @@ def test_serialize_matches_python_events(built):
         assert int(f[0]) == e.id and f[1] == names[int(e.kind)]
         assert f[4] == str(e.bytes_total)
         assert f[5] == "deps=" + ",".join(map(str, e.deps))
+
+
+def test_control_plane_timer_reference_vs_ours(built):
+    """BASELINE.md §3 "Timing 1": the same timing driver linked against the
+    compiled reference and against libfcdp walks identical programs (events per
+    step, comm_volume checksum)."""
+    import json
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    ref, ours = root / "oracle" / "_ref" / "time_ref", root / "oracle" / "_ref" / "time_ours"
+    if not ref.exists() or not ours.exists():
+        pytest.skip("timing drivers not built (needs /root/reference)")
+    args = ["fcdp-comm", "2", "4", "20", "2"] + [str(x) for x in (131072000, *([202907648] * 4), 131076096)]
+    a = json.loads(subprocess.run([str(ref)] + args, capture_output=True, text=True, check=True).stdout)
+    b = json.loads(subprocess.run([str(ours)] + args, capture_output=True, text=True, check=True).stdout)
+    assert a["events_per_step"] == b["events_per_step"] and a["check"] == b["check"]
