@@ -10,5 +10,5 @@ $CMD > gpurun_out/plain.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on \
     -k regex:"adam_kernel|concat_kernel|expand_kernel|rs_dense_kernel|rs_masked_kernel|rs_finalize_kernel|copy_kernel" \
-    -s 40 -c 8 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+    -s 20 -c 6 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
 echo profile-done
