@@ -514,12 +514,16 @@ def main():
         peak, unit_peak, src = hbm, "GB/s", "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     roofline = {"bound": "nvlink" if nvlink_bound else "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": unit_peak, "frac": (achieved / peak) if (achieved and peak) else None,
-                "traffic": ncu_traffic(dom) if (not nvlink_bound and world == 1) else None,  # the ncu capture is the N=1 run "alg_bytes_per_launch": per_launch_bytes,
+                # the committed ncu capture is the default N=1 GPT-2 run; other configs have other launch sizes
+                "traffic": ncu_traffic(dom) if (not nvlink_bound and world == 1 and args.preset == "gpt2-1.3b") else None, "alg_bytes_per_launch": per_launch_bytes,
                 "ms_per_launch": per_launch_ms, "peak_source": src,
                 "share_of_step": d["ms"] / main_run["ms"] if main_run["ms"] else None,
                 # north_star's nominal denominators (B200: ~8 TB/s HBM3e, 900 GB/s NVLink per direction)
                 "peak_nominal": 900.0 if nvlink_bound else 8000.0,
                 "frac_of_nominal": (achieved / (900.0 if nvlink_bound else 8000.0)) if achieved else None}
+    if per_launch_bytes < 64e6:
+        # a few MB per launch (PEFT trainable slices): launch latency, not bandwidth, bounds it
+        roofline["note"] = f"{per_launch_bytes / 1e6:.1f} MB per launch: launch-latency regime"
     if roofline["bound"] == "hbm":
         iso = isolated_rate(dom, per_launch_bytes, mc.dtype_bytes, dev)
         if iso:
