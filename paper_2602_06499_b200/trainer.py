@@ -14,14 +14,14 @@ from the buffer the backward pass re-gathered - ZeRO-3/FCDP semantics
 """
 from __future__ import annotations
 
-from typing import Dict, List, Optional, Sequence
+from typing import Dict, List, Optional
 
 import numpy as np
 import torch
 
 from . import shardsim as S
 from .driving_model import LayerDef, ModelConfig, layer_forward
-from .engine import BWD, FWD, Engine
+from .engine import FWD, Engine
 from .tensors import device_view
 
 

@@ -17,7 +17,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from tests.engine_oracle import Sim, grad_coeff
+from tests.engine_oracle import Sim
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu

@@ -1,5 +1,5 @@
 """Probe cudaHostRegister limits on POSIX shm regions (sizes, flags)."""
-import ctypes, mmap, os, sys
+import ctypes, mmap, os
 import torch
 torch.cuda.init()
 cudart = ctypes.CDLL("libcudart.so.12") if False else None
