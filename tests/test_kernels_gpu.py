@@ -222,3 +222,32 @@ def test_tma_bulk_copy_path(built):
     r = subprocess.run([sys.executable, "-c", _TMA_SCRIPT, root], env=dict(os.environ, FCDP_COPY="tma"),
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "tma-ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("eb", [2, 4])
+def test_adam_special_values_bit_exact(built, eb):
+    """AdamW on gradients that exercise the IEEE division / sqrt edge paths:
+    exact zeros (0/eps), denormal squares, huge and tiny magnitudes."""
+    from paper_2602_06499_b200 import _capi
+    dev = _dev()
+    lib = built
+    rng = np.random.default_rng(17)
+    n = 4096
+    g = np.concatenate([np.zeros(1024, np.float32),                               # 0 -> m = v = 0 paths
+                        (rng.standard_normal(1024) * 1e-22).astype(np.float32),   # g*g underflows to denormal/0
+                        (rng.standard_normal(1024) * 1e18).astype(np.float32),    # g*g near the fp32 max
+                        (rng.standard_normal(1024) * 1e-3).astype(np.float32)])
+    w = rng.standard_normal(n).astype(np.float32)
+    m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+    p = np.zeros(n, np.uint16 if eb == 2 else np.float32)
+    dw, dm, dv, dg = (torch.from_numpy(a.copy()).to(dev) for a in (w, m, v, g))
+    dp = torch.zeros(n * eb, dtype=torch.uint8, device=dev)
+    for step in (1, 2):
+        O.adam(w, m, v, g, p, 1e-3, 0.9, 0.95, 1e-8, 0.1, step)
+        cfg = _capi.AdamConfig(1e-3, 0.9, 0.95, 1e-8, 0.1, step)
+        _capi.check(lib.fcdp_adam_step(n, C.byref(cfg), _ptr(dw), _ptr(dm), _ptr(dv), _ptr(dg), _ptr(dp), eb, None))
+        torch.cuda.synchronize()
+        assert np.array_equal(dw.cpu().numpy().view(np.uint32), w.view(np.uint32)), step
+        assert np.array_equal(dm.cpu().numpy().view(np.uint32), m.view(np.uint32)), step
+        assert np.array_equal(dv.cpu().numpy().view(np.uint32), v.view(np.uint32)), step
+        assert np.array_equal(dp.cpu().numpy(), p.view(np.uint8)), step
