@@ -39,7 +39,7 @@ def _u8(a: np.ndarray, dev):
 
 
 SIZES = [1, 33, 4096 + 7]
-GEOS = [(1, 1), (2, 1), (1, 4), (2, 2), (2, 4), (4, 2)]
+GEOS = [(1, 1), (2, 1), (1, 4), (2, 2), (2, 4), (4, 2), (1, 8), (8, 1), (1, 3)]
 
 
 @pytest.mark.parametrize("chunks", SIZES)
@@ -89,7 +89,7 @@ def test_partition_bit_exact(built, chunks):
 
 
 @pytest.mark.parametrize("eb", [2, 4])
-@pytest.mark.parametrize("N,g", [(1, 1), (2, 1), (1, 4), (2, 2), (2, 4)])
+@pytest.mark.parametrize("N,g", [(1, 1), (2, 1), (1, 4), (2, 2), (2, 4), (1, 8), (1, 3)])
 def test_rs_slice_bit_exact(built, eb, N, g):
     from paper_2602_06499_b200._capi import check
     dev = _dev()
