@@ -21,7 +21,7 @@ def test_partition_roundtrip(chunks):
         assert np.array_equal(f.reshape(-1, 16), c[~m.astype(bool)])
 
 
-@pytest.mark.parametrize("N,g", [(1, 1), (2, 1), (1, 4), (2, 2), (2, 4), (4, 2)])
+@pytest.mark.parametrize("N,g", [(1, 1), (2, 1), (1, 4), (2, 2), (2, 4), (4, 2), (1, 8), (8, 1), (2, 3)])
 def test_expand_equals_unpartition_of_slices(N, g):
     chunks = 517
     rng = np.random.default_rng(7)
