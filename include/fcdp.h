@@ -292,7 +292,11 @@ int fcdp_engine_init_params(fcdp_engine* e, uint64_t seed, const fcdp_init_range
 int fcdp_engine_set_adam(fcdp_engine* e, const fcdp_adam_config* cfg);
 int fcdp_engine_set_compute(fcdp_engine* e, fcdp_compute_fn fn, void* user);
 /* Execute one program (built for this engine's plan/model/topology) and apply
- * step_state.  Asynchronous: returns once every event is enqueued. */
+ * step_state.  Asynchronous: returns once every event is enqueued.
+ * The reference has no executor: it stops at build_iteration
+ * (proj/src/schedule.cpp:341-352) and step_state (schedule.cpp:354-387).  The
+ * event semantics executed here are Algorithm 1 and the
+ * builder's event meanings (schedule.cpp:107-292). */
 int fcdp_engine_run(fcdp_engine* e, const fcdp_program* program, fcdp_states* states);
 /* The same, driven event by event by an external executor that walks
  * EventProgram.events in id order (SURVEY §8(b) caller): begin, then exec for
