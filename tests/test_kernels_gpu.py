@@ -251,3 +251,48 @@ def test_adam_special_values_bit_exact(built, eb):
         assert np.array_equal(dm.cpu().numpy().view(np.uint32), m.view(np.uint32)), step
         assert np.array_equal(dv.cpu().numpy().view(np.uint32), v.view(np.uint32)), step
         assert np.array_equal(dp.cpu().numpy(), p.view(np.uint8)), step
+
+
+def test_expand_partition_random_shapes_bit_exact(built):
+    """Randomised: sizes 1..3000 chunks, any mask density, every node x GPU shape
+    up to 8 GPUs, every portion set - CUDA expand and partition vs the oracle."""
+    hyp = pytest.importorskip("hypothesis")
+    from hypothesis import given, settings, strategies as st
+    from paper_2602_06499_b200._capi import check
+    dev = _dev()
+    lib = built
+
+    @settings(max_examples=40, deadline=None, derandomize=True)
+    @given(chunks=st.integers(1, 3000), density=st.floats(0.0, 1.0),
+           shape=st.sampled_from([(1, 1), (2, 1), (1, 2), (2, 2), (1, 4), (2, 4), (4, 2), (1, 8), (8, 1), (2, 3)]),
+           seed=st.integers(0, 2**31 - 1), pset=st.sampled_from([0, 1, 2]))
+    def run(chunks, density, shape, seed, pset):
+        N, g = shape
+        rng = np.random.default_rng(seed)
+        m = (rng.random(chunks) < density).astype(np.uint8)
+        geo = O.geom(chunks, m, N, g)
+        lay = _layout(lib, chunks, m, 2, N, g)
+        try:
+            nat = rng.integers(0, 256, chunks * 16, dtype=np.uint8)
+            t, f = O.partition(nat, m)
+            dnat = _u8(nat, dev)
+            dt = torch.zeros(max(geo.slice_t * g, 1) * 16, dtype=torch.uint8, device=dev)
+            df = torch.zeros(max(geo.slice_f * g, 1) * 16, dtype=torch.uint8, device=dev)
+            check(lib.fcdp_partition(lay, _ptr(dnat), _ptr(dt), _ptr(df), None))
+            torch.cuda.synchronize()
+            assert np.array_equal(dt.cpu().numpy()[:t.size], t)
+            assert np.array_equal(df.cpu().numpy()[:f.size], f)
+            T = (C.c_void_p * g)(*[dt.data_ptr() + j * geo.slice_t * 16 for j in range(g)])
+            F = (C.c_void_p * g)(*[df.data_ptr() + j * geo.slice_f * 16 for j in range(g)])
+            out = torch.full((chunks * 16,), 0x5A, dtype=torch.uint8, device=dev)
+            check(lib.fcdp_expand(lay, T, F, _ptr(out), pset, None))
+            torch.cuda.synchronize()
+            tp = dt.cpu().numpy(); fp = df.cpu().numpy()
+            ref = np.full(chunks * 16, 0x5A, np.uint8)
+            O.expand(geo, m, [tp[j * geo.slice_t * 16:(j + 1) * geo.slice_t * 16] for j in range(g)],
+                     [fp[j * geo.slice_f * 16:(j + 1) * geo.slice_f * 16] for j in range(g)], ref, pset)
+            assert np.array_equal(out.cpu().numpy(), ref)
+        finally:
+            lib.fcdp_layout_destroy(lay)
+
+    run()
