@@ -296,3 +296,53 @@ def test_expand_partition_random_shapes_bit_exact(built):
             lib.fcdp_layout_destroy(lay)
 
     run()
+
+
+def test_rs_random_shapes_bit_exact(built):
+    """Randomised reduce-scatter: random masks / sizes / shapes (g up to 8) and
+    both dtypes; intra-node RS kernel (own fp32 shard + wire) then the
+    inter-node epilogue, each vs the oracle bit for bit."""
+    pytest.importorskip("hypothesis")
+    from hypothesis import given, settings, strategies as st
+    from paper_2602_06499_b200._capi import check
+    dev = _dev()
+    lib = built
+
+    @settings(max_examples=25, deadline=None, derandomize=True)
+    @given(chunks=st.integers(1, 1500), density=st.floats(0.01, 1.0),
+           shape=st.sampled_from([(1, 1), (2, 1), (1, 2), (2, 2), (1, 4), (2, 4), (4, 2), (1, 8), (3, 2)]),
+           eb=st.sampled_from([2, 4]), seed=st.integers(0, 2**31 - 1))
+    def run(chunks, density, shape, eb, seed):
+        N, g = shape
+        V = 16 // eb
+        rng = np.random.default_rng(seed)
+        m = (rng.random(chunks) < density).astype(np.uint8)
+        geo = O.geom(chunks, m, N, g)
+        lay = _layout(lib, chunks, m, eb, N, g)
+        try:
+            xs = [rng.standard_normal(chunks * V).astype(np.float32) for _ in range(g)]
+            grads = [O.f32_to_bf16(a) for a in xs] if eb == 2 else xs
+            dg = [_u8(a, dev) for a in grads]
+            G = (C.c_void_p * g)(*[t.data_ptr() for t in dg])
+            j, n = int(rng.integers(0, g)), int(rng.integers(0, N))
+            scale = 1.0 / (N * g)
+            own, wire = O.rs_slice(geo, m, eb, grads, j, n, scale, N == 1)
+            down = torch.zeros(max(own.size, 4), dtype=torch.float32, device=dev)
+            dwire = torch.zeros(max(wire.nbytes, 16), dtype=torch.uint8, device=dev)
+            check(lib.fcdp_rs_slice(lay, G, j, n, scale, int(N == 1), _ptr(down), _ptr(dwire), None))
+            torch.cuda.synchronize()
+            assert np.array_equal(down.cpu().numpy()[:own.size].view(np.uint32), own.view(np.uint32))
+            if N > 1 and geo.shard_t:
+                sh = geo.shard_t * V
+                rx = (O.f32_to_bf16(rng.standard_normal(N * sh).astype(np.float32)) if eb == 2
+                      else rng.standard_normal(N * sh).astype(np.float32))
+                ref = O.rs_finalize(own[:sh].copy(), rx, N, n, eb, sh, scale)
+                drx, downs = _u8(rx, dev), down[:sh].contiguous()
+                out = torch.zeros(sh, dtype=torch.float32, device=dev)
+                check(lib.fcdp_rs_finalize(sh, N, n, eb, _ptr(downs), _ptr(drx), sh, scale, _ptr(out), None))
+                torch.cuda.synchronize()
+                assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+        finally:
+            lib.fcdp_layout_destroy(lay)
+
+    run()
