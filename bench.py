@@ -232,39 +232,88 @@ def isolated_rate(kernel_class: str, alg_bytes: float, eb: int, dev):
     return {"ms_per_launch": ms, "achieved": alg_bytes / (ms / 1e3) / 1e9}
 
 
+def gpu_capacity_bytes_smi() -> int:
+    """This box's GPU memory without creating a CUDA context (nvidia-smi); the
+    reference arm builds the same tau-admission programs as the GPU arm."""
+    try:
+        r = subprocess.run(["nvidia-smi", "--query-gpu=memory.total", "--format=csv,noheader,nounits", "-i", "0"],
+                           capture_output=True, text=True, timeout=30)
+        return int(float(r.stdout.strip().splitlines()[0])) << 20
+    except Exception:
+        return 183359 << 20  # B200
+
+
+def cpu_path_sample(args, mc, N, g, seq, steps, warmup, capacity):
+    """The C++ CPU executor (oracle/cpu_executor.cpp) on this host's cores: every
+    event of the reference-built program of the bench workload, at full size, all
+    N*g simulated ranks (one std::thread each), host DRAM; compute events are a
+    synthetic elementwise gradient (no model GEMMs - the reference has none)."""
+    import psutil
+    from oracle.cpu_step import host_bytes_needed, path_executor
+    need = host_bytes_needed(args.preset, N, g)
+    avail = psutil.virtual_memory().available
+    if need > 0.85 * avail:
+        return None, f"needs {need / 1e9:.1f} GB of host memory, {avail / 1e9:.1f} GB available"
+    tau = args.tau if args.strategy in ("fcdp", "fcdp-comm") else 0.0
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    ex = path_executor(args.preset, N, g, args.strategy, tau, capacity if tau > 0 else 0, args.batch, seq,
+                       threads=threads)
+    setup_s = time.perf_counter() - t0
+    for _ in range(max(0, warmup)):
+        ex.step()
+    secs, st = [], None
+    for _ in range(max(1, steps)):
+        st = ex.step()
+        secs.append(st["seconds"])
+    ex.close()
+    tokens = N * g * args.batch * seq
+    total = sum(secs)
+    return {"value": tokens * len(secs) / total, "ms_per_step": 1e3 * total / len(secs), "steps": len(secs),
+            "warmup": warmup, "threads": threads, "threads_per_rank": max(1, threads // (N * g)),
+            "setup_s": setup_s, "host_bytes": need, "bytes_moved_per_step": st["bytes_moved"],
+            "host_GBps": st["bytes_moved"] / (total / len(secs)) / 1e9,
+            "nic_bytes_per_node_per_step": st["nic_tx_fwd_ag"] + st["nic_tx_bwd_ag"] + st["nic_tx_rs"],
+            "sample": (f"full step of the path, every one of the {st['events']} events of the reference-built "
+                       f"{args.strategy} program ({mc.name}, all {len(mc.layer_defs())} layers, full size, "
+                       f"{N}x{g} simulated ranks = {N * g} rank threads, {threads} host threads), host DRAM; "
+                       f"compute events = synthetic elementwise gradient, no model GEMMs (the reference has "
+                       f"no model compute; leaving it out only speeds the CPU up)")}, None
+
+
 def run_reference(args, world_n):
-    """--impl reference: the oracle port of the path on the host cores (rank 0)."""
+    """--impl reference: the C++ CPU reference of the path on the host cores
+    (rank 0 only; the other ranks exit without work)."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    from oracle.cpu_step import cpu_step_sample
     from paper_2602_06499_b200.driving_model import PRESETS
     mc = PRESETS[args.preset]
     seq = args.seq or mc.seq
     N, g = TOPOLOGY.get(world_n, (1, world_n))
-    vals = []
-    t0 = time.time()
-    r = None
-    warm = 0
-    for _ in range(max(0, args.warmup)):  # untimed warm-up samples (page cache, allocator), capped at 60 s
-        cpu_step_sample(args.preset, batch=args.batch, seq=seq, repeats=1)
-        warm += 1
-        if time.time() - t0 > 60:
-            break
-    t0 = time.time()
-    for _ in range(max(1, args.steps)):
-        r = cpu_step_sample(args.preset, batch=args.batch, seq=seq, repeats=1)
-        vals.append(r["tokens_per_s_per_gpu"])
-        if time.time() - t0 > 240:
-            break
-    value = statistics.median(vals) * 1.0  # the whole job's work runs on the same host cores
+    if args.topology:
+        N, g = (int(x) for x in args.topology.lower().split("x"))
+    if args.batch <= 0:
+        args.batch = 8
+    res, why = cpu_path_sample(args, mc, N, g, seq, args.steps, args.warmup, gpu_capacity_bytes_smi())
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": why}), flush=True)
+        return
+    value = res["value"]
+    cpu = {"value": value, "unit": "tokens/s", "cores": res["threads"], "kind": "port", "sample": res["sample"],
+           "executor": "oracle/cpu_executor.cpp (C++; reference control plane oracle/_ref/libshardsim_ref.a)",
+           "host_GBps": res["host_GBps"], "bytes_moved_per_step": res["bytes_moved_per_step"],
+           "setup_s": res["setup_s"], "control_plane": control_plane_timing(mc, args.strategy, N, g)}
+    try:
+        from oracle.cpu_step import c1_tiny_timing
+        cpu["c1_tiny"] = c1_tiny_timing()
+    except Exception as e:  # noqa: BLE001 - a side measurement, never fatal
+        cpu["c1_tiny"] = {"error": str(e)[:200]}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world_n,
-            "steps": len(vals), "warmup": warm, "ms_per_step": 1e3 * args.batch * seq / value,
+            "steps": res["steps"], "warmup": res["warmup"], "ms_per_step": res["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16" if mc.dtype_bytes == 2 else "fp32", "data": "synthetic",
-            "config": workload_config(args, mc, N, g, world_n, seq),
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-                             "sample": r["sample"], "control_plane": control_plane_timing(mc, args.strategy, N, g)},
+            "config": workload_config(args, mc, N, g, world_n, seq), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -479,10 +528,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle.cpu_step import cpu_step_sample
-        r = cpu_step_sample(args.preset, batch=args.batch, seq=seq, repeats=2)
-        cpu = {"value": r["tokens_per_s_per_gpu"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
-               "sample": r["sample"], "control_plane": control_plane_timing(mc, args.strategy, N, g)}
+        # bounded: 1 warm-up + 3 timed full steps of the path on the C++ CPU executor
+        r, why = cpu_path_sample(args, mc, N, g, seq, 3, 1, capacity)
+        if r is None:
+            cpu = {"value": None, "unit": "tokens/s", "unavailable": why}
+        else:
+            cpu = {"value": r["value"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+                   "sample": r["sample"], "ms_per_step": r["ms_per_step"], "host_GBps": r["host_GBps"],
+                   "control_plane": control_plane_timing(mc, args.strategy, N, g)}
 
     if rank != 0:
         if world > 1:

@@ -85,11 +85,12 @@ void fo_unpartition(int64_t chunks, const uint8_t* mask, const void* t, const vo
   }
 }
 
-void fo_expand(const fo_geom* g, const uint8_t* mask, const void* const* t_slices,
-               const void* const* f_slices, void* natural, int32_t param_set) {
+void fo_expand_part(const fo_geom* g, const uint8_t* mask, const void* const* t_slices,
+                    const void* const* f_slices, void* natural, int32_t param_set, int64_t c_lo, int64_t c_hi,
+                    int64_t kt_lo) {
   uint8_t* out = (uint8_t*)natural;
-  int64_t kt = 0, kf = 0;
-  for (int64_t c = 0; c < g->chunks; ++c) {
+  int64_t kt = kt_lo, kf = c_lo - kt_lo;
+  for (int64_t c = c_lo; c < c_hi; ++c) {
     const int tr = mask == NULL || mask[c];
     const int64_t k = tr ? kt++ : kf++;
     if (tr ? param_set == 2 : param_set == 1) continue;
@@ -100,15 +101,21 @@ void fo_expand(const fo_geom* g, const uint8_t* mask, const void* const* t_slice
   }
 }
 
-void fo_rs_slice(const fo_geom* g, const uint8_t* mask, int32_t elem_bytes, const void* const* grads,
-                 int32_t j, int32_t n, float scale, int32_t final_scale, float* own_out, void* wire_out) {
+void fo_expand(const fo_geom* g, const uint8_t* mask, const void* const* t_slices,
+               const void* const* f_slices, void* natural, int32_t param_set) {
+  fo_expand_part(g, mask, t_slices, f_slices, natural, param_set, 0, g->chunks, 0);
+}
+
+void fo_rs_slice_part(const fo_geom* g, const uint8_t* mask, int32_t elem_bytes, const void* const* grads,
+                      int32_t j, int32_t n, float scale, int32_t final_scale, float* own_out, void* wire_out,
+                      int64_t c_lo, int64_t c_hi, int64_t kt_lo) {
   const int32_t V = kChunk / elem_bytes;
   const int64_t k0 = (int64_t)j * g->slice_t;
   int64_t k1 = k0 + g->slice_t;
   if (k1 > g->pt) k1 = g->pt;
   const int64_t own_lo = (int64_t)n * g->shard_t, own_hi = own_lo + g->shard_t;
-  int64_t kt = 0;
-  for (int64_t c = 0; c < g->chunks; ++c) {
+  int64_t kt = kt_lo;
+  for (int64_t c = c_lo; c < c_hi; ++c) {
     if (!(mask == NULL || mask[c])) continue;
     const int64_t k = kt++;
     if (k < k0 || k >= k1) continue;
@@ -122,6 +129,11 @@ void fo_rs_slice(const fo_geom* g, const uint8_t* mask, int32_t elem_bytes, cons
         store_elem(wire_out, rel * V + e, elem_bytes, acc);
     }
   }
+}
+
+void fo_rs_slice(const fo_geom* g, const uint8_t* mask, int32_t elem_bytes, const void* const* grads,
+                 int32_t j, int32_t n, float scale, int32_t final_scale, float* own_out, void* wire_out) {
+  fo_rs_slice_part(g, mask, elem_bytes, grads, j, n, scale, final_scale, own_out, wire_out, 0, g->chunks, 0);
 }
 
 void fo_rs_finalize(int64_t n_elems, int32_t nodes, int32_t node, int32_t elem_bytes, const float* own,

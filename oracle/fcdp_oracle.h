@@ -55,12 +55,22 @@ void fo_unpartition(int64_t chunks, const uint8_t* mask, const void* t, const vo
 void fo_expand(const fo_geom* g, const uint8_t* mask, const void* const* t_slices,
                const void* const* f_slices, void* natural, int32_t param_set);
 
+/* The same over natural chunks [c_lo, c_hi) only; kt_lo = trainable chunks
+ * before c_lo (so a layer can be split across threads: results are identical). */
+void fo_expand_part(const fo_geom* g, const uint8_t* mask, const void* const* t_slices,
+                    const void* const* f_slices, void* natural, int32_t param_set, int64_t c_lo, int64_t c_hi,
+                    int64_t kt_lo);
+
 /* Hierarchical reduce-scatter, intra step, for slice j on node n:
  * sum over the g natural gradient buffers in order 0..g-1 in fp32.  Own shard
  * chunks -> own_out (fp32, times scale iff final_scale); other shards ->
  * wire_out (slice-relative, parameter dtype, RNE). */
 void fo_rs_slice(const fo_geom* g, const uint8_t* mask, int32_t elem_bytes, const void* const* grads,
                  int32_t j, int32_t n, float scale, int32_t final_scale, float* own_out, void* wire_out);
+
+void fo_rs_slice_part(const fo_geom* g, const uint8_t* mask, int32_t elem_bytes, const void* const* grads,
+                      int32_t j, int32_t n, float scale, int32_t final_scale, float* own_out, void* wire_out,
+                      int64_t c_lo, int64_t c_hi, int64_t kt_lo);
 
 /* Inter step epilogue: out[i] = scale * sum_{m=0..N-1} part_m[i]. */
 void fo_rs_finalize(int64_t n_elems, int32_t nodes, int32_t node, int32_t elem_bytes, const float* own,

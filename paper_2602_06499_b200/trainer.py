@@ -37,18 +37,8 @@ class FcdpTrainer:
         self.batch, self.seq = batch_per_gpu, seq_len or cfg.seq
         self.dtype = torch.bfloat16 if cfg.dtype_bytes == 2 else torch.float32
         self.defs: List[LayerDef] = cfg.layer_defs()
-        # activation bytes per sample feed the tau-admission projection
-        # (schedule.cpp:196-208); a bf16 transformer block with flash attention
-        # keeps about 34 * seq * hidden bytes, the head its logits (+ fp32 copy).
-        ffn = cfg.ffn or 4 * cfg.hidden
-
-        def act(d: LayerDef) -> int:
-            if d.kind == "head":
-                return self.seq * cfg.vocab_rows * 6
-            if d.kind == "embed":
-                return self.seq * cfg.hidden * 2
-            return int(self.seq * cfg.hidden * 34 * max(1.0, ffn / (4 * cfg.hidden)))
-        layers = [S.LayerSpec(i, d.numel, d.trainable_params() / d.numel, activation_bytes_per_sample=act(d))
+        layers = [S.LayerSpec(i, d.numel, d.trainable_params() / d.numel,
+                              activation_bytes_per_sample=activation_bytes(cfg, d, self.seq))
                   for i, d in enumerate(self.defs)]
         self.model = S.ModelSpec(layers, cfg.dtype_bytes, batch_per_gpu=batch_per_gpu)
         self.gpu_capacity_bytes = gpu_capacity_bytes
@@ -159,6 +149,19 @@ class FcdpTrainer:
                 if layer == 0:
                     self._grad_act = None
                     self._saved_out = None
+
+
+def activation_bytes(cfg: ModelConfig, d: LayerDef, seq: int) -> int:
+    """Activation bytes per sample of one layer, fed to the tau-admission
+    projection (reference schedule.cpp:196-208): a bf16 transformer block with
+    flash attention keeps about 34 * seq * hidden bytes, the head its logits
+    (+ an fp32 copy)."""
+    ffn = cfg.ffn or 4 * cfg.hidden
+    if d.kind == "head":
+        return seq * cfg.vocab_rows * 6
+    if d.kind == "embed":
+        return seq * cfg.hidden * 2
+    return int(seq * cfg.hidden * 34 * max(1.0, ffn / (4 * cfg.hidden)))
 
 
 def synthetic_batch(vocab: int, batch: int, seq: int, seed: int, step: int, rank: int,

@@ -1,7 +1,22 @@
 """End-to-end training parity: FCDP / ZeRO-3 / FCDP-Comm on the B200 engine vs a
 plain single-process torch fp32 CPU reference of the same model, same
-synthetic inputs and seeds.  Tolerances (stated per north_star): fp32 model
-rel 1e-4 on loss and params; bf16 model 2e-2 on loss."""
+synthetic inputs and seeds: loss, the reduced fp32 gradient and the updated
+fp32 master weights after every step, per layer (trainable portion, gathered
+from all ranks' shards in global shard order r = j*N + n).
+
+Tolerances (north_star's "stated fp32 tolerance"), per
+layer and step, err = |engine - reference|:
+  fp32 model (C1 tiny):  loss rel 1e-4;  grad max err <= 1e-4 * max|grad_ref|;
+                         master: 99.9% of elements within 1e-6 + 1e-4*|w_ref|,
+                         and every element within 2*lr*step (AdamW moves an element
+                         by at most ~lr per step, so a near-zero gradient whose sign
+                         differs between two fp32 summation orders can move it
+                         the other way - bounded, and rare).
+  bf16 models:           loss rel 2e-2;  grad ||err||_2 <= 5e-2 * ||grad_ref||_2;
+                         master update (w - w0): ||err||_2 <= 0.25 * ||dw_ref||_2.
+The bf16 tolerances also cover the inter-node RS wire: at N > 1 the node's
+partial sums cross the NIC in bf16 (costmodel.cpp:86-88 books the bytes in the
+parameter dtype); the N = 2 case reports its error beside the N = 1 case."""
 import json
 import pickle
 import subprocess
@@ -12,6 +27,8 @@ from pathlib import Path
 import numpy as np
 import pytest
 
+from tests.model_reference import compare, cpu_reference
+
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
@@ -19,8 +36,8 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def run(tmp_path, preset, strategy, N=1, g=1, steps=3, batch=2, lr=1e-3, wd=0.01, seed=0x5EED):
     world = N * g
-    if world > (torch.cuda.device_count() if torch.cuda.is_available() else 0):
-        pytest.skip(f"needs {world} GPUs")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")  # ranks share GPUs round-robin (rank % device_count)
     cfg = dict(preset=preset, strategy=strategy, N=N, g=g, steps=steps, batch=batch, lr=lr, wd=wd, seed=seed,
                shm=f"fcdp_tr_{uuid.uuid4().hex[:10]}", out=str(tmp_path))
     procs = [subprocess.Popen([sys.executable, str(ROOT / "tests/trainer_worker.py"), json.dumps(dict(cfg, rank=r))],
@@ -31,79 +48,37 @@ def run(tmp_path, preset, strategy, N=1, g=1, steps=3, batch=2, lr=1e-3, wd=0.01
     return cfg, [pickle.load(open(tmp_path / f"rank{r}.pkl", "rb")) for r in range(world)]
 
 
-def cpu_reference(cfg):
-    """Single-process fp32 torch training of the same model on the CPU."""
-    from oracle import oracle as O
-    from paper_2602_06499_b200.driving_model import PRESETS, layer_forward
-    from paper_2602_06499_b200.trainer import synthetic_batch
-    mc = PRESETS[cfg["preset"]]
-    defs = mc.layer_defs()
-    eb = mc.dtype_bytes
-    flats = []
-    for l, d in enumerate(defs):
-        nat = O.init_natural(d.numel, eb, cfg["seed"], l, d.init_ranges())
-        w = O.bf16_to_f32(nat) if eb == 2 else nat.astype(np.float32)
-        flats.append(torch.from_numpy(w.copy()))
-    params = []
-    for l, d in enumerate(defs):
-        p = {}
-        for t in d.tensors:
-            v = flats[l][d.offsets[t.name]:d.offsets[t.name] + t.numel].view(t.shape).clone()
-            v.requires_grad_(t.trainable)
-            p[t.name] = v
-        params.append(p)
-    opt_state = {}
-    world = cfg["N"] * cfg["g"]
-    losses = []
-    b1, b2, eps, lr, wd = 0.9, 0.95, 1e-8, cfg["lr"], cfg["wd"]
-    for step in range(1, cfg["steps"] + 1):
-        total = 0.0
-        for r in range(world):
-            x, y = synthetic_batch(mc.vocab, cfg["batch"], mc.seq, cfg["seed"], step, r)
-            h = None
-            for l, d in enumerate(defs):
-                h = layer_forward(mc, d, params[l], h, x, y)
-            (h / world).backward()
-            total += float(h)
-        losses.append(total / world)
-        with torch.no_grad():
-            for l, d in enumerate(defs):
-                for t in d.tensors:
-                    if not t.trainable:
-                        continue
-                    w = params[l][t.name]
-                    m, v = opt_state.setdefault((l, t.name), (torch.zeros_like(w), torch.zeros_like(w)))
-                    gr = w.grad
-                    m.mul_(b1).add_((1 - b1) * gr)
-                    v.mul_(b2).add_((1 - b2) * gr * gr)
-                    mh = m / (1 - b1 ** step)
-                    vh = v / (1 - b2 ** step)
-                    w.sub_(lr * (mh / (vh.sqrt() + eps) + wd * w))
-                    w.grad = None
-    return losses
+def _losses(res):
+    return np.mean([r["losses"] for r in res], axis=0)  # each rank reports its local mean
 
 
 @pytest.mark.parametrize("strategy", ["fcdp", "zero3"])
 def test_tiny_fp32_parity(tmp_path, built, strategy):
     cfg, res = run(tmp_path, "tiny", strategy)
     ref = cpu_reference(cfg)
-    np.testing.assert_allclose(res[0]["losses"], ref, rtol=1e-4)
+    np.testing.assert_allclose(_losses(res), ref["losses"], rtol=1e-4)
+    compare(cfg, res, ref, fp32=True)
 
 
-def test_tiny_fp32_two_ranks(tmp_path, built):
-    cfg, res = run(tmp_path, "tiny", "fcdp", N=2, g=1)
+@pytest.mark.parametrize("N,g,strategy", [(2, 1, "fcdp"), (1, 2, "fcdp"), (2, 2, "zero3"), (2, 2, "fcdp")])
+def test_tiny_fp32_multi_rank(tmp_path, built, N, g, strategy):
+    cfg, res = run(tmp_path, "tiny", strategy, N=N, g=g)
     ref = cpu_reference(cfg)
-    mean = np.mean([r["losses"] for r in res], axis=0)  # each rank reports its local mean
-    np.testing.assert_allclose(mean, ref, rtol=1e-4)
+    np.testing.assert_allclose(_losses(res), ref["losses"], rtol=1e-4)
+    compare(cfg, res, ref, fp32=True)
 
 
-def test_gpt2_bf16(tmp_path, built):
-    cfg, res = run(tmp_path, "gpt2-small-test", "fcdp")
+@pytest.mark.parametrize("N", [1, 2])
+def test_gpt2_bf16(tmp_path, built, N):
+    cfg, res = run(tmp_path, "gpt2-small-test", "fcdp", N=N)
     ref = cpu_reference(cfg)
-    np.testing.assert_allclose(res[0]["losses"], ref, rtol=2e-2)
+    np.testing.assert_allclose(_losses(res), ref["losses"], rtol=2e-2)
+    compare(cfg, res, ref, fp32=False)
 
 
-def test_llama_lora_fcdp_comm(tmp_path, built):
-    cfg, res = run(tmp_path, "llama-lora-test", "fcdp-comm", steps=4)
+@pytest.mark.parametrize("N,g", [(1, 1), (2, 2)])
+def test_llama_lora_fcdp_comm(tmp_path, built, N, g):
+    cfg, res = run(tmp_path, "llama-lora-test", "fcdp-comm", N=N, g=g, steps=4)
     ref = cpu_reference(cfg)
-    np.testing.assert_allclose(res[0]["losses"], ref, rtol=2e-2)
+    np.testing.assert_allclose(_losses(res), ref["losses"], rtol=2e-2)
+    compare(cfg, res, ref, fp32=False)

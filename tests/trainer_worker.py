@@ -25,19 +25,24 @@ def main():
     t = FcdpTrainer(mc, topo, plan, rank=rank, world_size=N * g, device=dev, shm_name=cfg["shm"],
                     batch_per_gpu=cfg["batch"], seed=cfg["seed"], nic_pacing=False, lr=cfg["lr"],
                     weight_decay=cfg["wd"])
-    losses = []
+    from oracle import oracle as O
+    V = 16 // mc.dtype_bytes
+    geos = [O.geom(d.numel * mc.dtype_bytes // 16, d.chunk_mask(mc.dtype_bytes), N, g) for d in t.defs]
+    losses, grads, masters = [], [], []
     for step in range(1, cfg["steps"] + 1):
         x, y = synthetic_batch(mc.vocab, cfg["batch"], mc.seq, cfg["seed"], step, rank, device=t.device)
         loss = t.step(x, y)
         t.sync()
         losses.append(float(loss.item()))
+        # this rank's fp32 shard of the reduced gradient of this step and of the
+        # updated master weights (global shard j*N + n of each trainable portion)
+        grads.append({l: t.engine.read_grad(l, geo.shard_t * V) for l, geo in enumerate(geos) if geo.pt})
+        masters.append({l: t.engine.read_master(l, geo.shard_t * V) for l, geo in enumerate(geos) if geo.pt})
     shards = {}
-    for l, d in enumerate(t.defs):
-        from oracle import oracle as O
-        geo = O.geom(d.numel * mc.dtype_bytes // 16, d.chunk_mask(mc.dtype_bytes), N, g)
+    for l, geo in enumerate(geos):
         shards[l] = (t.engine.read_shard(l, False, geo.shard_t * 16), t.engine.read_shard(l, True, geo.shard_f * 16))
     with open(os.path.join(cfg["out"], f"rank{rank}.pkl"), "wb") as f:
-        pickle.dump({"losses": losses, "shards": shards}, f)
+        pickle.dump({"losses": losses, "shards": shards, "grads": grads, "masters": masters}, f)
     t.engine.barrier()
     t.close()
 
