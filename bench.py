@@ -162,7 +162,7 @@ def control_plane_timing(mc, strategy: str, N: int, g: int, iters: int = 1000):
     return out or None
 
 
-def isolated_rate(kernel_class: str, alg_bytes: float, eb: int, dev):
+def isolated_rate(kernel_class: str, alg_bytes: float, eb: int, dev, fused_adam: bool = False):
     """The dominant kernel re-timed alone (after the timed region) at the live
     per-launch size: stateless C-ABI launch on synthetic buffers, L2 flushed
     between reps, CUDA events, median.  The live number in `roofline` includes
@@ -184,7 +184,19 @@ def isolated_rate(kernel_class: str, alg_bytes: float, eb: int, dev):
         return out
 
     V = 16 // eb
-    if kernel_class == "adamw":
+    if kernel_class == "adamw" and fused_adam:
+        # G = 1: the fused RS + AdamW reading the bf16 gradient in place (24 + 2*eb B/param)
+        n = int(alg_bytes // (6 * 4 + 2 * eb)) // (16 // eb) * (16 // eb)
+        w, m_, v_ = torch.randn(n, device=dev), torch.zeros(n, device=dev), torch.zeros(n, device=dev)
+        g_ = torch.randn(n, device=dev).mul_(1e-3).to(torch.bfloat16 if eb == 2 else torch.float32)
+        par = torch.empty(n * eb, dtype=torch.uint8, device=dev)
+        cfg = _capi.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0, 1)
+        offs, cnts = (C.c_int64 * 1)(0), (C.c_int64 * 1)(n)
+        ptrs = (C.c_void_p * 1)(g_.data_ptr())
+        keep += [w, m_, v_, g_, par]
+        fn = lambda: _capi.check(lib.fcdp_adam_grad_step(n, C.byref(cfg), 1.0, 1, offs, ptrs, cnts, P(w), P(m_),
+                                                         P(v_), P(par), eb, None, None))
+    elif kernel_class == "adamw":
         n = int(alg_bytes // (7 * 4 + eb)) // 4 * 4
         # real-valued inputs: an all-zero gradient sends the IEEE divisions down their slow path
         w, g_ = torch.randn(n, device=dev), torch.randn(n, device=dev).mul_(1e-3)
@@ -578,7 +590,7 @@ def main():
         # a few MB per launch (PEFT trainable slices): launch latency, not bandwidth, bounds it
         roofline["note"] = f"{per_launch_bytes / 1e6:.1f} MB per launch: launch-latency regime"
     if roofline["bound"] == "hbm":
-        iso = isolated_rate(dom, per_launch_bytes, mc.dtype_bytes, dev)
+        iso = isolated_rate(dom, per_launch_bytes, mc.dtype_bytes, dev, fused_adam=(world == 1))
         if iso:
             iso["frac"] = iso["achieved"] / peak if peak else None
             roofline["isolated"] = iso

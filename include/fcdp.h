@@ -174,6 +174,14 @@ int fcdp_program_layer_flags(const fcdp_program* program, uint8_t* out, int32_t 
 /* serialize_program (schedule.hpp:83-85); *len receives the full length (incl. when truncated) */
 int fcdp_program_serialize(const fcdp_program* program, char* buf, size_t capacity, size_t* len);
 void fcdp_program_destroy(fcdp_program* program);
+/* A program from an explicit event list (an external scheduler's program, or a
+ * mutated one for the SPEC.md:389-409 mutation harness).  Event i must have
+ * id i; deps of event i are deps[dep_offsets[i] .. dep_offsets[i+1]); flags as
+ * fcdp_program_layer_flags.  The engine checks what it executes (freshness,
+ * zero backward AgInter for the FCDP family) and answers FCDP_ERR_PROTOCOL. */
+int fcdp_program_create(uint64_t iteration_index, int32_t strategy, uint32_t num_events,
+                        const fcdp_event* events, const uint32_t* dep_offsets, const uint32_t* deps,
+                        int32_t num_layers, const uint8_t* layer_flags, fcdp_program** out);
 
 /* ============================================================== data plane
  * Layer layout.  A layer is a flat natural-order buffer of E elements of
@@ -231,6 +239,15 @@ typedef struct fcdp_adam_config {
 } fcdp_adam_config;
 int fcdp_adam_step(int64_t n, const fcdp_adam_config* cfg, float* master, float* m, float* v,
                    const float* grad, void* param, int32_t param_elem_bytes, void* stream);
+/* G = 1 fused reduce-scatter + AdamW of a dense layer (the engine's path at one
+ * GPU): the gradient in the parameter dtype from segments (element offset,
+ * pointer, count; 16-byte aligned; uncovered elements have gradient 0),
+ * g = (0 + x) * scale, then AdamW - bit-identical to fcdp_rs_slice (g = 1,
+ * final scale) followed by fcdp_adam_step.  keep_grad (nullable) receives g. */
+int fcdp_adam_grad_step(int64_t n, const fcdp_adam_config* cfg, float scale, int32_t num_segs,
+                        const int64_t* elem_offsets, const void* const* grads, const int64_t* counts,
+                        float* master, float* m, float* v, void* param, int32_t param_elem_bytes,
+                        float* keep_grad, void* stream);
 
 /* Init spec: element ranges of the natural layer with a rule each.
  * kind 0: uniform(-scale, scale) from splitmix64(seed, layer, element)
@@ -298,6 +315,14 @@ int fcdp_engine_set_compute(fcdp_engine* e, fcdp_compute_fn fn, void* user);
  * event semantics executed here are Algorithm 1 and the
  * builder's event meanings (schedule.cpp:107-292). */
 int fcdp_engine_run(fcdp_engine* e, const fcdp_program* program, fcdp_states* states);
+/* Errors and engine state: an error while a program runs (a protocol violation,
+ * a failed compute callback, an OOM, a cross-rank timeout) leaves this rank's
+ * cross-rank sequence counters out of step with its peers.  The engine latches
+ * the failure, raises the job's abort flag (peers waiting on this rank fail
+ * fast with FCDP_ERR_TIMEOUT instead of reading stale data), and refuses every
+ * later begin/run with FCDP_ERR_PROTOCOL: destroy and recreate it.  Every rank
+ * must run the same program: begin compares a hash of the program with every
+ * peer's and answers FCDP_ERR_CONFIG on a mismatch. */
 /* The same, driven event by event by an external executor that walks
  * EventProgram.events in id order (SURVEY §8(b) caller): begin, then exec for
  * ids 0..n-1, then end (which applies step_state).  Each exec enqueues that
@@ -343,6 +368,25 @@ typedef struct fcdp_kernel_stats {
   uint64_t link_bytes[FCDP_KCLASSES];
 } fcdp_kernel_stats;
 int fcdp_engine_set_timing(fcdp_engine* e, int32_t on);
+
+/* One GPU (G = 1), dense trainable layer: the gradient reduce-scatter is the
+ * identity up to its fp32 widen and 1/G scale, so the engine fuses it into
+ * AdamW (cast/scale + update in one pass over the layer, per layer, right after
+ * its backward).  The fused kernel can read the gradient straight from the
+ * caller's own buffers: inside the backward compute callback of `layer`, call
+ * fcdp_engine_grad_segments with up to 24 sorted, disjoint, 16-byte aligned
+ * (offset, pointer, count) segments in the parameter dtype - elements no
+ * segment covers have gradient 0 - instead of writing grad_out.  The buffers
+ * must stay valid, and unwritten by work not ordered after the program's end
+ * on the compute stream, until fcdp_engine_run / fcdp_engine_end returns.
+ * takes_grad_segments answers whether `layer` qualifies (only inside a program;
+ * otherwise FCDP_ERR_CONFIG from grad_segments: fill grad_out).
+ * set_keep_grad(1): the fused path also writes the fp32 gradient shard (what
+ * fcdp_engine_read_grad returns; tests), at 4 more bytes per parameter. */
+int fcdp_engine_grad_segments(fcdp_engine* e, int32_t layer, int32_t n, const int64_t* elem_offsets,
+                              const void* const* ptrs, const int64_t* counts);
+int fcdp_engine_takes_grad_segments(fcdp_engine* e, int32_t layer, int32_t* out);
+int fcdp_engine_set_keep_grad(fcdp_engine* e, int32_t on);
 int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t reset);
 
 /* Executed-event trace of the last fcdp_engine_run (when tracing is on): for

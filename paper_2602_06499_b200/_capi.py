@@ -137,6 +137,8 @@ SIGNATURES = {
     "fcdp_program_num_events": (C.c_int, [P, C.POINTER(u32)]),
     "fcdp_program_event": (C.c_int, [P, u32, C.POINTER(EventC), C.POINTER(u32), u32]),
     "fcdp_program_layer_flags": (C.c_int, [P, C.POINTER(C.c_uint8), i32]),
+    "fcdp_program_create": (C.c_int, [C.c_uint64, i32, u32, C.POINTER(EventC), C.POINTER(u32), C.POINTER(u32), i32,
+                                      C.POINTER(C.c_uint8), C.POINTER(P)]),
     "fcdp_program_serialize": (C.c_int, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "fcdp_program_destroy": (None, [P]),
     "fcdp_layout_create": (C.c_int, [i64, C.POINTER(C.c_uint8), i32, i32, i32, PP]),
@@ -147,6 +149,8 @@ SIGNATURES = {
     "fcdp_rs_slice": (C.c_int, [P, PP, i32, i32, f32, i32, P, P, P]),
     "fcdp_rs_finalize": (C.c_int, [i64, i32, i32, i32, P, P, i64, f32, P, P]),
     "fcdp_adam_step": (C.c_int, [i64, C.POINTER(AdamConfig), P, P, P, P, P, i32, P]),
+    "fcdp_adam_grad_step": (C.c_int, [i64, C.POINTER(AdamConfig), C.c_float, i32, C.POINTER(C.c_int64), C.POINTER(P),
+                                      C.POINTER(C.c_int64), P, P, P, P, i32, P, P]),
     "fcdp_init_natural": (C.c_int, [P, u64, i32, C.POINTER(InitRange), i32, P, P]),
     "fcdp_engine_create": (C.c_int, [C.POINTER(EngineConfig), P, C.POINTER(Topology), C.POINTER(Plan),
                                      C.POINTER(C.POINTER(C.c_uint8)), PP]),
@@ -169,6 +173,9 @@ SIGNATURES = {
     "fcdp_engine_read_host_cache": (C.c_int, [P, i32, i32, P, C.c_size_t]),
     "fcdp_engine_destroy": (None, [P]),
     "fcdp_engine_set_timing": (C.c_int, [P, i32]),
+    "fcdp_engine_grad_segments": (C.c_int, [P, i32, i32, C.POINTER(C.c_int64), C.POINTER(P), C.POINTER(C.c_int64)]),
+    "fcdp_engine_takes_grad_segments": (C.c_int, [P, i32, C.POINTER(i32)]),
+    "fcdp_engine_set_keep_grad": (C.c_int, [P, i32]),
     "fcdp_engine_kernel_stats": (C.c_int, [P, C.POINTER(KernelStats), i32]),
     "fcdp_engine_set_trace": (C.c_int, [P, i32]),
     "fcdp_engine_trace": (C.c_int, [P, C.POINTER(f32), C.POINTER(f32), u32, C.POINTER(u32)]),

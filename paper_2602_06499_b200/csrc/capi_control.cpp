@@ -279,6 +279,42 @@ int fcdp_program_event(const fcdp_program* p, uint32_t i, fcdp_event* out, uint3
   });
 }
 
+int fcdp_program_create(uint64_t it, int32_t strategy, uint32_t n, const fcdp_event* ev, const uint32_t* off,
+                        const uint32_t* deps, int32_t num_layers, const uint8_t* flags, fcdp_program** out) {
+  return guarded([&] {
+    if (strategy < 0 || strategy > static_cast<int32_t>(shardsim::StrategyKind::FcdpComm) || num_layers < 0)
+      throw shardsim::ConfigError("program_create: bad strategy or layer count");
+    shardsim::EventProgram p;
+    p.iteration_index = it;
+    p.strategy = static_cast<shardsim::StrategyKind>(strategy);
+    for (uint32_t i = 0; i < n; ++i) {
+      if (ev[i].id != i) throw shardsim::ConfigError("program_create: event ids must be 0..n-1 in order");
+      if (ev[i].kind < 0 || ev[i].kind > static_cast<int32_t>(shardsim::EventKind::Broadcast) ||
+          ev[i].param_set < 0 || ev[i].param_set > static_cast<int32_t>(shardsim::ParamSet::FrozenOnly) ||
+          ev[i].layer >= num_layers)
+        throw shardsim::ConfigError("program_create: event " + std::to_string(i) + " is malformed");
+      shardsim::Event e;
+      e.id = i;
+      e.kind = static_cast<shardsim::EventKind>(ev[i].kind);
+      e.layer = ev[i].layer;
+      e.param_set = static_cast<shardsim::ParamSet>(ev[i].param_set);
+      e.bytes_total = ev[i].bytes_total;
+      for (uint32_t k = off[i]; k < off[i + 1]; ++k) {
+        if (deps[k] >= i) throw shardsim::ConfigError("program_create: deps must point to earlier events");
+        e.deps.push_back(deps[k]);
+      }
+      p.events.push_back(std::move(e));
+    }
+    for (int32_t l = 0; l < num_layers; ++l) {
+      const uint8_t f = flags ? flags[l] : 0;
+      p.layer_retained.push_back((f & 1) ? 1 : 0);
+      p.layer_clean_path.push_back((f & 2) ? 1 : 0);
+      p.layer_dirty_path.push_back((f & 4) ? 1 : 0);
+    }
+    *out = new fcdp_program{std::move(p)};
+  });
+}
+
 int fcdp_program_layer_flags(const fcdp_program* p, uint8_t* out, int32_t cap) {
   return guarded([&] {
     const auto& pr = p->prog;

@@ -135,6 +135,32 @@ int fcdp_adam_step(int64_t n, const fcdp_adam_config* c, float* master, float* m
   });
 }
 
+int fcdp_adam_grad_step(int64_t n, const fcdp_adam_config* c, float scale, int32_t num_segs,
+                        const int64_t* elem_offsets, const void* const* grads, const int64_t* counts,
+                        float* master, float* m, float* v, void* param, int32_t eb, float* keep_grad,
+                        void* stream) {
+  return guarded([&] {
+    if (eb != 2 && eb != 4) throw shardsim::ConfigError("adam_grad_step: element bytes must be 2 or 4");
+    const int64_t V = fcdp::kChunkBytes / eb;
+    if (n % V) throw shardsim::ConfigError("adam_grad_step: n must be whole 16-byte chunks");
+    if (num_segs < 0 || num_segs > fcdp::kMaxGradSegs) throw shardsim::ConfigError("adam_grad_step: too many segments");
+    fcdp::GradSegs sg;
+    sg.n = num_segs;
+    for (int i = 0; i < num_segs; ++i) {
+      if (elem_offsets[i] % V || counts[i] % V) throw shardsim::ConfigError("adam_grad_step: unaligned segment");
+      sg.dst_chunk[i] = elem_offsets[i] / V;
+      sg.nchunks[i] = counts[i] / V;
+      sg.src[i] = grads[i];
+    }
+    fcdp::AdamParams p{c->lr, c->beta1, c->beta2, c->eps, c->weight_decay,
+                       static_cast<float>(1.0 - std::pow(static_cast<double>(c->beta1), c->step)),
+                       static_cast<float>(1.0 - std::pow(static_cast<double>(c->beta2), c->step))};
+    check_cuda(fcdp::launch_adam_grad(n / V, sg, p, scale, master, m, v, param, eb, keep_grad,
+                                      static_cast<cudaStream_t>(stream)),
+               "fcdp_adam_grad_step");
+  });
+}
+
 int fcdp_init_natural(const fcdp_layout* L, uint64_t seed, int32_t layer, const fcdp_init_range* r,
                       int32_t nr, void* natural, void* stream) {
   return guarded([&] {

@@ -509,6 +509,63 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(std::int64_t n, AdamPara
   }
 }
 
+// G = 1 (one GPU holds the whole dense layer): the reduce-scatter is the
+// identity up to its fp32 widen + 1/G scale, so it is fused into AdamW, which
+// reads the gradient straight from where backward left it - the engine's
+// natural gradient slot or the autograd buffers themselves (segments) - in the
+// parameter dtype.  Per 16-byte gradient chunk (V elements):
+//   g = (0 + x) * scale      exactly the rs_dense_kernel<T, 1> arithmetic
+//   AdamW(g)                 exactly adam_kernel's arithmetic
+// so results are bit-identical to RS-then-AdamW; the fp32 gradient shard is
+// written only when asked (keep_grad: readback for tests), saving 8 B/param of
+// HBM traffic and the separate RS pass.  Chunks no segment covers have g = 0.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) adam_grad_kernel(std::int64_t chunks, GradSegs segs, AdamParams p,
+                                                             float scale, float* __restrict__ master,
+                                                             float* __restrict__ m, float* __restrict__ v,
+                                                             void* __restrict__ param, float* __restrict__ keep) {
+  constexpr int V = Vec<T>::kN;
+  const float omb1 = __fsub_rn(1.0f, p.beta1), omb2 = __fsub_rn(1.0f, p.beta2);
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t c = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < chunks; c += step) {
+    uint4 q = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 1
+    for (int s = 0; s < segs.n; ++s)
+      if (c >= segs.dst_chunk[s] && c < segs.dst_chunk[s] + segs.nchunks[s]) {
+        q = __ldcs(static_cast<const uint4*>(segs.src[s]) + (c - segs.dst_chunk[s]));
+        break;
+      }
+    float g[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) g[e] = 0.0f;
+    Vec<T>::add(g, q);
+    float4* W4 = reinterpret_cast<float4*>(master) + c * (V / 4);
+    float4* M4 = reinterpret_cast<float4*>(m) + c * (V / 4);
+    float4* V4 = reinterpret_cast<float4*>(v) + c * (V / 4);
+    float4 w[V / 4], mm[V / 4], vv[V / 4];
+#pragma unroll
+    for (int k = 0; k < V / 4; ++k) {
+      w[k] = __ldcs(W4 + k);
+      mm[k] = __ldcs(M4 + k);
+      vv[k] = __ldcs(V4 + k);
+    }
+#pragma unroll
+    for (int k = 0; k < V / 4; ++k) {
+      const float4 gk = make_float4(__fmul_rn(g[4 * k], scale), __fmul_rn(g[4 * k + 1], scale),
+                                    __fmul_rn(g[4 * k + 2], scale), __fmul_rn(g[4 * k + 3], scale));
+      if (keep) __stcs(reinterpret_cast<float4*>(keep) + c * (V / 4) + k, gk);
+      adam_one(p, omb1, omb2, gk.x, w[k].x, mm[k].x, vv[k].x);
+      adam_one(p, omb1, omb2, gk.y, w[k].y, mm[k].y, vv[k].y);
+      adam_one(p, omb1, omb2, gk.z, w[k].z, mm[k].z, vv[k].z);
+      adam_one(p, omb1, omb2, gk.w, w[k].w, mm[k].w, vv[k].w);
+      __stcs(W4 + k, w[k]);
+      __stcs(M4 + k, mm[k]);
+      __stcs(V4 + k, vv[k]);
+      store4<T>(param, c * (V / 4) + k, w[k]);
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kThreads) widen_kernel(std::int64_t n, const void* __restrict__ src,
                                                          float* __restrict__ dst) {
@@ -702,6 +759,21 @@ cudaError_t launch_adam(std::int64_t n, const AdamParams& p, float* master, floa
     adam_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(n, p, master, m, v, grad, param);
   else
     adam_kernel<float><<<grid, kThreads, 0, s>>>(n, p, master, m, v, grad, param);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_adam_grad(std::int64_t chunks, const GradSegs& segs, const AdamParams& p, float scale,
+                             float* master, float* m, float* v, void* param, int param_elem_bytes, float* keep_grad,
+                             cudaStream_t s) {
+  if (chunks <= 0) return cudaSuccess;
+  if (segs.n < 0 || segs.n > kMaxGradSegs) return cudaErrorInvalidValue;
+  for (int i = 0; i < segs.n; ++i)
+    if (reinterpret_cast<std::uintptr_t>(segs.src[i]) % 16) return cudaErrorMisalignedAddress;
+  const int grid = grid_for(chunks, kThreads);
+  if (param_elem_bytes == 2)
+    adam_grad_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(chunks, segs, p, scale, master, m, v, param, keep_grad);
+  else
+    adam_grad_kernel<float><<<grid, kThreads, 0, s>>>(chunks, segs, p, scale, master, m, v, param, keep_grad);
   return cudaGetLastError();
 }
 

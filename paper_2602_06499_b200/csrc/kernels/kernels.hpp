@@ -45,6 +45,21 @@ struct AdamParams {
 cudaError_t launch_adam(std::int64_t n, const AdamParams& p, float* master, float* m, float* v,
                         const float* grad, void* param, int param_elem_bytes, cudaStream_t s);
 
+// G = 1 fused reduce-scatter (widen + scale) + AdamW of a dense trainable layer,
+// reading the gradient in the parameter dtype from up to kMaxGradSegs
+// segments (16-byte aligned; chunk offsets within the layer; chunks no segment
+// covers have gradient 0).  keep_grad (nullable) receives the fp32 gradient.
+inline constexpr int kMaxGradSegs = 24;
+struct GradSegs {
+  int n = 0;
+  std::int64_t dst_chunk[kMaxGradSegs];
+  std::int64_t nchunks[kMaxGradSegs];
+  const void* src[kMaxGradSegs];
+};
+cudaError_t launch_adam_grad(std::int64_t chunks, const GradSegs& segs, const AdamParams& p, float scale,
+                             float* master, float* m, float* v, void* param, int param_elem_bytes, float* keep_grad,
+                             cudaStream_t s);
+
 // Deterministic init of a natural layer; `ranges` is a device array.
 struct InitRange {
   std::int64_t begin, end;

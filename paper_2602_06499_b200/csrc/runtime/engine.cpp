@@ -171,7 +171,11 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   // GPU's socket, and place its pinned host tiers there (multi-socket hosts).
   numa_.num_nodes = numa_online_nodes();
   numa_.gpu_node = numa_node_of_gpu(cfg_.device);
+  // The pin is temporary: it covers the first touch of the host tiers and the
+  // start of the NIC thread (which keeps it); the caller's thread gets its own
+  // affinity back at the end of the constructor.
   const char* numa_env = std::getenv("FCDP_NUMA");
+  const SavedAffinity caller_affinity = numa_save_affinity();
   if (numa_.num_nodes > 1 && numa_.gpu_node >= 0 && !(numa_env && std::strcmp(numa_env, "0") == 0))
     numa_.cpus_bound = numa_pin_thread(numa_.gpu_node);
   build_layouts(chunk_masks);
@@ -206,13 +210,14 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   exchange_handles();
   nic_ = std::make_unique<NicEmulator>(*shm_, rank_, n_, topo_.inter_node.bandwidth_bytes_per_s,
                                        cfg_.nic_pacing != 0);
+  if (numa_.cpus_bound) numa_restore_affinity(caller_affinity);
   shm_->barrier(cfg_.timeout_s);
 }
 
 Engine::~Engine() {
   try {
     sync();
-    if (shm_) shm_->barrier(cfg_.timeout_s);  // no peer still reads our memory
+    if (shm_) shm_->barrier(cfg_.timeout_s, false);  // no peer still reads our memory (even after an abort)
   } catch (...) {
   }
   nic_.reset();
@@ -398,6 +403,8 @@ void Engine::allocate() {
   ag_staged_valid_.assign(L, 0);
   stepped_.assign(L, 0);
   prev_retained_.assign(L, 0);
+  grad_segs_.assign(L, GradSegs{});
+  grad_segs_set_.assign(L, 0);
 }
 
 void Engine::exchange_handles() {
@@ -724,6 +731,13 @@ void Engine::fence_alias_reads(cudaStream_t s) {
 }
 
 void Engine::ev_ag_inter(const Event& e, bool backward) {
+  // FCDP's backward reconstructs from the host cache + intra-node gather and
+  // issues no inter-node all-gather; ZeRO++
+  // gathers from its GPU replicas.  An executed program that does is rejected.
+  if (backward && !mics_ &&
+      (plan_.kind == shardsim::StrategyKind::Fcdp || plan_.kind == shardsim::StrategyKind::FcdpComm || zeropp_))
+    throw shardsim::ProtocolError("zero_bwd_ag_inter: backward AgInter of layer " + std::to_string(e.layer) + " in a " +
+                                  shardsim::to_string(plan_.kind) + " program");
   LayerRt& l = layers_[e.layer];
   const bool wt = wants_t(e.param_set) && l.has_t, wf = wants_f(e.param_set) && l.has_f;
   if (alias_gather(e, wt, wf)) {
@@ -1010,12 +1024,22 @@ void Engine::ev_compute(const Event& e, bool backward) {
     }
     grad = grad_slot(j_, gs);
   }
+  if (grad) grad_segs_set_[li] = 0;
   if (compute_fn_) {
+    bwd_callback_layer_ = grad ? li : -1;
     const int rc = compute_fn_(compute_user_, backward ? FCDP_EV_COMPUTE_BWD : FCDP_EV_COMPUTE_FWD, li, W, grad,
                                s_comp_);
+    bwd_callback_layer_ = -1;
     if (rc != 0) throw std::runtime_error("compute callback failed for layer " + std::to_string(li));
   } else if (grad) {
     CK(cudaMemsetAsync(grad, 0, l.chunks * kChunkBytes, s_comp_));  // data-plane-only mode
+  }
+  if (grad && !grad_segs_set_[li]) {  // the gradient is in the natural slot
+    GradSegs& sg = grad_segs_[li];
+    sg.n = 1;
+    sg.dst_chunk[0] = 0;
+    sg.nchunks[0] = l.chunks;
+    sg.src[0] = grad;
   }
   if (!backward && w_of_layer_[li] != 2 && !(w_of_layer_[li] == kAliasW && prog_->layer_retained[li]))
     w_of_layer_[li] = -1;  // the slot is free for the backward re-gather
@@ -1041,6 +1065,24 @@ void Engine::ev_reduce_scatter(const Event& e) {
   for (int jj = 0; jj < g_; ++jj) gp.p[jj] = grad_slot(jj, gs);
   const float scale = 1.0f / static_cast<float>(G_);
   float* final_out = grad32_ + l.off_t * V_;
+  if (fused_grad_ok(li)) {
+    // G = 1: the RS is the identity up to widen + scale; fused into AdamW,
+    // reading the gradient where backward left it (the slot or the segments)
+    fence_alias_reads(s);
+    const std::int64_t n = l.L.dev.shard_t * V_;
+    const std::size_t o = static_cast<std::size_t>(l.off_t) * V_;
+    const AdamParams p = adam_params(opt_steps_ + 1);
+    const std::uint64_t bytes = static_cast<std::uint64_t>(n) * (6 * sizeof(float) + 2 * eb_ + (keep_grad_ ? 4 : 0));
+    timed(3, s, bytes, [&] {
+      return launch_adam_grad(l.chunks, grad_segs_[li], p, scale, master_ + o, adam_m_ + o, adam_v_ + o,
+                              param_t_ + l.off_t * kChunkBytes, eb_, keep_grad_ ? grad32_ + o : nullptr, s);
+    });
+    stepped_[li] = 1;
+    write_flag(s, kGradFree, u);
+    CK(cudaEventRecord(rs_done_[gs], s));
+    grad_slot_of_layer_[li] = -1;
+    return;
+  }
   // algorithmic bytes: g gradient slices read + fp32 own shard + dtype wire for the rest
   const std::uint64_t rs_bytes = static_cast<std::uint64_t>(g_) * l.slice_real_t * C +
                                  static_cast<std::uint64_t>(l.my_real_t) * V_ * sizeof(float) +
@@ -1138,12 +1180,49 @@ void Engine::mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out) {
   done_s_ = s;
 }
 
+AdamParams Engine::adam_params(int step) const {
+  return AdamParams{adam_.lr, adam_.beta1, adam_.beta2, adam_.eps, adam_.weight_decay,
+                    static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta1), step)),
+                    static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta2), step))};
+}
+
+bool Engine::fused_grad_ok(int li) const {
+  static const char* env = std::getenv("FCDP_FUSED_ADAM");
+  if (env && std::strcmp(env, "0") == 0) return false;
+  const LayerRt& l = layers_.at(li);
+  return G_ == 1 && !zeropp_ && !mics_ && l.has_t && !l.has_f && l.L.dense_trainable() &&
+         prog_ != nullptr && has_opt_;
+}
+
+void Engine::grad_segments(int li, int n, const std::int64_t* offs, const void* const* ptrs,
+                           const std::int64_t* counts) {
+  if (li != bwd_callback_layer_)
+    throw shardsim::ConfigError("grad_segments: only inside the backward compute callback of that layer");
+  if (!fused_grad_ok(li))
+    throw shardsim::ConfigError("grad_segments: layer " + std::to_string(li) +
+                                " needs its gradient in grad_out (segments are taken at G = 1 for dense layers)");
+  if (n < 0 || n > kMaxGradSegs) throw shardsim::ConfigError("grad_segments: at most 24 segments");
+  const LayerRt& l = layers_[li];
+  GradSegs sg;
+  sg.n = n;
+  std::int64_t prev_end = 0;
+  for (int i = 0; i < n; ++i) {
+    if (offs[i] % V_ || counts[i] % V_ || reinterpret_cast<std::uintptr_t>(ptrs[i]) % kChunkBytes || counts[i] < 0 ||
+        offs[i] < prev_end || offs[i] + counts[i] > l.elems)
+      throw shardsim::ConfigError("grad_segments: segment " + std::to_string(i) +
+                                  " must be 16-byte aligned, sorted, disjoint and inside the layer");
+    sg.dst_chunk[i] = offs[i] / V_;
+    sg.nchunks[i] = counts[i] / V_;
+    sg.src[i] = ptrs[i];
+    prev_end = offs[i] + counts[i];
+  }
+  grad_segs_[li] = sg;
+  grad_segs_set_[li] = 1;
+}
+
 void Engine::adam_layer(int li, cudaStream_t s) {
   LayerRt& l = layers_[li];
-  const int step = opt_steps_ + 1;  // the step the program's OptimizerStep will complete
-  AdamParams p{adam_.lr, adam_.beta1, adam_.beta2, adam_.eps, adam_.weight_decay,
-               static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta1), step)),
-               static_cast<float>(1.0 - std::pow(static_cast<double>(adam_.beta2), step))};
+  const AdamParams p = adam_params(opt_steps_ + 1);  // the step the program's OptimizerStep will complete
   // the own shard must have left for the NIC before it is overwritten
   if (ag_staged_valid_[li]) CK(cudaStreamWaitEvent(s, ag_staged_[li], 0));
   fence_alias_reads(s);
@@ -1158,7 +1237,9 @@ void Engine::adam_layer(int li, cudaStream_t s) {
 
 void Engine::ev_optimizer(const Event&) {
   fence_alias_reads(s_comp_);
-  if (early_opt_) {
+  bool any_stepped = false;
+  for (char c : stepped_) any_stepped |= c != 0;
+  if (early_opt_ || any_stepped) {
     for (std::size_t li = 0; li < layers_.size(); ++li)
       if (layers_[li].has_t && !stepped_[li]) adam_layer(static_cast<int>(li), s_comp_);
     ++opt_steps_;
@@ -1190,11 +1271,96 @@ void Engine::run(const shardsim::EventProgram& prog, std::vector<shardsim::Param
   end(states);
 }
 
+void Engine::fail_job() {
+  // An error part-way through a program leaves this rank's sequence counters
+  // (q_, u_, piece ids) out of step with its peers, so no later program may run
+  // on this engine (peers could be satisfied early by stale flag values): latch
+  // the failure and raise the job's abort flag so peers blocked on this rank's
+  // posts fail fast instead of timing out.
+  failed_ = true;
+  if (shm_) shm_->header()->abort_flag.store(1);
+}
+
+std::uint64_t Engine::program_hash(const shardsim::EventProgram& prog) {
+  // FNV-1a over everything that decides the cross-rank sequence numbers: the
+  // iteration, the strategy, every event's kind / layer / portion set / deps
+  // and the per-layer retention flags.
+  std::uint64_t h = 1469598103934665603ull;
+  auto mix = [&](std::uint64_t v) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (v >> (8 * i)) & 0xff;
+      h *= 1099511628211ull;
+    }
+  };
+  mix(prog.iteration_index);
+  mix(static_cast<std::uint64_t>(prog.strategy));
+  mix(prog.events.size());
+  for (const Event& e : prog.events) {
+    mix(static_cast<std::uint64_t>(e.kind) | (static_cast<std::uint64_t>(static_cast<std::uint32_t>(e.layer)) << 8) |
+        (static_cast<std::uint64_t>(e.param_set) << 40));
+    mix(e.deps.size());
+    for (shardsim::EventId d : e.deps) mix(d);
+  }
+  for (char c : prog.layer_retained) mix(static_cast<std::uint64_t>(c != 0));
+  return h;
+}
+
+void Engine::check_same_program(const shardsim::EventProgram& prog) {
+  // Every rank must walk the same program (sequence numbers agree only then):
+  // publish this program's hash, wait for every peer's hash of the same program
+  // index and compare (e.g. per-rank gpu_capacity_bytes could make
+  // tau retention differ between ranks, which would otherwise read wrong data).
+  const std::uint32_t k = ++programs_;
+  const std::uint64_t h = program_hash(prog);
+  RankBlock& me = shm_->rank_block(rank_);
+  me.prog_hash[k % kProgRing].store(h, std::memory_order_relaxed);
+  me.prog_seq[k % kProgRing].store(k, std::memory_order_release);
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(cfg_.timeout_s);
+  for (int r = 0; r < G_; ++r) {
+    if (r == rank_) continue;
+    RankBlock& pb = shm_->rank_block(r);
+    for (int spin = 0;; ++spin) {
+      const std::uint32_t seq = pb.prog_seq[k % kProgRing].load(std::memory_order_acquire);
+      if (seq == k) {
+        const std::uint64_t ph = pb.prog_hash[k % kProgRing].load(std::memory_order_relaxed);
+        if (pb.prog_seq[k % kProgRing].load(std::memory_order_acquire) != k) continue;  // overwritten meanwhile
+        if (ph != h)
+          throw shardsim::ConfigError("engine: rank " + std::to_string(rank_) + " and rank " + std::to_string(r) +
+                                      " were given different programs for program #" + std::to_string(k) +
+                                      " (iteration " + std::to_string(prog.iteration_index) +
+                                      "); every rank must execute the same program");
+        break;
+      }
+      if (static_cast<std::int32_t>(seq - k) > 0) break;  // the peer is already kProgRing programs ahead
+      if (shm_->header()->abort_flag.load(std::memory_order_relaxed))
+        throw TimeoutError("engine: job aborted by a peer");
+      if (spin > 2000) {
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+        if (std::chrono::steady_clock::now() > deadline)
+          throw TimeoutError("engine: rank " + std::to_string(r) + " never started program #" + std::to_string(k));
+      }
+    }
+  }
+}
+
 void Engine::begin(const shardsim::EventProgram& prog) {
+  if (failed_)
+    throw shardsim::ProtocolError("engine: an earlier program failed on this rank; the engine cannot run further "
+                                  "programs (destroy and recreate it)");
   if (prog_) throw shardsim::ProtocolError("engine: a program is already in progress (missing end)");
   if (prog.strategy != plan_.kind) throw shardsim::ConfigError("engine: program strategy differs from the engine plan");
   if (prog.layer_retained.size() != layers_.size()) throw shardsim::ConfigError("engine: program is for another model");
   CK(cudaSetDevice(cfg_.device));
+  for (std::size_t i = 0; i < prog.events.size(); ++i)
+    if (prog.events[i].id != i) throw shardsim::ConfigError("engine: event ids must be 0..n-1 in order");
+  if (G_ > 1) {
+    try {
+      check_same_program(prog);
+    } catch (...) {
+      fail_job();
+      throw;
+    }
+  }
   prog_ = &prog;
   const std::size_t n_ev = prog.events.size();
   while (ev_done_.size() < n_ev) {
@@ -1202,8 +1368,6 @@ void Engine::begin(const shardsim::EventProgram& prog) {
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ev_done_.push_back(e);
   }
-  for (std::size_t i = 0; i < n_ev; ++i)
-    if (prog.events[i].id != i) throw shardsim::ConfigError("engine: event ids must be 0..n-1 in order");
   stream_of_.assign(n_ev, nullptr);
   last_fwd_ = 0;
   for (const Event& e : prog.events) {
@@ -1245,6 +1409,7 @@ void Engine::begin(const shardsim::EventProgram& prog) {
     // compute (N > 1); at N = 1 the update would just contend with the
     // backward GEMMs for HBM (measured: no gain).  FCDP_EARLY_OPT=0/1 forces.
     early_opt_ = has_opt && (eo ? std::strcmp(eo, "0") != 0 : N_ > 1);
+    has_opt_ = has_opt;
   }
   std::fill(cache_stage_f_.begin(), cache_stage_f_.end(), 0);
   if (shared_cache_)
@@ -1280,6 +1445,7 @@ void Engine::exec(std::uint32_t event_id) {
     //  keeps streaming the next layers while this one is expanded)
     const bool bwd = e.id > last_fwd;
     if (trace_) CK(cudaEventRecord(trace_begin_[e.id], s));
+    try {
     switch (e.kind) {
       case EventKind::AgInter: ev_ag_inter(e, bwd); break;
       case EventKind::H2D: ev_h2d(e); break;
@@ -1292,6 +1458,10 @@ void Engine::exec(std::uint32_t event_id) {
       case EventKind::MaskDirty: break;  // bookkeeping only (step_state)
       case EventKind::Broadcast:
         throw shardsim::ConfigError("engine: broadcast events (zero2) are not part of this data plane");
+    }
+    } catch (...) {
+      fail_job();
+      throw;
     }
     const cudaStream_t ds = done_s_ ? done_s_ : s;
     done_s_ = nullptr;

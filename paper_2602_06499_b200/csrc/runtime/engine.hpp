@@ -83,6 +83,13 @@ class Engine {
   void counters(int rank, fcdp_counters* out) const;
   void reset_counters();
 
+  // G = 1 fused gradient -> AdamW (see kernels.cu adam_grad_kernel)
+  bool fused_grad_ok(int layer) const;
+  // Inside the backward compute callback of `layer`: its gradient lives in
+  // these caller buffers (param dtype, 16-byte aligned) instead of grad_out.
+  void grad_segments(int layer, int n, const std::int64_t* elem_offsets, const void* const* ptrs,
+                     const std::int64_t* counts);
+  void set_keep_grad(bool on) { keep_grad_ = on; }
   void set_timing(bool on) { timing_ = on; }
   void kernel_stats(fcdp_kernel_stats* out, bool reset);
   void set_trace(bool on) { trace_ = on; }
@@ -92,8 +99,15 @@ class Engine {
   void read_master(int layer, float* host, std::size_t count);
   void read_grad(int layer, float* host, std::size_t count);
   void read_host_cache(int layer, bool frozen, void* host, std::size_t bytes);
+  bool failed() const { return failed_; }
 
  private:
+  // ---- failure / cross-rank program agreement
+  void fail_job();
+  static std::uint64_t program_hash(const shardsim::EventProgram& prog);
+  void check_same_program(const shardsim::EventProgram& prog);
+  bool failed_ = false;
+  std::uint32_t programs_ = 0;  // programs begun on this engine (same count on every rank)
   // ---- setup
   void build_layouts(const std::uint8_t* const* masks);
   void allocate();
@@ -215,10 +229,16 @@ class Engine {
   // launch after the last RS.  Elementwise, so results are identical.  On
   // by default when N > 1.
   bool early_opt_ = false;
+  bool has_opt_ = false;       // the current program has an OptimizerStep
   std::vector<char> stepped_;                 // per layer: updated early this iteration
   std::vector<cudaEvent_t> ag_staged_;        // per layer: own shard staged for the NIC (s_agsend_)
   std::vector<char> ag_staged_valid_;
   void adam_layer(int li, cudaStream_t s);
+  AdamParams adam_params(int step) const;
+  bool keep_grad_ = false;        // fused path also writes the fp32 gradient shard (readback)
+  int bwd_callback_layer_ = -1;   // layer whose backward callback is running
+  std::vector<GradSegs> grad_segs_;  // per layer: where its gradient is (fused path)
+  std::vector<char> grad_segs_set_;
   // G = 1: gathers of single-portion layers alias the shard (no copy)
   bool alias_used_ = false;
   std::vector<char> prev_retained_;  // per layer: retained in the previous executed program

@@ -99,6 +99,17 @@ int fcdp_engine_read_host_cache(fcdp_engine* e, int32_t layer, int32_t frozen, v
 
 int fcdp_engine_set_timing(fcdp_engine* e, int32_t on) { return guarded([&] { E(e).set_timing(on != 0); }); }
 
+int fcdp_engine_grad_segments(fcdp_engine* e, int32_t layer, int32_t n, const int64_t* elem_offsets,
+                              const void* const* ptrs, const int64_t* counts) {
+  return guarded([&] { E(e).grad_segments(layer, n, elem_offsets, ptrs, counts); });
+}
+
+int fcdp_engine_takes_grad_segments(fcdp_engine* e, int32_t layer, int32_t* out) {
+  return guarded([&] { *out = E(e).fused_grad_ok(layer) ? 1 : 0; });
+}
+
+int fcdp_engine_set_keep_grad(fcdp_engine* e, int32_t on) { return guarded([&] { E(e).set_keep_grad(on != 0); }); }
+
 int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t reset) {
   return guarded([&] { E(e).kernel_stats(out, reset != 0); });
 }

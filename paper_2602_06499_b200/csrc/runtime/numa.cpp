@@ -8,6 +8,7 @@
 #include <cctype>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <fstream>
 #include <sstream>
 
@@ -92,6 +93,32 @@ bool numa_pin_thread(int node) {
   for (int c : cpus)
     if (c >= 0 && c < CPU_SETSIZE) CPU_SET(c, &set);
   return sched_setaffinity(0, sizeof(set), &set) == 0;
+}
+
+SavedAffinity numa_save_affinity() {
+  SavedAffinity a;
+  static_assert(sizeof(cpu_set_t) <= sizeof(a.set), "cpu_set_t size");
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  if (sched_getaffinity(0, sizeof(set), &set) == 0) {
+    std::memcpy(a.set, &set, sizeof(set));
+    a.valid = true;
+  }
+  return a;
+}
+
+void numa_restore_affinity(const SavedAffinity& a) {
+  if (!a.valid) return;
+  cpu_set_t set;
+  std::memcpy(&set, a.set, sizeof(set));
+  sched_setaffinity(0, sizeof(set), &set);
+}
+
+int numa_node_of_page(const void* p) {
+  int node = -1;
+  constexpr unsigned long kMpolFNode = 1, kMpolFAddr = 2;
+  if (syscall(SYS_get_mempolicy, &node, nullptr, 0ul, p, kMpolFNode | kMpolFAddr) != 0) return -1;
+  return node;
 }
 
 }  // namespace fcdp

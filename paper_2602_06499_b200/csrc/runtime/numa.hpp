@@ -30,5 +30,16 @@ std::vector<int> parse_cpulist(const std::string& s);
 bool numa_prefer(void* p, std::size_t bytes, int node);
 // Pin the calling thread (and threads it creates later) to the node's cores.
 bool numa_pin_thread(int node);
+// The calling thread's CPU affinity, saved and restored around a temporary pin
+// (the engine pins only while it first-touches its host tiers and starts its
+// NIC thread; the caller's own thread gets its affinity back).
+struct SavedAffinity {
+  bool valid = false;
+  unsigned char set[128] = {};  // cpu_set_t bytes
+};
+SavedAffinity numa_save_affinity();
+void numa_restore_affinity(const SavedAffinity& a);
+// Node of the page holding p (get_mempolicy MPOL_F_NODE|MPOL_F_ADDR), -1 on error.
+int numa_node_of_page(const void* p);
 
 }  // namespace fcdp

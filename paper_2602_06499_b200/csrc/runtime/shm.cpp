@@ -4,6 +4,8 @@
 #include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
+#include <signal.h>
+#include <cerrno>
 
 #include <chrono>
 #include <cstring>
@@ -48,39 +50,51 @@ SharedBlock::SharedBlock(const std::string& name, int rank, int world, int nodes
       close(fd);
       throw std::runtime_error("ftruncate(shm) failed: " + std::string(std::strerror(errno)));
     }
-  } else {
-    for (;;) {
-      fd = shm_open(name_.c_str(), O_RDWR, 0600);
-      if (fd >= 0) {
-        struct stat st {};
-        if (fstat(fd, &st) == 0 && static_cast<std::size_t>(st.st_size) >= bytes_) break;
-        close(fd);
-        fd = -1;
-      }
-      if (std::chrono::steady_clock::now() > deadline)
-        throw TimeoutError("engine: shared control block " + name_ + " did not appear");
-      std::this_thread::sleep_for(std::chrono::milliseconds(2));
-    }
-  }
-  void* p = mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
-  close(fd);
-  if (p == MAP_FAILED) throw std::runtime_error("mmap(shm) failed: " + std::string(std::strerror(errno)));
-  hdr_ = static_cast<ShmHeader*>(p);
-
-  if (rank == 0) {
-    // ftruncate zero-fills; publish geometry, then the magic last.
+    void* p = mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) throw std::runtime_error("mmap(shm) failed: " + std::string(std::strerror(errno)));
+    hdr_ = static_cast<ShmHeader*>(p);
+    // ftruncate zero-fills; publish geometry and the creator, then the magic last.
     hdr_->world = world;
     hdr_->nodes = nodes;
     hdr_->local = local;
     hdr_->inter_slots = inter_slots;
     hdr_->slot_bytes = slot_bytes;
     hdr_->total_bytes = bytes_;
+    hdr_->creator_pid = static_cast<std::int32_t>(getpid());
+    hdr_->creator_nonce = now_ns() ^ (static_cast<std::uint64_t>(getpid()) << 40);
     hdr_->magic.store(kShmMagic, std::memory_order_release);
   } else {
-    while (hdr_->magic.load(std::memory_order_acquire) != kShmMagic) {
+    for (;;) {
+      fd = shm_open(name_.c_str(), O_RDWR, 0600);
+      if (fd >= 0) {
+        struct stat st {};
+        if (fstat(fd, &st) == 0 && static_cast<std::size_t>(st.st_size) >= bytes_) {
+          void* p = mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+          close(fd);
+          fd = -1;
+          if (p == MAP_FAILED) throw std::runtime_error("mmap(shm) failed: " + std::string(std::strerror(errno)));
+          auto* h = static_cast<ShmHeader*>(p);
+          while (h->magic.load(std::memory_order_acquire) != kShmMagic &&
+                 std::chrono::steady_clock::now() < deadline)
+            std::this_thread::sleep_for(std::chrono::milliseconds(1));
+          // a live creator: this is the current job's segment (a crashed job's
+          // rank 0 is gone, and its segment is about to be unlinked and recreated)
+          const bool live = h->magic.load(std::memory_order_acquire) == kShmMagic &&
+                            (kill(h->creator_pid, 0) == 0 || errno == EPERM);
+          if (live) {
+            hdr_ = h;
+            break;
+          }
+          munmap(p, bytes_);
+        } else {
+          close(fd);
+          fd = -1;
+        }
+      }
       if (std::chrono::steady_clock::now() > deadline)
-        throw TimeoutError("engine: shared control block " + name_ + " not initialised");
-      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+        throw TimeoutError("engine: shared control block " + name_ + " did not appear");
+      std::this_thread::sleep_for(std::chrono::milliseconds(2));
     }
     if (hdr_->world != world || hdr_->nodes != nodes || hdr_->local != local ||
         hdr_->slot_bytes != slot_bytes || hdr_->inter_slots != inter_slots)
@@ -157,7 +171,7 @@ void SharedBlock::await_posted(int rank, Flag f, std::uint32_t v, double timeout
   }
 }
 
-void SharedBlock::barrier(double timeout_s) const {
+void SharedBlock::barrier(double timeout_s, bool honour_abort) const {
   const std::uint32_t gen = hdr_->barrier_gen.load(std::memory_order_acquire);
   if (hdr_->barrier_count.fetch_add(1, std::memory_order_acq_rel) + 1 ==
       static_cast<std::uint32_t>(hdr_->world)) {
@@ -168,7 +182,8 @@ void SharedBlock::barrier(double timeout_s) const {
   const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(timeout_s);
   int spins = 0;
   while (hdr_->barrier_gen.load(std::memory_order_acquire) == gen) {
-    if (hdr_->abort_flag.load(std::memory_order_relaxed)) throw TimeoutError("engine: job aborted by a peer");
+    if (honour_abort && hdr_->abort_flag.load(std::memory_order_relaxed))
+      throw TimeoutError("engine: job aborted by a peer");
     if (++spins > 1000) {
       std::this_thread::sleep_for(std::chrono::microseconds(50));
       if (std::chrono::steady_clock::now() > deadline) throw TimeoutError("engine: barrier timed out");

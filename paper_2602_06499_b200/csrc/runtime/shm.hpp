@@ -21,6 +21,7 @@ namespace fcdp {
 
 inline constexpr std::uint64_t kShmMagic = 0x46434450'42323030ull;  // "FCDPB200"
 inline constexpr int kMaxRanks = 64;
+inline constexpr int kProgRing = 8;  // program hashes kept per rank (begin() agreement check)
 
 enum Flag : int {
   kAgTxReady = 0,  // inter AG: my staged piece <= id has crossed the emulated wire
@@ -61,6 +62,9 @@ struct alignas(64) RankBlock {
   std::uint64_t arena_bytes;
   std::int32_t pid, device;
   std::atomic<std::uint32_t> attached;
+  // Hash of the k-th program this rank began, in slot k % kProgRing.
+  std::atomic<std::uint64_t> prog_hash[kProgRing];
+  std::atomic<std::uint32_t> prog_seq[kProgRing];
 };
 
 struct alignas(64) NodeBlock {
@@ -72,6 +76,11 @@ struct alignas(64) ShmHeader {
   std::int32_t world, nodes, local, inter_slots;
   std::uint64_t slot_bytes;   // bytes of one staging slot
   std::uint64_t total_bytes;
+  // Rank 0's pid and a per-creation nonce, written before the magic: a rank
+  // that attached to a stale segment of a crashed job (same name) sees a dead
+  // creator and re-opens the name.
+  std::int32_t creator_pid;
+  std::uint64_t creator_nonce;
   alignas(64) std::atomic<std::uint32_t> barrier_count;
   alignas(64) std::atomic<std::uint32_t> barrier_gen;
   alignas(64) std::atomic<std::uint32_t> abort_flag;
@@ -130,7 +139,9 @@ class SharedBlock {
   void await_posted(int rank, Flag f, std::uint32_t v, double timeout_s) const;
 
   // Host barrier over all ranks (sense-reversing on a generation counter).
-  void barrier(double timeout_s) const;
+  // honour_abort = false: the teardown barrier, which must still gather every
+  // rank after a peer aborted (no rank may free memory a peer still reads).
+  void barrier(double timeout_s, bool honour_abort = true) const;
   // Reserve `ns` of wire time on node n's NIC; returns the finish time (ns,
   // steady clock).  Reservations from the node's ranks serialise.
   std::uint64_t reserve_nic(int node, std::uint64_t ns) const;

@@ -151,6 +151,24 @@ class Engine:
                        "link_bytes": int(k.link_bytes[i])}
                 for i, name in enumerate(self.KERNEL_CLASSES + self.COPY_CLASSES)}
 
+    def takes_grad_segments(self, layer: int) -> bool:
+        """Inside a backward callback: may `layer` hand its gradient over as
+        segments of the caller's own buffers (G = 1 fused RS + AdamW)?"""
+        out = C.c_int32()
+        check(lib().fcdp_engine_takes_grad_segments(self._h, layer, C.byref(out)))
+        return bool(out.value)
+
+    def grad_segments(self, layer: int, segments: Sequence[Tuple[int, int, int]]) -> None:
+        """[(element offset in the layer, device pointer, element count)], sorted."""
+        n = len(segments)
+        offs = (C.c_int64 * max(n, 1))(*[s[0] for s in segments])
+        ptrs = (C.c_void_p * max(n, 1))(*[s[1] for s in segments])
+        cnts = (C.c_int64 * max(n, 1))(*[s[2] for s in segments])
+        check(lib().fcdp_engine_grad_segments(self._h, layer, n, offs, ptrs, cnts))
+
+    def set_keep_grad(self, on: bool) -> None:
+        check(lib().fcdp_engine_set_keep_grad(self._h, int(on)))
+
     def set_trace(self, on: bool) -> None:
         check(lib().fcdp_engine_set_trace(self._h, int(on)))
 

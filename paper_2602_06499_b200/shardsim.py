@@ -19,7 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import Dict, List, Optional, Sequence
 
 from . import _capi
 from ._capi import ConfigError, ProtocolError, check, lib
@@ -477,6 +477,40 @@ class EventProgram:
         buf = (C.c_uint8 * max(num_layers, 1))()
         check(lib().fcdp_program_layer_flags(self.ptr, buf, num_layers))
         return list(buf)[:num_layers]
+
+    @staticmethod
+    def from_events(iteration_index: int, strategy: StrategyKind, events: Sequence[Event],
+                    layer_flags: Sequence[int]) -> "EventProgram":
+        """A program from an explicit event list (fcdp_program_create): an
+        external scheduler's program, or a mutated one."""
+        n = len(events)
+        arr = (_capi.EventC * max(n, 1))()
+        off = (C.c_uint32 * (n + 1))()
+        flat: List[int] = []
+        for i, e in enumerate(events):
+            arr[i] = _capi.EventC(e.id, int(e.kind), e.layer, int(e.param_set), e.bytes_total, len(e.deps))
+            off[i] = len(flat)
+            flat += list(e.deps)
+        off[n] = len(flat)
+        deps = (C.c_uint32 * max(len(flat), 1))(*flat)
+        L = len(layer_flags)
+        fl = (C.c_uint8 * max(L, 1))(*layer_flags)
+        out = C.c_void_p()
+        check(lib().fcdp_program_create(iteration_index, int(strategy), n, arr, off, deps, L, fl, C.byref(out)))
+        return EventProgram(out.value, strategy, iteration_index)
+
+    def without(self, drop: Sequence[int], num_layers: int,
+                replace: Optional[Dict[int, Event]] = None) -> "EventProgram":
+        """Mutation helper: this program minus the events `drop` (ids renumbered,
+        deps on dropped events removed), with events in `replace` swapped in."""
+        keep = [e for e in self.events if e.id not in set(drop)]
+        new_id = {e.id: i for i, e in enumerate(keep)}
+        evs = []
+        for e in keep:
+            r = (replace or {}).get(e.id, e)
+            evs.append(Event(new_id[e.id], r.kind, r.layer, r.param_set, r.bytes_total,
+                             [new_id[d] for d in e.deps if d in new_id]))
+        return EventProgram.from_events(self.iteration_index, self.strategy, evs, self.layer_flags(num_layers))
 
 
 def init_param_states(model: ModelSpec) -> List[ParamState]:

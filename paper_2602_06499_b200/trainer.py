@@ -14,6 +14,7 @@ from the buffer the backward pass re-gathered - ZeRO-3/FCDP semantics
 """
 from __future__ import annotations
 
+import os
 from typing import Dict, List, Optional
 
 import numpy as np
@@ -56,6 +57,8 @@ class FcdpTrainer:
         self._cur = None
         self._grad_act = None
         self.loss: Optional[torch.Tensor] = None
+        self._held_grads: List[torch.Tensor] = []
+        self._segments_ok = os.environ.get("FCDP_GRAD_SEGMENTS", "1") != "0"
         self.last_program: Optional[S.EventProgram] = None
 
     # -------------------------------------------------------------- API
@@ -67,6 +70,7 @@ class FcdpTrainer:
                                  gpu_capacity_bytes=self.gpu_capacity_bytes)
         self.tokens, self.labels = tokens, labels
         self.states = self.engine.run(prog, self.states)
+        self._held_grads.clear()  # the program (incl. its fused updates) is enqueued before the join
         self.last_program = prog
         return self.loss
 
@@ -93,6 +97,27 @@ class FcdpTrainer:
             _, layer, off, shape, stride = obj
             return torch.as_strided(self._bwd_w[layer], shape, stride, off)
         return obj
+
+    def _hand_over(self, layer: int, ldef: LayerDef, train, grads) -> bool:
+        """G = 1: give the engine autograd's own gradient buffers (no copy into
+        the natural gradient slot; the fused RS + AdamW reads them in place).
+        They stay referenced until step() returns (engine.run enqueued the
+        program's end, which orders the compute stream after the update)."""
+        if not self._segments_ok or not self.engine.takes_grad_segments(layer):
+            return False
+        segs = []
+        for n, gr in zip(train, grads):
+            if gr is None:
+                continue  # an unused tensor: gradient 0 (chunks no segment covers)
+            if not gr.is_contiguous() or gr.dtype != self.dtype or gr.data_ptr() % 16:
+                return False
+            segs.append((ldef.offsets[n], gr.data_ptr(), gr.numel()))
+        segs.sort()
+        if len(segs) > 24:
+            return False
+        self.engine.grad_segments(layer, segs)
+        self._held_grads.extend(g for g in grads if g is not None)
+        return True
 
     def _params(self, flat: torch.Tensor, ldef: LayerDef, grad: bool):
         out = {}
@@ -138,14 +163,15 @@ class FcdpTrainer:
                     self._grad_act = grads[0]
                     grads = grads[1:]
                 if g:
-                    G = device_view(g, ldef.numel, self.dtype, self.device)
-                    for n, gr in zip(train, grads):
-                        o = ldef.offsets[n]
-                        dst = G[o:o + gr.numel() if gr is not None else o]
-                        if gr is None:
-                            G[o:o + p[n].numel()].zero_()
-                        else:
-                            dst.copy_(gr.reshape(-1))
+                    if not self._hand_over(layer, ldef, train, grads):
+                        G = device_view(g, ldef.numel, self.dtype, self.device)
+                        for n, gr in zip(train, grads):
+                            o = ldef.offsets[n]
+                            dst = G[o:o + gr.numel() if gr is not None else o]
+                            if gr is None:
+                                G[o:o + p[n].numel()].zero_()
+                            else:
+                                dst.copy_(gr.reshape(-1))
                 if layer == 0:
                     self._grad_act = None
                     self._saved_out = None

@@ -12,6 +12,9 @@ the event programs the B200 engine executed plus its measured byte counters:
                         an event that reconstructs it, unless the layer was
                         retained (freshness, SPEC.md:244)
     bytes_conserved     per-node measured NIC bytes == comm_volume
+    trace_respects_deps over an EXECUTED trace (fcdp_engine_trace): no event's
+                        stream reached it before every dependency had finished
+                        on the device (the DAG edges were honoured at run time)
 
 check_* functions return a list of Violation(rule, event_id, detail); an
 empty list means the rule holds.  tests/test_verify.py mutates programs to
@@ -101,6 +104,44 @@ def check_compute_has_params(events: Sequence[Event], retained: Sequence[int] = 
 def check_bytes_conserved(measured: Dict[str, int], expected: Dict[str, int]) -> List[Violation]:
     return [Violation("bytes_conserved", None, f"{k}: measured {measured.get(k)} != oracle {v}")
             for k, v in expected.items() if measured.get(k) != v]
+
+
+def check_trace_respects_deps(events: Sequence[Event], begin_ms: Sequence[float], end_ms: Sequence[float],
+                              tol_ms: float = 0.05) -> List[Violation]:
+    """Executed-trace rule: every event began (its stream reached it, after its
+    dependency waits) no earlier than each dependency finished."""
+    out = []
+    for e in events:
+        for d in e.deps:
+            if begin_ms[e.id] + tol_ms < end_ms[d]:
+                out.append(Violation("trace_respects_deps", e.id,
+                                     f"{e.kind.name} L{e.layer} began at {begin_ms[e.id]:.3f} ms before dependency "
+                                     f"{d} finished at {end_ms[d]:.3f} ms"))
+    return out
+
+
+def overlap_fraction(events: Sequence[Event], begin_ms: Sequence[float], end_ms: Sequence[float],
+                     kinds: Iterable[EventKind], against: Iterable[EventKind]) -> Optional[float]:
+    """Fraction of the device time of events of `kinds` (e.g. the FCDP-Cache
+    D2H stores) that overlaps the union of events of `against` (e.g. compute):
+    north_star's "overlapped with compute", measured on an executed trace."""
+    kinds, against = set(kinds), set(against)
+    busy = sorted((begin_ms[e.id], end_ms[e.id]) for e in events if e.kind in against)
+    merged: List[List[float]] = []
+    for a, b in busy:
+        if merged and a <= merged[-1][1]:
+            merged[-1][1] = max(merged[-1][1], b)
+        else:
+            merged.append([a, b])
+    total = covered = 0.0
+    for e in events:
+        if e.kind not in kinds:
+            continue
+        a, b = begin_ms[e.id], end_ms[e.id]
+        total += b - a
+        for x, y in merged:
+            covered += max(0.0, min(b, y) - max(a, x))
+    return covered / total if total > 0 else None
 
 
 def check_program(strategy: StrategyKind, events: Sequence[Event], retained: Sequence[int] = ()) -> List[Violation]:

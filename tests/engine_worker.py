@@ -52,6 +52,7 @@ def main():
                  use_copy_engine=cfg.get("use_ce", False), timeout_s=120.0)
     eng.init_params(cfg["seed"], [[(0, E, 0, 0.05)] for E in cfg["params"]])
     eng.set_adam(lr=1e-2, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.01)
+    eng.set_keep_grad(True)  # the fused G = 1 path also writes the fp32 gradient shard (read_grad)
     stream = torch.cuda.ExternalStream(eng.compute_stream(), device=device)
     captures = []
     c = grad_coeff(rank)
@@ -66,13 +67,46 @@ def main():
                 G.copy_((W.float() * c).to(dtype))
 
     eng.set_compute(compute)
+    if cfg.get("trace"):
+        eng.set_trace(True)
     states = S.init_param_states(model)
     dumps = []
+    mut = cfg.get("mutate")
     for it in range(1, cfg["iters"] + 1):
-        prog = S.build_iteration(plan, model, topo, states, it,
-                                 gpu_capacity_bytes=cfg.get("capacity", 0))
+        cap = cfg.get("capacity", 0)
+        if mut and mut["kind"] == "capacity_mismatch" and rank == 1:
+            cap = mut["capacity"]
+        prog = S.build_iteration(plan, model, topo, states, it, gpu_capacity_bytes=cap)
+        if mut and it == mut["it"]:
+            # SPEC.md:389-409 mutation harness, applied to the EXECUTED program
+            evs = prog.events
+            last_fwd = max(e.id for e in evs if e.kind == S.EventKind.ComputeFwd)
+            if mut["kind"] == "drop_d2h":  # the layer's FCDP-Cache store is lost
+                drop = [e.id for e in evs if e.kind == S.EventKind.D2H and e.layer == mut["layer"]]
+                prog = prog.without(drop, model.num_layers())
+            elif mut["kind"] == "bwd_ag_inter":  # backward reload replaced by an inter-node gather
+                h2d = next(e for e in evs if e.kind == S.EventKind.H2D and e.layer == mut["layer"] and e.id > last_fwd)
+                intra = next(e for e in evs if e.kind == S.EventKind.AgIntra and e.layer == mut["layer"]
+                             and e.id > last_fwd)
+                ag = S.Event(h2d.id, S.EventKind.AgInter, h2d.layer, S.ParamSet.All, h2d.bytes_total, h2d.deps)
+                prog = prog.without([intra.id], model.num_layers(), replace={h2d.id: ag})
         eng.reset_counters()
         eng.barrier()
+        if mut and it == mut["it"]:
+            errs = []
+            try:
+                eng.run_stepwise(prog, states) if cfg.get("stepwise") else eng.run(prog, states)
+                eng.sync()
+            except Exception as ex:  # noqa: BLE001 - recorded for the test
+                errs.append((type(ex).__name__, getattr(ex, "args", [None])[0], str(ex)))
+            try:  # the engine must refuse to continue after a failed program
+                eng.run(prog, states)
+            except Exception as ex:  # noqa: BLE001
+                errs.append((type(ex).__name__, getattr(ex, "args", [None])[0], str(ex)))
+            with open(os.path.join(cfg["out"], f"rank{rank}.pkl"), "wb") as f:
+                pickle.dump({"errors": errs}, f)
+            eng.close()
+            return
         states = eng.run_stepwise(prog, states) if cfg.get("stepwise") else eng.run(prog, states)
         eng.sync()
         eng.barrier()
@@ -81,6 +115,9 @@ def main():
                                      for k, l, t in captures],
              "counters": eng.counters(), "host": {}, "grad": {}, "master": {}, "shard_t": {}, "shard_f": {},
              "retained": prog.layer_flags(model.num_layers())}
+        if cfg.get("trace"):
+            tr = eng.trace(prog)
+            d["trace"] = [(e.id, int(e.kind), e.layer, list(e.deps), b, t) for e, b, t in tr]
         captures.clear()
         for l in range(model.num_layers()):
             geo = O.geom(len(masks[l]), masks[l], scope_nodes(cfg), g)

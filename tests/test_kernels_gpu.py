@@ -169,6 +169,56 @@ def test_adam_bit_exact(built, eb):
 
 
 @pytest.mark.parametrize("eb", [2, 4])
+def test_fused_grad_adam_bit_exact(built, eb):
+    """G = 1 fused RS + AdamW (the engine's one-GPU path) vs the oracle's RS
+    (g = 1, final scale) followed by its AdamW: masters, moments, parameter
+    shard and the kept fp32 gradient bit for bit, with the gradient handed over
+    as segments that leave gaps (uncovered elements = gradient 0) and include
+    -0.0 / zero gradients."""
+    from paper_2602_06499_b200 import _capi
+    dev = _dev()
+    lib = built
+    V = 16 // eb
+    rng = np.random.default_rng(23)
+    chunks = 9001
+    n = chunks * V
+    mask = np.ones(chunks, np.uint8)
+    geo = O.geom(chunks, mask, 1, 1)
+    w = rng.standard_normal(n).astype(np.float32)
+    m = np.zeros(n, np.float32); v = np.zeros(n, np.float32)
+    p = np.zeros(n, np.uint16 if eb == 2 else np.float32)
+    dw, dm, dv = (torch.from_numpy(a.copy()).to(dev) for a in (w, m, v))
+    dp = torch.zeros(n * eb, dtype=torch.uint8, device=dev)
+    keep = torch.zeros(n, dtype=torch.float32, device=dev)
+    segs = [(0, 1000 * V), (1000 * V, 3000 * V), (4500 * V, 4000 * V), (8600 * V, 401 * V)]  # gap 4000..4500
+    for step in range(1, 4):
+        x = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+        x[:64] = 0.0
+        x[64:128] = -0.0
+        nat = O.f32_to_bf16(x) if eb == 2 else x
+        covered = np.zeros(n, bool)
+        for o, c in segs:
+            covered[o:o + c] = True
+        nat = np.where(covered, nat, np.zeros_like(nat))
+        own, _ = O.rs_slice(geo, mask, eb, [nat], 0, 0, 1.0, True)
+        O.adam(w, m, v, own, p, 1e-3, 0.9, 0.95, 1e-8, 0.1, step)
+        dnat = torch.from_numpy(nat.view(np.uint8).copy()).to(dev)
+        base = dnat.data_ptr()
+        offs = (C.c_int64 * len(segs))(*[o for o, _ in segs])
+        ptrs = (C.c_void_p * len(segs))(*[base + o * eb for o, _ in segs])
+        cnts = (C.c_int64 * len(segs))(*[c for _, c in segs])
+        cfg = _capi.AdamConfig(1e-3, 0.9, 0.95, 1e-8, 0.1, step)
+        _capi.check(lib.fcdp_adam_grad_step(n, C.byref(cfg), 1.0, len(segs), offs, ptrs, cnts, _ptr(dw), _ptr(dm),
+                                            _ptr(dv), _ptr(dp), eb, _ptr(keep), None))
+        torch.cuda.synchronize()
+        assert np.array_equal(keep.cpu().numpy().view(np.uint32), own.view(np.uint32)), step
+        assert np.array_equal(dw.cpu().numpy().view(np.uint32), w.view(np.uint32)), step
+        assert np.array_equal(dm.cpu().numpy().view(np.uint32), m.view(np.uint32)), step
+        assert np.array_equal(dv.cpu().numpy().view(np.uint32), v.view(np.uint32)), step
+        assert np.array_equal(dp.cpu().numpy(), p.view(np.uint8)), step
+
+
+@pytest.mark.parametrize("eb", [2, 4])
 def test_init_bit_exact(built, eb):
     from paper_2602_06499_b200 import _capi
     dev = _dev()
@@ -332,10 +382,19 @@ def test_rs_random_shapes_bit_exact(built):
             check(lib.fcdp_rs_slice(lay, G, j, n, scale, int(N == 1), _ptr(down), _ptr(dwire), None))
             torch.cuda.synchronize()
             assert np.array_equal(down.cpu().numpy()[:own.size].view(np.uint32), own.view(np.uint32))
+            # the wire: real chunks of the other nodes' shards, cast to the param dtype
+            w = dwire.cpu().numpy()[:wire.nbytes].view(wire.dtype)
+            sel = np.zeros(wire.size, bool)
+            sel[:max(0, min(geo.slice_t, geo.pt - j * geo.slice_t)) * V] = True
+            sel[n * geo.shard_t * V:(n + 1) * geo.shard_t * V] = False
+            assert np.array_equal(w[sel].view(np.uint8), wire[sel].view(np.uint8))
             if N > 1 and geo.shard_t:
                 sh = geo.shard_t * V
-                rx = (O.f32_to_bf16(rng.standard_normal(N * sh).astype(np.float32)) if eb == 2
-                      else rng.standard_normal(N * sh).astype(np.float32))
+                # the epilogue's input is the kernel's own wire output, as a peer node would send it
+                rx = np.zeros(N * sh, wire.dtype)
+                for m_ in range(N):
+                    if m_ != n:
+                        rx[m_ * sh:(m_ + 1) * sh] = w[m_ * sh:(m_ + 1) * sh]
                 ref = O.rs_finalize(own[:sh].copy(), rx, N, n, eb, sh, scale)
                 drx, downs = _u8(rx, dev), down[:sh].contiguous()
                 out = torch.zeros(sh, dtype=torch.float32, device=dev)

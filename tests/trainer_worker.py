@@ -26,6 +26,7 @@ def main():
                     batch_per_gpu=cfg["batch"], seed=cfg["seed"], nic_pacing=False, lr=cfg["lr"],
                     weight_decay=cfg["wd"])
     from oracle import oracle as O
+    t.engine.set_keep_grad(True)  # read_grad after the fused G = 1 update
     V = 16 // mc.dtype_bytes
     geos = [O.geom(d.numel * mc.dtype_bytes // 16, d.chunk_mask(mc.dtype_bytes), N, g) for d in t.defs]
     losses, grads, masters = [], [], []
