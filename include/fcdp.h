@@ -239,6 +239,10 @@ typedef struct fcdp_adam_config {
 } fcdp_adam_config;
 int fcdp_adam_step(int64_t n, const fcdp_adam_config* cfg, float* master, float* m, float* v,
                    const float* grad, void* param, int32_t param_elem_bytes, void* stream);
+/* Let kernels launched on `device` dereference `peer`'s memory over NVLink
+ * (single-process multi-GPU use of the stateless kernels; the engine itself
+ * maps peers through CUDA IPC). */
+int fcdp_enable_peer_access(int32_t device, int32_t peer);
 /* G = 1 fused reduce-scatter + AdamW of a dense layer (the engine's path at one
  * GPU): the gradient in the parameter dtype from segments (element offset,
  * pointer, count; 16-byte aligned; uncovered elements have gradient 0),
@@ -394,6 +398,16 @@ int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t res
  * at which its stream reached it (begin) and finished it (end). */
 int fcdp_engine_set_trace(fcdp_engine* e, int32_t on);
 int fcdp_engine_trace(fcdp_engine* e, float* begin_ms, float* end_ms, uint32_t capacity, uint32_t* count);
+
+/* Host-only NUMA placement checks (no GPU needed):
+ * parse a sysfs cpulist ("0-3,8"); and for `node`: online memory nodes, its
+ * CPU count, whether a preferred-node mbind of a fresh mapping succeeded, the
+ * node its first page landed on after first touch, and whether a temporary
+ * pin of the calling thread to the node was undone exactly (the engine pins
+ * only during construction). */
+int fcdp_numa_parse_cpulist(const char* list, int32_t* out, int32_t capacity, int32_t* count);
+int fcdp_numa_selftest(int32_t node, uint64_t bytes, int32_t* num_nodes, int32_t* cpus_in_node,
+                       int32_t* prefer_ok, int32_t* node_of_page, int32_t* affinity_restored);
 
 /* Host-only protocol self-test (no GPU needed): attach the shared control
  * block, run `rounds` barrier-separated rounds in which every rank charges

@@ -149,6 +149,10 @@ SIGNATURES = {
     "fcdp_rs_slice": (C.c_int, [P, PP, i32, i32, f32, i32, P, P, P]),
     "fcdp_rs_finalize": (C.c_int, [i64, i32, i32, i32, P, P, i64, f32, P, P]),
     "fcdp_adam_step": (C.c_int, [i64, C.POINTER(AdamConfig), P, P, P, P, P, i32, P]),
+    "fcdp_enable_peer_access": (C.c_int, [i32, i32]),
+    "fcdp_numa_parse_cpulist": (C.c_int, [C.c_char_p, C.POINTER(i32), i32, C.POINTER(i32)]),
+    "fcdp_numa_selftest": (C.c_int, [i32, C.c_uint64, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
+                                     C.POINTER(i32), C.POINTER(i32)]),
     "fcdp_adam_grad_step": (C.c_int, [i64, C.POINTER(AdamConfig), C.c_float, i32, C.POINTER(C.c_int64), C.POINTER(P),
                                       C.POINTER(C.c_int64), P, P, P, P, i32, P, P]),
     "fcdp_init_natural": (C.c_int, [P, u64, i32, C.POINTER(InitRange), i32, P, P]),

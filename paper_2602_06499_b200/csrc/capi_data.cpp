@@ -135,6 +135,22 @@ int fcdp_adam_step(int64_t n, const fcdp_adam_config* c, float* master, float* m
   });
 }
 
+int fcdp_enable_peer_access(int32_t device, int32_t peer) {
+  return guarded([&] {
+    int can = 0;
+    check_cuda(cudaDeviceCanAccessPeer(&can, device, peer), "cudaDeviceCanAccessPeer");
+    if (!can) throw shardsim::ConfigError("device " + std::to_string(device) + " cannot access peer " +
+                                         std::to_string(peer));
+    int cur = 0;
+    check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
+    check_cuda(cudaSetDevice(device), "cudaSetDevice");
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else check_cuda(e, "cudaDeviceEnablePeerAccess");
+    check_cuda(cudaSetDevice(cur), "cudaSetDevice");
+  });
+}
+
 int fcdp_adam_grad_step(int64_t n, const fcdp_adam_config* c, float scale, int32_t num_segs,
                         const int64_t* elem_offsets, const void* const* grads, const int64_t* counts,
                         float* master, float* m, float* v, void* param, int32_t eb, float* keep_grad,

@@ -3,8 +3,12 @@
 #include "fcdp.h"
 #include "runtime/engine.hpp"
 
+#include <sys/mman.h>
+
 #include <chrono>
+#include <cstring>
 #include <thread>
+#include <vector>
 
 struct fcdp_engine {
   fcdp::Engine* impl;
@@ -118,6 +122,33 @@ int fcdp_engine_set_trace(fcdp_engine* e, int32_t on) { return guarded([&] { E(e
 
 int fcdp_engine_trace(fcdp_engine* e, float* begin_ms, float* end_ms, uint32_t capacity, uint32_t* count) {
   return guarded([&] { *count = E(e).trace(begin_ms, end_ms, capacity); });
+}
+
+int fcdp_numa_parse_cpulist(const char* list, int32_t* out, int32_t capacity, int32_t* count) {
+  return guarded([&] {
+    const std::vector<int> v = fcdp::parse_cpulist(list ? list : "");
+    *count = static_cast<int32_t>(v.size());
+    for (int32_t i = 0; i < capacity && i < static_cast<int32_t>(v.size()); ++i) out[i] = v[i];
+  });
+}
+
+int fcdp_numa_selftest(int32_t node, uint64_t bytes, int32_t* num_nodes, int32_t* cpus_in_node,
+                       int32_t* prefer_ok, int32_t* node_of_page, int32_t* affinity_restored) {
+  return guarded([&] {
+    *num_nodes = fcdp::numa_online_nodes();
+    *cpus_in_node = static_cast<int32_t>(fcdp::numa_node_cpus(node).size());
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) throw fcdp::OomError("numa selftest: mmap failed");
+    *prefer_ok = fcdp::numa_prefer(p, bytes, node) ? 1 : 0;
+    std::memset(p, 1, bytes);  // first touch under the policy
+    *node_of_page = fcdp::numa_node_of_page(p);
+    munmap(p, bytes);
+    const fcdp::SavedAffinity before = fcdp::numa_save_affinity();
+    fcdp::numa_pin_thread(node);
+    fcdp::numa_restore_affinity(before);
+    const fcdp::SavedAffinity after = fcdp::numa_save_affinity();
+    *affinity_restored = before.valid && after.valid && std::memcmp(before.set, after.set, sizeof(before.set)) == 0;
+  });
 }
 
 int fcdp_nic_selftest(const char* name, int32_t rank, int32_t nodes, int32_t local, double bw, uint64_t payload,
