@@ -342,12 +342,9 @@ struct RsArgs {
 };
 
 template <typename T, int kG>
-__device__ __forceinline__ void rs_emit(const RsArgs& a, const GradPtrs& g, std::int64_t c,
-                                        std::int64_t rel, float* own_out, uint4* wire_out) {
+__device__ __forceinline__ void rs_emit_q(const RsArgs& a, const uint4 (&q)[kG], std::int64_t rel,
+                                          float* own_out, uint4* wire_out) {
   constexpr int V = Vec<T>::kN;
-  uint4 q[kG];
-#pragma unroll
-  for (int i = 0; i < kG; ++i) q[i] = static_cast<const uint4*>(g.p[i])[c];
   float acc[V];
 #pragma unroll
   for (int e = 0; e < V; ++e) acc[e] = 0.0f;
@@ -365,11 +362,20 @@ __device__ __forceinline__ void rs_emit(const RsArgs& a, const GradPtrs& g, std:
         r.z = __fmul_rn(r.z, a.scale);
         r.w = __fmul_rn(r.w, a.scale);
       }
-      o[e / 4] = r;
+      __stcs(o + e / 4, r);
     }
   } else {
-    wire_out[rel] = Vec<T>::pack(acc);
+    __stcs(wire_out + rel, Vec<T>::pack(acc));
   }
+}
+
+template <typename T, int kG>
+__device__ __forceinline__ void rs_emit(const RsArgs& a, const GradPtrs& g, std::int64_t c,
+                                        std::int64_t rel, float* own_out, uint4* wire_out) {
+  uint4 q[kG];
+#pragma unroll
+  for (int i = 0; i < kG; ++i) q[i] = static_cast<const uint4*>(g.p[i])[c];
+  rs_emit_q<T, kG>(a, q, rel, own_out, wire_out);
 }
 
 template <typename T, int kG>
@@ -391,16 +397,25 @@ __global__ void __launch_bounds__(kThreads) rs_masked_kernel(LayoutDev L, GradPt
   }
 }
 
+// Dense slice: kU chunks per lane per trip with every one of the kU * g
+// gradient loads (local HBM or NVLink peer) issued before any add or store -
+// 8 independent 16-byte loads in flight per lane whatever g is (the loads of
+// chunk u+1 no longer wait behind chunk u's stores, which may alias them).
 template <typename T, int kG>
 __global__ void __launch_bounds__(kThreads) rs_dense_kernel(GradPtrs g, RsArgs a, float* __restrict__ own_out,
                                                             uint4* __restrict__ wire_out) {
+  constexpr int kU = kG >= 8 ? 1 : 8 / kG;
   const std::int64_t n = a.k1 - a.k0;
   const std::int64_t stride = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
   std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  // two chunks per lane per trip: 2*g independent 16-byte loads in flight
-  for (; i + stride < n; i += 2 * stride) {
-    rs_emit<T, kG>(a, g, a.k0 + i, i, own_out, wire_out);
-    rs_emit<T, kG>(a, g, a.k0 + i + stride, i + stride, own_out, wire_out);
+  for (; i + (kU - 1) * stride < n; i += kU * stride) {
+    uint4 q[kU][kG];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int k = 0; k < kG; ++k) q[u][k] = __ldcs(static_cast<const uint4*>(g.p[k]) + a.k0 + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) rs_emit_q<T, kG>(a, q[u], i + u * stride, own_out, wire_out);
   }
   for (; i < n; i += stride) rs_emit<T, kG>(a, g, a.k0 + i, i, own_out, wire_out);
 }
@@ -519,50 +534,70 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(std::int64_t n, AdamPara
 // so results are bit-identical to RS-then-AdamW; the fp32 gradient shard is
 // written only when asked (keep_grad: readback for tests), saving 8 B/param of
 // HBM traffic and the separate RS pass.  Chunks no segment covers have g = 0.
+// The launcher turns the caller's segments into a cover of the whole layer
+// (gaps become zero-gradient segments) and gives every segment a share of the
+// grid proportional to its size, so a block finds its segment once and then
+// streams it like adam_kernel: 4 elements per lane, 2 groups per trip.
+constexpr int kMaxCover = 2 * kMaxGradSegs + 1;
+struct AdamCover {
+  int n;
+  int block0[kMaxCover + 1];         // first block of each segment; block0[n] = grid
+  std::int64_t elem0[kMaxCover];     // first element of the segment in the layer
+  std::int64_t count[kMaxCover];     // elements (multiple of 4)
+  const void* src[kMaxCover];        // gradient (param dtype), nullptr: zero gradient
+};
+
 template <typename T>
-__global__ void __launch_bounds__(kThreads) adam_grad_kernel(std::int64_t chunks, GradSegs segs, AdamParams p,
-                                                             float scale, float* __restrict__ master,
-                                                             float* __restrict__ m, float* __restrict__ v,
-                                                             void* __restrict__ param, float* __restrict__ keep) {
-  constexpr int V = Vec<T>::kN;
+__device__ __forceinline__ float4 grad4(const void* src, std::int64_t i4) {
+  if (!src) return make_float4(0.f, 0.f, 0.f, 0.f);
+  return load4<T>(src, i4);
+}
+
+template <typename T>
+__device__ __forceinline__ void adam_grad4(const AdamParams& p, float omb1, float omb2, float scale, float4 g,
+                                           float4 w, float4 mm, float4 vv, std::int64_t e4, float* master, float* m,
+                                           float* v, void* param, float* keep) {
+  // g = (0 + x) * scale: exactly the rs_dense_kernel<T, 1> final-scale arithmetic
+  g = make_float4(__fmul_rn(__fadd_rn(0.0f, g.x), scale), __fmul_rn(__fadd_rn(0.0f, g.y), scale),
+                  __fmul_rn(__fadd_rn(0.0f, g.z), scale), __fmul_rn(__fadd_rn(0.0f, g.w), scale));
+  if (keep) __stcs(reinterpret_cast<float4*>(keep) + e4, g);
+  adam_one(p, omb1, omb2, g.x, w.x, mm.x, vv.x);
+  adam_one(p, omb1, omb2, g.y, w.y, mm.y, vv.y);
+  adam_one(p, omb1, omb2, g.z, w.z, mm.z, vv.z);
+  adam_one(p, omb1, omb2, g.w, w.w, mm.w, vv.w);
+  __stcs(reinterpret_cast<float4*>(master) + e4, w);
+  __stcs(reinterpret_cast<float4*>(m) + e4, mm);
+  __stcs(reinterpret_cast<float4*>(v) + e4, vv);
+  store4<T>(param, e4, w);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) adam_grad_kernel(AdamCover cv, AdamParams p, float scale,
+                                                             float* __restrict__ master, float* __restrict__ m,
+                                                             float* __restrict__ v, void* __restrict__ param,
+                                                             float* __restrict__ keep) {
+  int s = 0;
+  while (s + 1 < cv.n && static_cast<int>(blockIdx.x) >= cv.block0[s + 1]) ++s;
   const float omb1 = __fsub_rn(1.0f, p.beta1), omb2 = __fsub_rn(1.0f, p.beta2);
-  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  for (std::int64_t c = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < chunks; c += step) {
-    uint4 q = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll 1
-    for (int s = 0; s < segs.n; ++s)
-      if (c >= segs.dst_chunk[s] && c < segs.dst_chunk[s] + segs.nchunks[s]) {
-        q = __ldcs(static_cast<const uint4*>(segs.src[s]) + (c - segs.dst_chunk[s]));
-        break;
-      }
-    float g[V];
-#pragma unroll
-    for (int e = 0; e < V; ++e) g[e] = 0.0f;
-    Vec<T>::add(g, q);
-    float4* W4 = reinterpret_cast<float4*>(master) + c * (V / 4);
-    float4* M4 = reinterpret_cast<float4*>(m) + c * (V / 4);
-    float4* V4 = reinterpret_cast<float4*>(v) + c * (V / 4);
-    float4 w[V / 4], mm[V / 4], vv[V / 4];
-#pragma unroll
-    for (int k = 0; k < V / 4; ++k) {
-      w[k] = __ldcs(W4 + k);
-      mm[k] = __ldcs(M4 + k);
-      vv[k] = __ldcs(V4 + k);
-    }
-#pragma unroll
-    for (int k = 0; k < V / 4; ++k) {
-      const float4 gk = make_float4(__fmul_rn(g[4 * k], scale), __fmul_rn(g[4 * k + 1], scale),
-                                    __fmul_rn(g[4 * k + 2], scale), __fmul_rn(g[4 * k + 3], scale));
-      if (keep) __stcs(reinterpret_cast<float4*>(keep) + c * (V / 4) + k, gk);
-      adam_one(p, omb1, omb2, gk.x, w[k].x, mm[k].x, vv[k].x);
-      adam_one(p, omb1, omb2, gk.y, w[k].y, mm[k].y, vv[k].y);
-      adam_one(p, omb1, omb2, gk.z, w[k].z, mm[k].z, vv[k].z);
-      adam_one(p, omb1, omb2, gk.w, w[k].w, mm[k].w, vv[k].w);
-      __stcs(W4 + k, w[k]);
-      __stcs(M4 + k, mm[k]);
-      __stcs(V4 + k, vv[k]);
-      store4<T>(param, c * (V / 4) + k, w[k]);
-    }
+  const std::int64_t groups = cv.count[s] / 4, base4 = cv.elem0[s] / 4;
+  const void* src = cv.src[s];
+  const std::int64_t step = static_cast<std::int64_t>(cv.block0[s + 1] - cv.block0[s]) * blockDim.x;
+  std::int64_t i = static_cast<std::int64_t>(blockIdx.x - cv.block0[s]) * blockDim.x + threadIdx.x;
+  const float4* W4 = reinterpret_cast<const float4*>(master);
+  const float4* M4 = reinterpret_cast<const float4*>(m);
+  const float4* V4 = reinterpret_cast<const float4*>(v);
+  for (; i + step < groups; i += 2 * step) {
+    const std::int64_t a = base4 + i, b = base4 + i + step;
+    const float4 ga = grad4<T>(src, i), gb = grad4<T>(src, i + step);
+    const float4 wa = __ldcs(W4 + a), ma = __ldcs(M4 + a), va = __ldcs(V4 + a);
+    const float4 wb = __ldcs(W4 + b), mb = __ldcs(M4 + b), vb = __ldcs(V4 + b);
+    adam_grad4<T>(p, omb1, omb2, scale, ga, wa, ma, va, a, master, m, v, param, keep);
+    adam_grad4<T>(p, omb1, omb2, scale, gb, wb, mb, vb, b, master, m, v, param, keep);
+  }
+  for (; i < groups; i += step) {
+    const std::int64_t a = base4 + i;
+    adam_grad4<T>(p, omb1, omb2, scale, grad4<T>(src, i), __ldcs(W4 + a), __ldcs(M4 + a), __ldcs(V4 + a), a, master,
+                  m, v, param, keep);
   }
 }
 
@@ -708,7 +743,8 @@ cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n
   const bool bf16 = L.dev.elem_bytes == 2;
   const bool dense = L.dense_trainable();
   const std::int64_t wb = dense ? 0 : L.rs_word_begin[j], we = dense ? 0 : L.rs_word_end[j];
-  const int grid = dense ? grid_for(a.k1 - a.k0, kThreads * 2) : grid_for((we - wb) * 32, kThreads);
+  const int grid = dense ? grid_for(a.k1 - a.k0, kThreads * std::max(1, 8 / L.dev.local))
+                         : grid_for((we - wb) * 32, kThreads);
   auto go = [&](auto tag_t, auto tag_g) {
     using T = decltype(tag_t);
     constexpr int G = decltype(tag_g)::value;
@@ -767,13 +803,37 @@ cudaError_t launch_adam_grad(std::int64_t chunks, const GradSegs& segs, const Ad
                              cudaStream_t s) {
   if (chunks <= 0) return cudaSuccess;
   if (segs.n < 0 || segs.n > kMaxGradSegs) return cudaErrorInvalidValue;
-  for (int i = 0; i < segs.n; ++i)
+  const std::int64_t V = kChunkBytes / param_elem_bytes;
+  AdamCover cv{};
+  std::int64_t at = 0;  // chunks covered so far
+  auto push = [&](std::int64_t c0, std::int64_t nc, const void* src) {
+    if (nc <= 0) return;
+    cv.elem0[cv.n] = c0 * V;
+    cv.count[cv.n] = nc * V;
+    cv.src[cv.n] = src;
+    ++cv.n;
+  };
+  for (int i = 0; i < segs.n; ++i) {
     if (reinterpret_cast<std::uintptr_t>(segs.src[i]) % 16) return cudaErrorMisalignedAddress;
-  const int grid = grid_for(chunks, kThreads);
+    if (segs.dst_chunk[i] < at || segs.dst_chunk[i] + segs.nchunks[i] > chunks) return cudaErrorInvalidValue;
+    push(at, segs.dst_chunk[i] - at, nullptr);  // gap: zero gradient
+    push(segs.dst_chunk[i], segs.nchunks[i], segs.src[i]);
+    at = segs.dst_chunk[i] + segs.nchunks[i];
+  }
+  push(at, chunks - at, nullptr);
+  // grid shares proportional to segment size (at least one block each)
+  const int total = grid_for(chunks * V / 4, kThreads * 2);
+  int b = 0;
+  for (int i = 0; i < cv.n; ++i) {
+    cv.block0[i] = b;
+    const std::int64_t share = (cv.count[i] * total + chunks * V - 1) / (chunks * V);
+    b += static_cast<int>(std::max<std::int64_t>(1, share));
+  }
+  cv.block0[cv.n] = b;
   if (param_elem_bytes == 2)
-    adam_grad_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(chunks, segs, p, scale, master, m, v, param, keep_grad);
+    adam_grad_kernel<__nv_bfloat16><<<b, kThreads, 0, s>>>(cv, p, scale, master, m, v, param, keep_grad);
   else
-    adam_grad_kernel<float><<<grid, kThreads, 0, s>>>(chunks, segs, p, scale, master, m, v, param, keep_grad);
+    adam_grad_kernel<float><<<b, kThreads, 0, s>>>(cv, p, scale, master, m, v, param, keep_grad);
   return cudaGetLastError();
 }
 

@@ -197,6 +197,15 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   CK(cudaStreamCreateWithPriority(&s_agsend_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_rssend_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_rsrecv_, cudaStreamNonBlocking, hi));
+  // G = 1 fused RS + AdamW: a memory-bound update beside the backward GEMMs; at
+  // the compute stream's (low) priority it fills the gaps between the model's
+  // kernels instead of pre-empting them (FCDP_OPT_PRIO=high keeps it on s_rs_)
+  CK(cudaStreamCreateWithPriority(&s_opt_, cudaStreamNonBlocking, lo));
+  CK(cudaEventCreateWithFlags(&opt_fork_, cudaEventDisableTiming));
+  {
+    const char* e = std::getenv("FCDP_OPT_PRIO");
+    opt_low_ = !(e && std::strcmp(e, "high") == 0);
+  }
   for (auto& e : fin_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_staged_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -244,8 +253,9 @@ Engine::~Engine() {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : fin_done_)
     if (e) cudaEventDestroy(e);
-  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_})
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_, s_opt_})
     if (s) cudaStreamDestroy(s);
+  if (opt_fork_) cudaEventDestroy(opt_fork_);
   for (void* p : {static_cast<void*>(param_t_), static_cast<void*>(param_f_), static_cast<void*>(master_),
                   static_cast<void*>(adam_m_), static_cast<void*>(adam_v_), static_cast<void*>(grad32_),
                   static_cast<void*>(w_slots_[0]), static_cast<void*>(w_slots_[1]),
@@ -262,6 +272,8 @@ Engine::~Engine() {
   for (auto& ev : cache_staged_)
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : ag_staged_)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : d2h_done_)
     if (ev) cudaEventDestroy(ev);
   for (int nn = 0; nn < kMaxNodes; ++nn)
     if (hc_peer_[nn]) {
@@ -405,6 +417,13 @@ void Engine::allocate() {
   prev_retained_.assign(L, 0);
   grad_segs_.assign(L, GradSegs{});
   grad_segs_set_.assign(L, 0);
+  d2h_done_.assign(L, nullptr);
+  for (auto& ev : d2h_done_) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  d2h_done_valid_.assign(L, 0);
+  {
+    const char* e = std::getenv("FCDP_DEFER_D2H");
+    defer_d2h_ = !(e && std::strcmp(e, "0") == 0);
+  }
 }
 
 void Engine::exchange_handles() {
@@ -723,9 +742,13 @@ unsigned char* Engine::alias_ptr(int li) const {
   return l.has_t ? param_t_ + l.off_t * kChunkBytes : param_f_ + l.off_f * kChunkBytes;
 }
 
-void Engine::fence_alias_reads(cudaStream_t s) {
+void Engine::fence_alias_reads(cudaStream_t s, int layer) {
   // FCDP-Cache D2H of an aliased layer reads the shard that AdamW rewrites
   if (!alias_used_) return;
+  if (layer >= 0) {  // only that layer's store reads that layer's shard
+    if (d2h_done_valid_[layer]) CK(cudaStreamWaitEvent(s, d2h_done_[layer], 0));
+    return;
+  }
   CK(cudaEventRecord(alias_fence_, s_cache_));
   CK(cudaStreamWaitEvent(s, alias_fence_, 0));
 }
@@ -942,13 +965,10 @@ void Engine::ev_ag_intra(const Event& e, bool backward) {
   pending_h2d_[e.layer] = {};
 }
 
-void Engine::ev_d2h(const Event& e) {
-  LayerRt& l = layers_[e.layer];
-  const bool wt = wants_t(e.param_set) && l.has_t, wf = wants_f(e.param_set) && l.has_f;
+void Engine::store_d2h(int layer, bool wt, bool wf, int slot_t, int slot_f) {
+  LayerRt& l = layers_[layer];
   const std::size_t C = kChunkBytes;
   unsigned char* H = host_cache_ + l.host_off * C;
-  std::uint64_t bytes = 0;
-  int slot_t = -1, slot_f = -1;
   // Copy slice j of a portion from X to the host cache; when this GPU's own
   // shard was staged there already (write-once staging), only the peers' shards.
   auto store = [&](bool frozen, int slot) {
@@ -956,7 +976,7 @@ void Engine::ev_d2h(const Event& e) {
     const std::size_t base = frozen ? l.L.dev.slice_t * C : 0;
     const unsigned char* Xs = slot == kAliasX ? (frozen ? param_f_ + l.off_f * C : param_t_ + l.off_t * C)
                                               : x_slot(j_, slot) + base;
-    const bool own_staged = frozen ? cache_stage_f_[e.layer] : cache_stage_t_[e.layer];
+    const bool own_staged = frozen ? cache_stage_f_[layer] : cache_stage_t_[layer];
     if (!own_staged || N_ == 1) {
       const std::int64_t real = frozen ? l.slice_real_f : l.slice_real_t;
       const std::size_t b = static_cast<std::size_t>(real) * C;
@@ -973,13 +993,26 @@ void Engine::ev_d2h(const Event& e) {
         }, static_cast<std::uint64_t>(real) * C);
     }
   };
-  const bool staged_any = (wt && cache_stage_t_[e.layer]) || (wf && cache_stage_f_[e.layer]);
-  if (staged_any && N_ > 1) CK(cudaStreamWaitEvent(s_cache_, cache_staged_[e.layer], 0));
+  const bool staged_any = (wt && cache_stage_t_[layer]) || (wf && cache_stage_f_[layer]);
+  if (staged_any && N_ > 1) CK(cudaStreamWaitEvent(s_cache_, cache_staged_[layer], 0));
+  if (wt) store(false, slot_t);
+  if (wf) store(true, slot_f);
+  for (int sl : {slot_t, slot_f})
+    if (sl >= 0) CK(cudaEventRecord(x_reader_[sl], s_cache_));
+  CK(cudaEventRecord(d2h_done_[layer], s_cache_));
+  d2h_done_valid_[layer] = 1;
+}
+
+void Engine::ev_d2h(const Event& e) {
+  LayerRt& l = layers_[e.layer];
+  const bool wt = wants_t(e.param_set) && l.has_t, wf = wants_f(e.param_set) && l.has_f;
+  const std::size_t C = kChunkBytes;
+  int slot_t = -1, slot_f = -1;
+  std::uint64_t bytes = 0;
   if (wt) {
     slot_t = x_of_t_[e.layer];
     if (slot_t < 0 && slot_t != kAliasX)
       throw shardsim::ProtocolError("d2h of a trainable portion that was not gathered");
-    store(false, slot_t);
     bytes += l.slice_real_t * C;
     l.host_version_t = static_cast<std::int64_t>(l.shard_version_t);
   }
@@ -987,13 +1020,36 @@ void Engine::ev_d2h(const Event& e) {
     slot_f = x_of_f_[e.layer];
     if (slot_f < 0 && slot_f != kAliasX)
       throw shardsim::ProtocolError("d2h of a frozen portion that was not gathered");
-    store(true, slot_f);
     bytes += l.slice_real_f * C;
     l.host_version_f = 0;
   }
-  for (int sl : {slot_t, slot_f})
-    if (sl >= 0) CK(cudaEventRecord(x_reader_[sl], s_cache_));
   shm_->add(rank_, kCacheD2H, bytes);
+  // One GPU, layer read in place (alias): the store's source is the shard,
+  // which only this layer's own update rewrites, after its backward reload.
+  // The backward needs the stores last-layer-first, while the program emits
+  // them in forward order behind each ComputeFwd (schedule.cpp:209-223); on
+  // one copy stream that puts the last layer's store - the first the backward
+  // reloads - behind every other (about 50 ms of PCIe for GPT-2 1.3B).  So the
+  // stores are queued and issued in reverse at the forward->backward turn (or
+  // as soon as anything depends on one): same bytes, same deps, LIFO order.
+  const bool alias_src = (!wt || slot_t == kAliasX) && (!wf || slot_f == kAliasX);
+  if (defer_d2h_ && G_ == 1 && alias_src) {
+    deferred_d2h_.push_back({e.id, e.layer, wt, wf});
+    d2h_deferred_id_[e.id] = 1;
+    return;
+  }
+  store_d2h(e.layer, wt, wf, slot_t, slot_f);
+}
+
+void Engine::flush_deferred_d2h() {
+  for (auto it = deferred_d2h_.rbegin(); it != deferred_d2h_.rend(); ++it) {
+    if (trace_) CK(cudaEventRecord(trace_begin_[it->id], s_cache_));
+    store_d2h(it->layer, it->t, it->f, it->t ? kAliasX : -1, it->f ? kAliasX : -1);
+    CK(cudaEventRecord(ev_done_[it->id], s_cache_));  // dependents enqueued from now on wait for the copy
+    if (trace_) CK(cudaEventRecord(trace_end_[it->id], s_cache_));
+    d2h_deferred_id_[it->id] = 0;
+  }
+  deferred_d2h_.clear();
 }
 
 void Engine::ev_compute(const Event& e, bool backward) {
@@ -1068,7 +1124,13 @@ void Engine::ev_reduce_scatter(const Event& e) {
   if (fused_grad_ok(li)) {
     // G = 1: the RS is the identity up to widen + scale; fused into AdamW,
     // reading the gradient where backward left it (the slot or the segments)
-    fence_alias_reads(s);
+    if (opt_low_) {
+      CK(cudaEventRecord(opt_fork_, s));
+      s = s_opt_;
+      CK(cudaStreamWaitEvent(s, opt_fork_, 0));
+      done_s_ = s;
+    }
+    fence_alias_reads(s, li);
     const std::int64_t n = l.L.dev.shard_t * V_;
     const std::size_t o = static_cast<std::size_t>(l.off_t) * V_;
     const AdamParams p = adam_params(opt_steps_ + 1);
@@ -1225,7 +1287,7 @@ void Engine::adam_layer(int li, cudaStream_t s) {
   const AdamParams p = adam_params(opt_steps_ + 1);  // the step the program's OptimizerStep will complete
   // the own shard must have left for the NIC before it is overwritten
   if (ag_staged_valid_[li]) CK(cudaStreamWaitEvent(s, ag_staged_[li], 0));
-  fence_alias_reads(s);
+  fence_alias_reads(s, li);
   const std::int64_t n = l.L.dev.shard_t * V_;
   const std::size_t o = static_cast<std::size_t>(l.off_t) * V_;
   timed(3, s, static_cast<std::uint64_t>(n) * (7 * sizeof(float) + eb_), [&] {
@@ -1375,7 +1437,7 @@ void Engine::begin(const shardsim::EventProgram& prog) {
     if (e.kind == EventKind::ComputeFwd) last_fwd_ = e.id;
   }
   next_event_ = 0;
-  for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_})
+  for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_, s_opt_})
     CK(cudaStreamWaitEvent(s, iter_done_, 0));
   if (trace_) {
     auto grow = [&](std::vector<cudaEvent_t>& v) {
@@ -1389,7 +1451,7 @@ void Engine::begin(const shardsim::EventProgram& prog) {
     grow(trace_end_);
     if (!trace_start_) CK(cudaEventCreate(&trace_start_));
     CK(cudaEventRecord(trace_start_, s_comp_));
-    for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_})
+    for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_, s_opt_})
       CK(cudaStreamWaitEvent(s, trace_start_, 0));
     traced_events_ = static_cast<std::uint32_t>(n_ev);
   } else {
@@ -1412,6 +1474,9 @@ void Engine::begin(const shardsim::EventProgram& prog) {
     has_opt_ = has_opt;
   }
   std::fill(cache_stage_f_.begin(), cache_stage_f_.end(), 0);
+  deferred_d2h_.clear();
+  d2h_deferred_id_.assign(n_ev, 0);
+  std::fill(d2h_done_valid_.begin(), d2h_done_valid_.end(), 0);
   if (shared_cache_)
     for (const Event& e : prog.events)
       if (e.kind == EventKind::D2H) {  // every D2H stores a forward-gathered layer
@@ -1437,6 +1502,11 @@ void Engine::exec(std::uint32_t event_id) {
     if (debug)
       std::fprintf(stderr, "[fcdp r%d] it=%llu enqueue ev %u %s layer %d\n", rank_,
                    static_cast<unsigned long long>(prog.iteration_index), e.id, shardsim::to_string(e.kind), e.layer);
+    if (!deferred_d2h_.empty()) {
+      bool flush = e.id > last_fwd;  // the forward->backward turn
+      for (shardsim::EventId d : e.deps) flush |= d2h_deferred_id_[d] != 0;
+      if (flush) flush_deferred_d2h();
+    }
     for (shardsim::EventId d : e.deps)
       if (stream_of[d] != s) CK(cudaStreamWaitEvent(s, ev_done_[d], 0));
     // (the staging side s_agsend_ needs none of the program's deps: its source,
@@ -1466,8 +1536,10 @@ void Engine::exec(std::uint32_t event_id) {
     const cudaStream_t ds = done_s_ ? done_s_ : s;
     done_s_ = nullptr;
     stream_of[e.id] = ds;
-    CK(cudaEventRecord(ev_done_[e.id], ds));
-    if (trace_) CK(cudaEventRecord(trace_end_[e.id], ds));
+    if (!d2h_deferred_id_[e.id]) {  // a deferred store records these when it is issued
+      CK(cudaEventRecord(ev_done_[e.id], ds));
+      if (trace_) CK(cudaEventRecord(trace_end_[e.id], ds));
+    }
   }
   ++next_event_;
 }
@@ -1478,9 +1550,10 @@ void Engine::end(std::vector<shardsim::ParamState>& states) {
   if (next_event_ != prog.events.size())
     throw shardsim::ProtocolError("engine: end after " + std::to_string(next_event_) + " of " +
                                   std::to_string(prog.events.size()) + " events");
+  if (!deferred_d2h_.empty()) flush_deferred_d2h();
   // join: the next iteration starts after everything of this one
-  const cudaStream_t side[6] = {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_};
-  for (int i = 0; i < 6; ++i) {
+  const cudaStream_t side[7] = {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_, s_opt_};
+  for (int i = 0; i < 7; ++i) {
     CK(cudaEventRecord(join_[i], side[i]));
     CK(cudaStreamWaitEvent(s_comp_, join_[i], 0));
   }
@@ -1510,7 +1583,7 @@ void Engine::sync() {
   // Poll instead of blocking so a cross-rank wait that can never be satisfied
   // (a peer died, a protocol bug) ends in a diagnosable TimeoutError.
   const auto deadline = std::chrono::steady_clock::now() + std::chrono::duration<double>(cfg_.timeout_s);
-  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_}) {
+  for (cudaStream_t s : {s_comp_, s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_, s_opt_}) {
     if (!s) continue;
     for (int spin = 0;; ++spin) {
       const cudaError_t q = cudaStreamQuery(s);

@@ -214,7 +214,10 @@ class Engine {
   std::vector<cudaEvent_t> x_reader_;  // last local reader of each X slot
   cudaEvent_t rs_done_[2] = {nullptr, nullptr};
   cudaEvent_t iter_done_ = nullptr;
-  cudaEvent_t join_[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t join_[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t s_opt_ = nullptr;   // G = 1 fused RS + AdamW (low priority by default)
+  cudaEvent_t opt_fork_ = nullptr;
+  bool opt_low_ = true;
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, u_ = 0;
@@ -245,7 +248,22 @@ class Engine {
   cudaEvent_t alias_fence_ = nullptr;
   bool alias_gather(const shardsim::Event& e, bool wt, bool wf);
   unsigned char* alias_ptr(int li) const;
-  void fence_alias_reads(cudaStream_t s);
+  void fence_alias_reads(cudaStream_t s, int layer = -1);
+  // G = 1: FCDP-Cache stores read the shard itself, which nothing overwrites
+  // before that layer's update in the backward; they are queued and issued
+  // last-layer-first at the forward->backward turn (see ev_d2h).
+  struct DeferredD2H {
+    std::uint32_t id;
+    int layer;
+    bool t, f;
+  };
+  std::vector<DeferredD2H> deferred_d2h_;
+  std::vector<char> d2h_deferred_id_;       // per event id of the current program
+  std::vector<cudaEvent_t> d2h_done_;       // per layer: its FCDP-Cache store finished (this iteration)
+  std::vector<char> d2h_done_valid_;
+  bool defer_d2h_ = true;
+  void store_d2h(int layer, bool wt, bool wf, int slot_t, int slot_f);
+  void flush_deferred_d2h();
 
   // per-iteration bookkeeping
   struct PendingSlice {

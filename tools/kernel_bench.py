@@ -91,11 +91,27 @@ def main():
     wire = torch.empty(E, dtype=torch.bfloat16, device=dev)
     timeit("rs_dense_g1_final", lambda: _capi.check(lib.fcdp_rs_slice(
         dense, (C.c_void_p * 1)(G.data_ptr()), 0, 0, 1.0, 1, P(own), P(wire), None)), E * 2 + E * 4)
-    Gs = [G] + [torch.randn(E, device=dev).to(torch.bfloat16) for _ in range(3)]
-    d4b = layout(np.ones(chunks, np.uint8), 2, 1, 4)
-    timeit("rs_dense_g4_local", lambda: _capi.check(lib.fcdp_rs_slice(
-        d4b, (C.c_void_p * 4)(*[x.data_ptr() for x in Gs]), 1, 0, 0.25, 1, P(own), P(wire), None)),
-        4 * (E // 4) * 2 + (E // 4) * 4)
+    Gs = [G] + [torch.randn(E, device=dev).to(torch.bfloat16) for _ in range(7)]
+    for gg in (2, 4, 8):
+        dgb = layout(np.ones(chunks, np.uint8), 2, 1, gg)
+        timeit(f"rs_dense_g{gg}_local", lambda: _capi.check(lib.fcdp_rs_slice(
+            dgb, (C.c_void_p * gg)(*[x.data_ptr() for x in Gs[:gg]]), 1, 0, 1.0 / gg, 1, P(own), P(wire), None)),
+            gg * (E // gg) * 2 + (E // gg) * 4)
+    # 2 x 1 (N = 2): own half fp32, the other half to the wire in bf16
+    d21 = layout(np.ones(chunks, np.uint8), 2, 2, 1)
+    timeit("rs_dense_2x1_wire", lambda: _capi.check(lib.fcdp_rs_slice(
+        d21, (C.c_void_p * 1)(G.data_ptr()), 0, 0, 0.5, 0, P(own), P(wire), None)), E * 2 + (E // 2) * 4 + (E // 2) * 2)
+    # --- G = 1 fused RS + AdamW of one GPT-2 1.3B block (the engine's one-GPU launch)
+    wl, ml, vl = torch.randn(E, device=dev), torch.zeros(E, device=dev), torch.zeros(E, device=dev)
+    pl = torch.empty(E, dtype=torch.bfloat16, device=dev)
+    cfg1 = _capi.AdamConfig(1e-4, 0.9, 0.95, 1e-8, 0.0, 1)
+    offs, cnts, ptrs = (C.c_int64 * 1)(0), (C.c_int64 * 1)(E), (C.c_void_p * 1)(G.data_ptr())
+    timeit("adamw_fused_grad_block", lambda: _capi.check(lib.fcdp_adam_grad_step(
+        E, C.byref(cfg1), 1.0, 1, offs, ptrs, cnts, P(wl), P(ml), P(vl), P(pl), 2, None, None)), E * 28)
+    wl2 = torch.randn(E, device=dev)
+    g32 = torch.randn(E, device=dev)
+    timeit("adamw_block", lambda: _capi.check(lib.fcdp_adam_step(E, C.byref(cfg1), P(wl2), P(ml), P(vl), P(g32), P(pl),
+                                                                 2, None)), E * 30)
     # --- inter-node finalize, N = 2
     n = E // 2
     timeit("rs_finalize_N2", lambda: _capi.check(lib.fcdp_rs_finalize(n, 2, 0, 2, P(own), P(wire), n, 0.5, P(own), None)),

@@ -58,7 +58,8 @@ def main():
 
     nbytes = a.mb << 20
     # (1) copy-engine peer read, both directions measured separately
-    src1 = torch.empty(nbytes, dtype=torch.uint8, device=d1)
+    src1 = torch.zeros(nbytes, dtype=torch.uint8, device=d1)
+    torch.cuda.synchronize(d1)
     dst0 = torch.empty(nbytes, dtype=torch.uint8, device=d0)
     ms = timeit(lambda: dst0.copy_(src1, non_blocking=True))
     res["peer_copy_1to0_GBps"] = nbytes / (ms / 1e3) / 1e9
@@ -87,6 +88,8 @@ def main():
         # correctness: gathered = concat of the slices
         for j, t in enumerate(slices):
             t.fill_(j + 1)
+        torch.cuda.synchronize(d1)
+        torch.cuda.synchronize(d0)
         fn()
         torch.cuda.synchronize()
         got = out.view(g, per)[:, ::4096].cpu()
@@ -102,6 +105,7 @@ def main():
         lay = C.c_void_p()
         _capi.check(lib.fcdp_layout_create(chunks, mask.ctypes.data_as(C.POINTER(C.c_uint8)), 2, 1, g, C.byref(lay)))
         grads = [torch.randn(chunks * 8, device=d0 if j == 0 else d1).to(torch.bfloat16) for j in range(g)]
+        torch.cuda.synchronize(d1)
         gp = (C.c_void_p * g)(*[t.data_ptr() for t in grads])
         slice_chunks = chunks // g
         own = torch.empty(slice_chunks * 8, dtype=torch.float32, device=d0)
@@ -113,6 +117,8 @@ def main():
                            "hbm_bytes": slice_chunks * 16 + slice_chunks * 8 * 4}
         # correctness vs torch on GPU0
         ref = sum(t[:slice_chunks * 8].to(d0).float() for t in grads) * (1.0 / g)
+        torch.cuda.synchronize(d1)
+        torch.cuda.synchronize(d0)
         fn()
         torch.cuda.synchronize()
         assert torch.allclose(own, ref, rtol=1e-6, atol=1e-6), "rs mismatch"
