@@ -131,6 +131,18 @@ def measured_peaks():
         return {}
 
 
+def nvlink_peak():
+    """Measured NVLink peer-copy rate per direction on this pool's B200s
+    (tools/nvlink_probe.py, profiles/r02_nvlink_probe.json), with its source."""
+    try:
+        d = json.loads((ROOT / "profiles" / "r02_nvlink_probe.json").read_text())
+        return float(d["nvlink_peak_GBps_measured"]), ("profiles/r02_nvlink_probe.json: measured copy-engine peer copy "
+                                                        "GPU1->GPU0 (tools/nvlink_probe.py); the gather / RS kernels reach "
+                                                        "0.99-1.00 of it alone")
+    except Exception:
+        return 770.0, "B200_PROFILING.md peer copy 770 GB/s per direction (fallback: no committed probe)"
+
+
 def ncu_traffic(kernel_class: str):
     """dram bytes per launch from the committed ncu --set full summary, if any."""
     try:
@@ -572,15 +584,17 @@ def main():
         # an intra-node gather / pull-reduce: bounded by NVLink ingress, not HBM
         link_per_launch = d["link_bytes"] / max(d["launches"], 1)
         achieved = link_per_launch / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else None
-        peak, unit_peak, src = 770.0, "GB/s", ("B200_PROFILING.md measured NVLink peer copy, 770 GB/s per direction "
-                                               "(900 nominal); achieved = NVLink ingress bytes / launch time")
+        pk, why = nvlink_peak()
+        peak, unit_peak, src = pk, "GB/s", why + "; achieved = NVLink ingress bytes / launch time"
     else:
         achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else None
         peak, unit_peak, src = hbm, "GB/s", "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     roofline = {"bound": "nvlink" if nvlink_bound else "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": unit_peak, "frac": (achieved / peak) if (achieved and peak) else None,
                 # the committed ncu capture is the default N=1 GPT-2 run; other configs have other launch sizes
-                "traffic": ncu_traffic(dom) if (not nvlink_bound and world == 1 and args.preset == "gpt2-1.3b") else None, "alg_bytes_per_launch": per_launch_bytes,
+                "traffic": (ncu_traffic("adamw_fused_rs" if (dom == "adamw" and world == 1) else dom)
+                            if (not nvlink_bound and world == 1 and args.preset == "gpt2-1.3b") else None),
+                "alg_bytes_per_launch": per_launch_bytes,
                 "ms_per_launch": per_launch_ms, "peak_source": src,
                 "share_of_step": d["ms"] / main_run["ms"] if main_run["ms"] else None,
                 # north_star's nominal denominators (B200: ~8 TB/s HBM3e, 900 GB/s NVLink per direction)

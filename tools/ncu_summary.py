@@ -13,8 +13,10 @@ import subprocess
 import sys
 from collections import defaultdict
 
-CLASSES = [("adamw", r"adam_kernel"), ("rs_finalize", r"rs_finalize_kernel"), ("rs_slice", r"rs_(dense|masked)_kernel"),
-           ("gather_expand", r"(expand_kernel|concat_kernel|copy_kernel)"), ("partition", r"partition_kernel")]
+CLASSES = [("adamw_fused_rs", r"adam_grad_kernel"), ("adamw", r"adam_kernel"), ("rs_finalize", r"rs_finalize_kernel"),
+           ("rs_slice", r"rs_(dense|masked)_kernel"),
+           ("gather_expand", r"(expand_kernel|concat_kernel|copy_kernel|bulk_copy_kernel)"),
+           ("partition", r"partition_kernel"), ("fcdp_setup", r"(init_kernel|widen_kernel)")]
 
 
 def klass(name):
@@ -96,7 +98,7 @@ def summarise_launches(path):
         unit = d.get("Metric Unit", "")
         scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(unit, 1e-6)
         name = d["Kernel Name"]
-        key = klass(name) or ("torch/cublas:" + name[:60])
+        key = klass(name) or (("fcdp:" if "fcdp::" in name else "torch/cublas:") + name[:60])
         tot[key] += v * scale
         cnt[key] += 1
     all_ms = sum(tot.values())
