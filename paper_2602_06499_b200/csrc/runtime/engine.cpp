@@ -197,14 +197,15 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   CK(cudaStreamCreateWithPriority(&s_agsend_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_rssend_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_rsrecv_, cudaStreamNonBlocking, hi));
-  // G = 1 fused RS + AdamW: a memory-bound update beside the backward GEMMs; at
-  // the compute stream's (low) priority it fills the gaps between the model's
-  // kernels instead of pre-empting them (FCDP_OPT_PRIO=high keeps it on s_rs_)
+  // G = 1 fused RS + AdamW runs on s_rs_ (high priority: its CTAs are placed
+  // ahead of the backward GEMMs', measured equal step time and a better live
+  // rate than the low-priority stream).  FCDP_OPT_PRIO=low moves it to s_opt_,
+  // at the compute stream's priority.
   CK(cudaStreamCreateWithPriority(&s_opt_, cudaStreamNonBlocking, lo));
   CK(cudaEventCreateWithFlags(&opt_fork_, cudaEventDisableTiming));
   {
     const char* e = std::getenv("FCDP_OPT_PRIO");
-    opt_low_ = !(e && std::strcmp(e, "high") == 0);
+    opt_low_ = e && std::strcmp(e, "low") == 0;
   }
   for (auto& e : fin_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1503,7 +1504,10 @@ void Engine::exec(std::uint32_t event_id) {
       std::fprintf(stderr, "[fcdp r%d] it=%llu enqueue ev %u %s layer %d\n", rank_,
                    static_cast<unsigned long long>(prog.iteration_index), e.id, shardsim::to_string(e.kind), e.layer);
     if (!deferred_d2h_.empty()) {
-      bool flush = e.id > last_fwd;  // the forward->backward turn
+      // the forward->backward turn: the first backward event that is not itself
+      // one of the forward's cache stores (the last layer's D2H follows the last
+      // ComputeFwd and must be the first store issued)
+      bool flush = e.id > last_fwd && e.kind != EventKind::D2H;
       for (shardsim::EventId d : e.deps) flush |= d2h_deferred_id_[d] != 0;
       if (flush) flush_deferred_d2h();
     }

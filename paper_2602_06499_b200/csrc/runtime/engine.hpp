@@ -215,9 +215,9 @@ class Engine {
   cudaEvent_t rs_done_[2] = {nullptr, nullptr};
   cudaEvent_t iter_done_ = nullptr;
   cudaEvent_t join_[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  cudaStream_t s_opt_ = nullptr;   // G = 1 fused RS + AdamW (low priority by default)
+  cudaStream_t s_opt_ = nullptr;   // G = 1 fused RS + AdamW when FCDP_OPT_PRIO=low
   cudaEvent_t opt_fork_ = nullptr;
-  bool opt_low_ = true;
+  bool opt_low_ = false;
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, u_ = 0;

@@ -19,7 +19,15 @@ CLASSES = [("adamw_fused_rs", r"adam_grad_kernel"), ("adamw", r"adam_kernel"), (
            ("partition", r"partition_kernel"), ("fcdp_setup", r"(init_kernel|widen_kernel)")]
 
 
+def ours(name):
+    """A kernel of libfcdp: namespace fcdp::(anonymous); ncu prints it either as
+    "fcdp::<unnamed>::k" or, shortened, "unnamed>::k" at the start of the name."""
+    return "fcdp::" in name or re.match(r"^(void )?unnamed>::", name) is not None
+
+
 def klass(name):
+    if not ours(name):
+        return None
     for c, pat in CLASSES:
         if re.search(pat, name):
             return c
@@ -98,7 +106,7 @@ def summarise_launches(path):
         unit = d.get("Metric Unit", "")
         scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(unit, 1e-6)
         name = d["Kernel Name"]
-        key = klass(name) or (("fcdp:" if "fcdp::" in name else "torch/cublas:") + name[:60])
+        key = klass(name) or (("fcdp:" if ours(name) else "torch/cublas:") + name[:60])
         tot[key] += v * scale
         cnt[key] += 1
     all_ms = sum(tot.values())
