@@ -161,11 +161,12 @@ def _views(flat, ldef: LayerDef):
 
 
 def _rope(x, base=10000.0):
+    """Rotary embedding of x [b, s, nh, d] (rotated pairs (0,1), (2,3), ...)."""
     import torch
-    b, nh, s, d = x.shape
+    b, s, nh, d = x.shape
     pos = torch.arange(s, device=x.device, dtype=torch.float32)
     inv = base ** (-torch.arange(0, d, 2, device=x.device, dtype=torch.float32) / d)
-    ang = pos[:, None] * inv[None, :]
+    ang = (pos[:, None] * inv[None, :])[:, None, :]  # [s, 1, d/2]: broadcast over heads
     cos, sin = ang.cos().to(x.dtype), ang.sin().to(x.dtype)
     x1, x2 = x[..., 0::2], x[..., 1::2]
     out = torch.stack((x1 * cos - x2 * sin, x1 * sin + x2 * cos), dim=-1)
@@ -185,8 +186,11 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
     if ldef.kind == "gpt2_block":
         b, s, _ = x.shape
         a = F.layer_norm(x, (h,), p["ln1_w"], p["ln1_b"])
-        qkv = F.linear(a, p["qkv_w"], p["qkv_b"]).view(b, s, 3, nh, h // nh).permute(2, 0, 3, 1, 4)
-        o = F.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], is_causal=True)
+        # q, k, v stay [b, s, nh, hd] in memory and reach SDPA as transposed views;
+        # the output comes back in the same layout, so neither direction needs a
+        # strided copy (tools/attn_layout_probe.py: 0.85 vs 1.29 ms per block fwd+bwd)
+        q, k, v = F.linear(a, p["qkv_w"], p["qkv_b"]).view(b, s, 3, nh, h // nh).unbind(2)
+        o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), is_causal=True)
         x = x + F.linear(o.transpose(1, 2).reshape(b, s, h), p["proj_w"], p["proj_b"])
         m = F.layer_norm(x, (h,), p["ln2_w"], p["ln2_b"])
         return x + F.linear(F.gelu(F.linear(m, p["fc_w"], p["fc_b"]), approximate="tanh"), p["fc2_w"], p["fc2_b"])
@@ -199,8 +203,8 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
             if f"{name}_A" in p:
                 y = y + F.linear(F.linear(inp, p[f"{name}_A"]), p[f"{name}_B"])
             return y
-        q = _rope(proj("q", a).view(b, s, nh, h // nh).transpose(1, 2))
-        k = _rope(proj("k", a).view(b, s, nh, h // nh).transpose(1, 2))
+        q = _rope(proj("q", a).view(b, s, nh, h // nh)).transpose(1, 2)
+        k = _rope(proj("k", a).view(b, s, nh, h // nh)).transpose(1, 2)
         v = proj("v", a).view(b, s, nh, h // nh).transpose(1, 2)
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
         x = x + proj("o", o.transpose(1, 2).reshape(b, s, h))
