@@ -603,6 +603,12 @@ def main():
     if per_launch_bytes < 64e6:
         # a few MB per launch (PEFT trainable slices): launch latency, not bandwidth, bounds it
         roofline["note"] = f"{per_launch_bytes / 1e6:.1f} MB per launch: launch-latency regime"
+    elif dom in ("adamw", "rs_slice") and d["ms"] < main_run["ms"]:
+        # the per-layer update / reduce-scatter runs on its own stream beside the
+        # backward GEMMs of the next layers, off the compute stream's critical path;
+        # its live duration includes waiting for SMs the GEMM CTAs hold
+        roofline["note"] = ("live = CUDA events around each launch while it shares the GPU with the concurrent "
+                            "backward GEMMs (off the critical path); isolated = the same launch alone")
     if roofline["bound"] == "hbm":
         iso = isolated_rate(dom, per_launch_bytes, mc.dtype_bytes, dev, fused_adam=(world == 1))
         if iso:
