@@ -239,6 +239,17 @@ typedef struct fcdp_adam_config {
 } fcdp_adam_config;
 int fcdp_adam_step(int64_t n, const fcdp_adam_config* cfg, float* master, float* m, float* v,
                    const float* grad, void* param, int32_t param_elem_bytes, void* stream);
+/* Driving-model LayerNorm (not the parameter-movement path; bf16 rows of h
+ * elements, h a multiple of 256 and <= 2048, fp32 statistics): forward writes y
+ * and per-row mean / rstd; backward writes dx and (if dw, db are non-NULL) the
+ * gamma / beta gradients through a deterministic two-stage column reduction in
+ * `scratch` (2 * splits * h floats). */
+int fcdp_layernorm_fwd(int64_t rows, int32_t h, float eps, const void* x, const void* w, const void* b, void* y,
+                       float* mean, float* rstd, void* stream);
+int fcdp_layernorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, const void* w, const float* mean,
+                       const float* rstd, void* dx, void* dw, void* db, float* scratch, int32_t splits,
+                       void* stream);
+
 /* Let kernels launched on `device` dereference `peer`'s memory over NVLink
  * (single-process multi-GPU use of the stateless kernels; the engine itself
  * maps peers through CUDA IPC). */

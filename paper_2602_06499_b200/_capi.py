@@ -150,6 +150,8 @@ SIGNATURES = {
     "fcdp_rs_finalize": (C.c_int, [i64, i32, i32, i32, P, P, i64, f32, P, P]),
     "fcdp_adam_step": (C.c_int, [i64, C.POINTER(AdamConfig), P, P, P, P, P, i32, P]),
     "fcdp_enable_peer_access": (C.c_int, [i32, i32]),
+    "fcdp_layernorm_fwd": (C.c_int, [i64, i32, C.c_float, P, P, P, P, P, P, P]),
+    "fcdp_layernorm_bwd": (C.c_int, [i64, i32, P, P, P, P, P, P, P, P, P, i32, P]),
     "fcdp_numa_parse_cpulist": (C.c_int, [C.c_char_p, C.POINTER(i32), i32, C.POINTER(i32)]),
     "fcdp_numa_selftest": (C.c_int, [i32, C.c_uint64, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
                                      C.POINTER(i32), C.POINTER(i32)]),

@@ -9,6 +9,7 @@
 #include "common/layout.hpp"
 #include "fcdp.h"
 #include "kernels/kernels.hpp"
+#include "kernels/model_kernels.hpp"
 
 struct fcdp_layout {
   fcdp::Layout host;
@@ -132,6 +133,25 @@ int fcdp_adam_step(int64_t n, const fcdp_adam_config* c, float* master, float* m
                        static_cast<float>(1.0 - std::pow(static_cast<double>(c->beta2), c->step))};
     check_cuda(fcdp::launch_adam(n, p, master, m, v, grad, param, eb, static_cast<cudaStream_t>(stream)),
                "fcdp_adam_step");
+  });
+}
+
+int fcdp_layernorm_fwd(int64_t rows, int32_t h, float eps, const void* x, const void* w, const void* b, void* y,
+                       float* mean, float* rstd, void* stream) {
+  return guarded([&] {
+    if (!fcdp::layernorm_supported(h)) throw shardsim::ConfigError("layernorm: h must be a multiple of 256, <= 2048");
+    check_cuda(fcdp::launch_layernorm_fwd(rows, h, eps, x, w, b, y, mean, rstd, static_cast<cudaStream_t>(stream)),
+               "fcdp_layernorm_fwd");
+  });
+}
+
+int fcdp_layernorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, const void* w, const float* mean,
+                       const float* rstd, void* dx, void* dw, void* db, float* scratch, int32_t splits, void* stream) {
+  return guarded([&] {
+    if (!fcdp::layernorm_supported(h)) throw shardsim::ConfigError("layernorm: h must be a multiple of 256, <= 2048");
+    check_cuda(fcdp::launch_layernorm_bwd(rows, h, dy, x, w, mean, rstd, dx, dw, db, scratch, splits,
+                                          static_cast<cudaStream_t>(stream)),
+               "fcdp_layernorm_bwd");
   });
 }
 

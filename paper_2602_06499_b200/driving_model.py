@@ -173,6 +173,65 @@ def _rope(x, base=10000.0):
     return out.flatten(-2)
 
 
+_LN = None
+
+
+def _layer_norm(x, w, b, eps=1e-5):
+    """LayerNorm of the GPT-2 blocks: libfcdp's bandwidth kernels for bf16 rows
+    (h a multiple of 256, <= 2048, on the GPU), torch's otherwise."""
+    global _LN
+    import torch
+    import torch.nn.functional as F
+    h = x.shape[-1]
+    if not (x.is_cuda and x.dtype == torch.bfloat16 and h % 256 == 0 and h <= 2048):
+        return F.layer_norm(x, (h,), w, b, eps)
+    if _LN is None:
+        _LN = _make_layernorm()
+    return _LN.apply(x, w, b, eps)
+
+
+def _make_layernorm():
+    import ctypes as C
+    import torch
+    from ._capi import check, lib
+
+    P = lambda t: C.c_void_p(t.data_ptr())
+
+    class LayerNormFn(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, x, w, b, eps):
+            xc = x.contiguous()
+            h = xc.shape[-1]
+            rows = xc.numel() // h
+            y = torch.empty_like(xc)
+            mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+            rstd = torch.empty_like(mean)
+            s = C.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+            check(lib().fcdp_layernorm_fwd(rows, h, eps, P(xc), P(w), P(b), P(y), P(mean), P(rstd), s))
+            ctx.save_for_backward(xc, w, mean, rstd)
+            return y
+
+        @staticmethod
+        def backward(ctx, dy):
+            xc, w, mean, rstd = ctx.saved_tensors
+            h = xc.shape[-1]
+            rows = xc.numel() // h
+            dyc = dy.contiguous()
+            dx = torch.empty_like(xc)
+            want_w = ctx.needs_input_grad[1] or ctx.needs_input_grad[2]
+            dw = torch.empty(h, dtype=w.dtype, device=w.device) if want_w else None
+            db = torch.empty(h, dtype=w.dtype, device=w.device) if want_w else None
+            splits = 64
+            scratch = torch.empty(2 * splits * h, dtype=torch.float32, device=xc.device) if want_w else None
+            s = C.c_void_p(torch.cuda.current_stream(xc.device).cuda_stream)
+            check(lib().fcdp_layernorm_bwd(rows, h, P(dyc), P(xc), P(w), P(mean), P(rstd), P(dx),
+                                           P(dw) if want_w else None, P(db) if want_w else None,
+                                           P(scratch) if want_w else None, splits, s))
+            return dx, dw, db, None
+
+    return LayerNormFn
+
+
 def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=None):
     """Forward of one layer.  x: [b, s, h] (None for the embedding)."""
     import torch
@@ -185,14 +244,14 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         return y
     if ldef.kind == "gpt2_block":
         b, s, _ = x.shape
-        a = F.layer_norm(x, (h,), p["ln1_w"], p["ln1_b"])
+        a = _layer_norm(x, p["ln1_w"], p["ln1_b"])
         # q, k, v stay [b, s, nh, hd] in memory and reach SDPA as transposed views;
         # the output comes back in the same layout, so neither direction needs a
         # strided copy (tools/attn_layout_probe.py: 0.85 vs 1.29 ms per block fwd+bwd)
         q, k, v = F.linear(a, p["qkv_w"], p["qkv_b"]).view(b, s, 3, nh, h // nh).unbind(2)
         o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), is_causal=True)
         x = x + F.linear(o.transpose(1, 2).reshape(b, s, h), p["proj_w"], p["proj_b"])
-        m = F.layer_norm(x, (h,), p["ln2_w"], p["ln2_b"])
+        m = _layer_norm(x, p["ln2_w"], p["ln2_b"])
         return x + F.linear(F.gelu(F.linear(m, p["fc_w"], p["fc_b"]), approximate="tanh"), p["fc2_w"], p["fc2_b"])
     if ldef.kind == "llama_block":
         b, s, _ = x.shape
@@ -212,7 +271,7 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         return x + F.linear(F.silu(F.linear(m, p["gate_w"])) * F.linear(m, p["up_w"]), p["down_w"])
     if ldef.kind == "head":
         if "lnf_w" in p:
-            a = F.layer_norm(x, (h,), p["lnf_w"], p["lnf_b"])
+            a = _layer_norm(x, p["lnf_w"], p["lnf_b"])
         else:
             a = F.rms_norm(x, (h,), p["norm_w"], eps=1e-5)
         logits = F.linear(a, p["lm_w"])

@@ -66,6 +66,8 @@ def main():
     W = torch.empty_like(X)
     timeit("concat_dense_g1", lambda: _capi.check(lib.fcdp_expand(dense, (C.c_void_p * 1)(X.data_ptr()), None, P(W), 0, None)),
            2 * chunks * 16)
+    # like-for-like denominator at this launch size: torch's own D2D copy (copy engine / cudaMemcpy)
+    timeit("torch_copy_same_size", lambda: W.copy_(X), 2 * chunks * 16)
     d4 = layout(np.ones(chunks, np.uint8), 2, 1, 4)
     per = chunks // 4 * 16
     Xs = [X[i * per:(i + 1) * per] for i in range(4)]
