@@ -453,7 +453,10 @@ def main():
         cap = torch.cuda.get_device_properties(dev).total_memory
         b, oom = S.max_feasible_batch(plan, model, topo, cap)
         b = int(min(b, 256)) if not oom else 1
+        measured_act[0] = int(max_over_ranks(float(act // L)))
         return int(max_over_ranks(-b) * -1) if world > 1 else b
+
+    measured_act = [None]  # per layer per sample, from the probe (feeds every run's tau projection)
 
     capacity = torch.cuda.get_device_properties(dev).total_memory
 
@@ -463,7 +466,8 @@ def main():
         tr = FcdpTrainer(mc, topo, plan, rank=rank, world_size=world, device=local, shm_name=shm,
                          batch_per_gpu=args.batch, seq_len=seq, nic_pacing=not args.no_pacing, lr=1e-4,
                          use_copy_engine=args.copy_engine, timeout_s=args.engine_timeout,
-                         gpu_capacity_bytes=capacity if tau > 0 else 0)
+                         gpu_capacity_bytes=capacity if tau > 0 else 0,
+                         activation_bytes_per_sample=measured_act[0])
         batches = [synthetic_batch(mc.vocab, args.batch, seq, 0x5EED, i, rank, device=dev)
                    for i in range(warmup + steps)]
         for i in range(warmup):

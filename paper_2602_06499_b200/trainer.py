@@ -30,7 +30,8 @@ class FcdpTrainer:
     def __init__(self, cfg: ModelConfig, topo: S.ClusterTopology, plan: S.StrategyPlan, *, rank: int,
                  world_size: int, device: int, shm_name: str, batch_per_gpu: int, seq_len: Optional[int] = None,
                  seed: int = 0x5EED, nic_pacing: bool = True, lr: float = 1e-4, weight_decay: float = 0.0,
-                 gpu_capacity_bytes: int = 0, use_copy_engine: bool = False, timeout_s: float = 600.0):
+                 gpu_capacity_bytes: int = 0, use_copy_engine: bool = False, timeout_s: float = 600.0,
+                 activation_bytes_per_sample: Optional[int] = None):
         self.cfg = cfg
         self.topo, self.plan = topo, plan
         self.rank, self.world = rank, world_size
@@ -38,8 +39,12 @@ class FcdpTrainer:
         self.batch, self.seq = batch_per_gpu, seq_len or cfg.seq
         self.dtype = torch.bfloat16 if cfg.dtype_bytes == 2 else torch.float32
         self.defs: List[LayerDef] = cfg.layer_defs()
+        # activation bytes per sample per layer feed the tau-admission projection;
+        # a measured figure (bench.py's ZeRO-3 max-batch probe) overrides the estimate
         layers = [S.LayerSpec(i, d.numel, d.trainable_params() / d.numel,
-                              activation_bytes_per_sample=activation_bytes(cfg, d, self.seq))
+                              activation_bytes_per_sample=(activation_bytes_per_sample
+                                                           if activation_bytes_per_sample is not None
+                                                           else activation_bytes(cfg, d, self.seq)))
                   for i, d in enumerate(self.defs)]
         self.model = S.ModelSpec(layers, cfg.dtype_bytes, batch_per_gpu=batch_per_gpu)
         self.gpu_capacity_bytes = gpu_capacity_bytes
