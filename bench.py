@@ -428,7 +428,11 @@ def main():
         return out
 
     def zero3_max_batch() -> int:
-        """strategy.cpp:116-137 with a measured activation coefficient."""
+        """strategy.cpp:116-137 with a measured activation coefficient, and the
+        capacity reduced by what this engine really keeps resident beyond the
+        reference's persistent estimate (the reference counts optimizer state as
+        6 x the grad bytes; the engine also keeps fp32 masters, gathered-layer
+        and peer-visible slots), so the chosen batch actually fits."""
         plan = S.StrategyPlan(S.StrategyKind.Zero3)
         shm = bcast(f"fcdp_probe_{uuid.uuid4().hex[:12]}" if rank == 0 else None)
         tr = FcdpTrainer(mc, topo, plan, rank=rank, world_size=world, device=local, shm_name=shm,
@@ -437,6 +441,8 @@ def main():
         tr.step(x, y)
         tr.sync()
         torch.cuda.synchronize()
+        free, total = torch.cuda.mem_get_info(dev)
+        engine_bytes = (total - free) - torch.cuda.memory_reserved(dev)  # outside torch's allocator
         torch.cuda.reset_peak_memory_stats(dev)
         base = torch.cuda.memory_allocated(dev)
         tr.step(x, y)
@@ -451,12 +457,22 @@ def main():
         for lyr in model.layers:
             lyr.activation_bytes_per_sample = act // L
         cap = torch.cuda.get_device_properties(dev).total_memory
-        b, oom = S.max_feasible_batch(plan, model, topo, cap)
+        ref_persistent = S.memory_footprint(plan, model, topo).gpu_persistent_bytes
+        extra = max(0, engine_bytes - ref_persistent)
+        b, oom = S.max_feasible_batch(plan, model, topo, max(cap - extra, 1))
         b = int(min(b, 256)) if not oom else 1
         measured_act[0] = int(max_over_ranks(float(act // L)))
-        return int(max_over_ranks(-b) * -1) if world > 1 else b
+        b = int(max_over_ranks(-b) * -1) if world > 1 else b
+        if rank == 0:
+            print(f"[bench] ZeRO-3 max batch {b}: activation {act / 2**30:.2f} GiB per sample, engine resident "
+                  f"{engine_bytes / 2**30:.1f} GiB vs reference persistent {ref_persistent / 2**30:.1f} GiB",
+                  file=sys.stderr, flush=True)
+        probe_info.update({"zero3_max_batch": b, "activation_bytes_per_sample": act, "capacity_reduction": extra,
+                           "engine_resident_bytes": engine_bytes, "reference_persistent_bytes": ref_persistent})
+        return b
 
     measured_act = [None]  # per layer per sample, from the probe (feeds every run's tau projection)
+    probe_info = {}
 
     capacity = torch.cuda.get_device_properties(dev).total_memory
 
@@ -466,7 +482,7 @@ def main():
         tr = FcdpTrainer(mc, topo, plan, rank=rank, world_size=world, device=local, shm_name=shm,
                          batch_per_gpu=args.batch, seq_len=seq, nic_pacing=not args.no_pacing, lr=1e-4,
                          use_copy_engine=args.copy_engine, timeout_s=args.engine_timeout,
-                         gpu_capacity_bytes=capacity if tau > 0 else 0,
+                         gpu_capacity_bytes=(capacity - probe_info.get("capacity_reduction", 0)) if tau > 0 else 0,
                          activation_bytes_per_sample=measured_act[0])
         batches = [synthetic_batch(mc.vocab, args.batch, seq, 0x5EED, i, rank, device=dev)
                    for i in range(warmup + steps)]
@@ -477,7 +493,10 @@ def main():
         barrier()
         tr.engine.reset_counters()
         tr.engine.kernel_stats(reset=True)
-        tr.engine.set_timing(timing)
+        # the timed region runs without per-kernel event timing (the kernel
+        # statistics come from a separate pass below), so the headline carries
+        # no instrumentation and ZeRO-3 / FCDP are timed the same way
+        tr.engine.set_timing(False)
         barrier()
         sampler = ClockSampler(world) if (rank == 0 and timing) else None
         if sampler:
@@ -495,10 +514,23 @@ def main():
         ms = max_over_ranks(e0.elapsed_time(e1))
         per_step = [round(evs[i].elapsed_time(evs[i + 1]), 3) for i in range(steps)]
         counters = tr.engine.counters()
-        kst = tr.engine.kernel_stats(reset=True)
         numa = tr.engine.numa()
-        tr.engine.set_timing(False)
         loss_v = float(loss.item())
+        launches = tr.engine.kernel_stats(reset=True)  # launch counts of the timed region
+        gpu_launches = sum(launches[k]["launches"] for k in tr.engine.KERNEL_CLASSES)
+        kst, kst_steps = None, 0
+        if timing:
+            # kernel statistics pass: CUDA events around every engine launch
+            kst_steps = min(steps, 5)
+            tr.engine.kernel_stats(reset=True)
+            tr.engine.set_timing(True)
+            for i in range(kst_steps):
+                tr.step(*batches[warmup + i])
+            tr.sync()
+            torch.cuda.synchronize()
+            kst = tr.engine.kernel_stats(reset=True)
+            tr.engine.set_timing(False)
+            barrier()
         # per-node inter-group bytes per step (sum over the node's ranks), from the NIC counters
         node_tx = {k: sum_over_ranks(counters[k]) / N / steps for k in ("nic_tx_fwd_ag", "nic_tx_bwd_ag", "nic_tx_rs",
                                                                        "nic_tx_grad_sync")}
@@ -531,8 +563,10 @@ def main():
         tr.close()
         del tr
         torch.cuda.empty_cache()
-        return {"ms": ms, "per_step": per_step, "counters": counters, "kernels": kst, "clocks": clocks, "loss": loss_v,
-                "node_tx": node_tx, "cache": cache, "vol": vol, "e2e": e2e, "numa": numa}
+        return {"ms": ms, "per_step": per_step, "counters": counters, "kernels": kst, "kst_steps": kst_steps,
+                "gpu_launches": gpu_launches,
+                "clocks": clocks, "loss": loss_v, "node_tx": node_tx, "cache": cache, "vol": vol, "e2e": e2e,
+                "numa": numa}
 
     pcie = pcie_peak()
     if args.batch <= 0:
@@ -577,6 +611,7 @@ def main():
     hbm = peaks.get("hbm_gbs")
     from paper_2602_06499_b200.engine import Engine as _E
     allst = main_run["kernels"]
+    ks = max(main_run["kst_steps"], 1)  # steps of the kernel-statistics pass
     kst = {k: v for k, v in allst.items() if k in _E.KERNEL_CLASSES}
     cst = {k: v for k, v in allst.items() if k in _E.COPY_CLASSES}
     dom = max(kst, key=lambda k: kst[k]["ms"]) if any(v["ms"] for v in kst.values()) else "adamw"
@@ -600,14 +635,14 @@ def main():
                             if (not nvlink_bound and world == 1 and args.preset == "gpt2-1.3b") else None),
                 "alg_bytes_per_launch": per_launch_bytes,
                 "ms_per_launch": per_launch_ms, "peak_source": src,
-                "share_of_step": d["ms"] / main_run["ms"] if main_run["ms"] else None,
+                "share_of_step": (d["ms"] / ks) / ms_step if ms_step else None,
                 # north_star's nominal denominators (B200: ~8 TB/s HBM3e, 900 GB/s NVLink per direction)
                 "peak_nominal": 900.0 if nvlink_bound else 8000.0,
                 "frac_of_nominal": (achieved / (900.0 if nvlink_bound else 8000.0)) if achieved else None}
     if per_launch_bytes < 64e6:
         # a few MB per launch (PEFT trainable slices): launch latency, not bandwidth, bounds it
         roofline["note"] = f"{per_launch_bytes / 1e6:.1f} MB per launch: launch-latency regime"
-    elif dom in ("adamw", "rs_slice") and d["ms"] < main_run["ms"]:
+    elif dom in ("adamw", "rs_slice"):
         # the per-layer update / reduce-scatter runs on its own stream beside the
         # backward GEMMs of the next layers, off the compute stream's critical path;
         # its live duration includes waiting for SMs the GEMM CTAs hold
@@ -618,7 +653,7 @@ def main():
         if iso:
             iso["frac"] = iso["achieved"] / peak if peak else None
             roofline["isolated"] = iso
-    gpu_launches = sum(v["launches"] for v in kst.values())
+    gpu_launches = main_run["gpu_launches"]
     ag = {"fcdp_fwd": main_run["node_tx"]["nic_tx_fwd_ag"], "fcdp_bwd": main_run["node_tx"]["nic_tx_bwd_ag"],
           "fcdp_rs": main_run["node_tx"]["nic_tx_rs"],
           "oracle_fcdp_fwd": main_run["vol"].fwd_ag_inter, "oracle_fcdp_bwd": main_run["vol"].bwd_ag_inter}
@@ -645,9 +680,9 @@ def main():
             continue
         gbs = v["alg_bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None
         peak_c = pcie["d2h"] if k.endswith("d2h") else pcie["h2d"]
-        copies[k] = {"bytes_per_step": v["alg_bytes"] / args.steps, "copies_per_step": v["launches"] / args.steps,
+        copies[k] = {"bytes_per_step": v["alg_bytes"] / ks, "copies_per_step": v["launches"] / ks,
                      "GBps": gbs, "pcie_peak_gbps": peak_c, "frac": gbs / peak_c if gbs else None}
-    kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
+    kernels = {k: {"launches_per_step": v["launches"] / ks, "ms_per_step": v["ms"] / ks,
                    "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None} for k, v in kst.items()}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -674,7 +709,12 @@ def main():
                                 "ms_per_step": tau_run["ms"] / args.zero3_steps, "cache": tau_run["cache"],
                                 "ag_inter_fwd_bwd": [tau_run["node_tx"]["nic_tx_fwd_ag"], tau_run["node_tx"]["nic_tx_bwd_ag"]]}
                                if tau_run else None),
-        "host_numa": main_run["numa"], "kernels": kernels, "loss": main_run["loss"], "ms_each_step_rank0": main_run["per_step"],
+        "host_numa": main_run["numa"], "kernels": kernels,
+        "batch_probe": probe_info or None,
+        "kernel_stats_pass": {"steps": ks, "note": "per-kernel CUDA-event timing (kernels, roofline, copies) comes "
+                                                   "from this many extra steps after the timed region; the timed "
+                                                   "region itself runs uninstrumented"},
+        "loss": main_run["loss"], "ms_each_step_rank0": main_run["per_step"],
     }
     print(json.dumps(line), flush=True)
     if world > 1:
