@@ -250,6 +250,38 @@ int fcdp_layernorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, c
                        const float* rstd, void* dx, void* dw, void* db, float* scratch, int32_t splits,
                        void* stream);
 
+/* Driving-model bias gradient (bf16 [rows x cols], cols a multiple of 8):
+ * db[c] = sum_r dy[r, c] in fp32, deterministic two-stage reduction through
+ * `scratch` (splits * cols floats; splits from fcdp_colsum_splits). */
+int fcdp_colsum_splits(int64_t rows, int32_t cols);
+int fcdp_bias_grad(int64_t rows, int32_t cols, const void* dy, void* db, float* scratch, int32_t splits,
+                   void* stream);
+/* Driving-model MLP activation: y = gelu_tanh(h + b) (bias add fused), and its
+ * backward dh = dy * gelu'(h + b) fused with db = sum_r dh (scratch as above). */
+int fcdp_bias_gelu_fwd(int64_t rows, int32_t cols, const void* h, const void* b, void* y, void* stream);
+int fcdp_bias_gelu_bwd(int64_t rows, int32_t cols, const void* dy, const void* h, const void* b, void* dh, void* db,
+                       float* scratch, int32_t splits, void* stream);
+/* Driving-model LM head loss: cross-entropy of bf16 logit rows (vocab a
+ * multiple of 8; label < 0 = ignored row).  Forward writes per-row loss and
+ * log-sum-exp; backward writes dlogits = (softmax - onehot) * scale[0] (scale:
+ * a device fp32 scalar, e.g. grad / valid rows) into a separate buffer. */
+int fcdp_xent_fwd(int64_t rows, int32_t vocab, const void* logits, const int64_t* labels, float* loss, float* lse,
+                  void* stream);
+int fcdp_xent_bwd(int64_t rows, int32_t vocab, const void* logits, const int64_t* labels, const float* lse,
+                  const float* scale, void* dlogits, void* stream);
+
+/* Driving-model Llama blocks: rotary embedding of x [batch, seq, heads, dim]
+ * (bf16; pairs (2i, 2i+1); fp32 cos / sin tables [seq, dim / 2]; inverse != 0
+ * rotates back - the backward), and SwiGLU y = silu(g) * u over [rows x f]
+ * with its backward (row strides in elements, multiples of 8, so g and u may
+ * be the two halves of one [rows x 2f] GEMM output). */
+int fcdp_rope(int64_t batch, int32_t seq, int32_t heads, int32_t dim, const void* x, const float* cos_table,
+              const float* sin_table, int32_t inverse, void* y, void* stream);
+int fcdp_swiglu_fwd(int64_t rows, int32_t f, const void* g, int64_t g_stride, const void* u, int64_t u_stride, void* y,
+                    void* stream);
+int fcdp_swiglu_bwd(int64_t rows, int32_t f, const void* dy, const void* g, int64_t g_stride, const void* u,
+                    int64_t u_stride, void* dg, int64_t dg_stride, void* du, int64_t du_stride, void* stream);
+
 /* Let kernels launched on `device` dereference `peer`'s memory over NVLink
  * (single-process multi-GPU use of the stateless kernels; the engine itself
  * maps peers through CUDA IPC). */
@@ -409,6 +441,17 @@ int fcdp_engine_kernel_stats(fcdp_engine* e, fcdp_kernel_stats* out, int32_t res
  * at which its stream reached it (begin) and finished it (end). */
 int fcdp_engine_set_trace(fcdp_engine* e, int32_t on);
 int fcdp_engine_trace(fcdp_engine* e, float* begin_ms, float* end_ms, uint32_t capacity, uint32_t* count);
+
+/* NIC bandwidth profile (Fig. 10): when on, this rank's NIC emulator
+ * records every payload it paces onto its node's emulated wire.  The drain call
+ * returns up to `capacity` records made since the last call: the wire interval
+ * [start_ns, end_ns) on steady_clock (the clock every rank's NIC shares), the
+ * bytes, and the kind (0 = forward AgInter, 1 = backward AgInter, 2 =
+ * inter-node reduce-scatter, 15 = MiCS/ZeRO++ gradient sync).  Payloads of one
+ * node never overlap on its wire (one NIC per node, topology.hpp:23-25). */
+int fcdp_engine_set_nic_log(fcdp_engine* e, int32_t on);
+int fcdp_engine_nic_log(fcdp_engine* e, uint64_t* start_ns, uint64_t* end_ns, uint64_t* bytes, int32_t* kind,
+                        uint32_t capacity, uint32_t* count);
 
 /* Host-only NUMA placement checks (no GPU needed):
  * parse a sysfs cpulist ("0-3,8"); and for `node`: online memory nodes, its

@@ -152,6 +152,15 @@ SIGNATURES = {
     "fcdp_enable_peer_access": (C.c_int, [i32, i32]),
     "fcdp_layernorm_fwd": (C.c_int, [i64, i32, C.c_float, P, P, P, P, P, P, P]),
     "fcdp_layernorm_bwd": (C.c_int, [i64, i32, P, P, P, P, P, P, P, P, P, i32, P]),
+    "fcdp_colsum_splits": (C.c_int, [i64, i32]),
+    "fcdp_bias_grad": (C.c_int, [i64, i32, P, P, P, i32, P]),
+    "fcdp_bias_gelu_fwd": (C.c_int, [i64, i32, P, P, P, P]),
+    "fcdp_bias_gelu_bwd": (C.c_int, [i64, i32, P, P, P, P, P, P, i32, P]),
+    "fcdp_xent_fwd": (C.c_int, [i64, i32, P, P, P, P, P]),
+    "fcdp_xent_bwd": (C.c_int, [i64, i32, P, P, P, P, P, P]),
+    "fcdp_rope": (C.c_int, [i64, i32, i32, i32, P, P, P, i32, P, P]),
+    "fcdp_swiglu_fwd": (C.c_int, [i64, i32, P, i64, P, i64, P, P]),
+    "fcdp_swiglu_bwd": (C.c_int, [i64, i32, P, P, i64, P, i64, P, i64, P, i64, P]),
     "fcdp_numa_parse_cpulist": (C.c_int, [C.c_char_p, C.POINTER(i32), i32, C.POINTER(i32)]),
     "fcdp_numa_selftest": (C.c_int, [i32, C.c_uint64, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
                                      C.POINTER(i32), C.POINTER(i32)]),
@@ -185,6 +194,9 @@ SIGNATURES = {
     "fcdp_engine_kernel_stats": (C.c_int, [P, C.POINTER(KernelStats), i32]),
     "fcdp_engine_set_trace": (C.c_int, [P, i32]),
     "fcdp_engine_trace": (C.c_int, [P, C.POINTER(f32), C.POINTER(f32), u32, C.POINTER(u32)]),
+    "fcdp_engine_set_nic_log": (C.c_int, [P, i32]),
+    "fcdp_engine_nic_log": (C.c_int, [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(i32), u32,
+                                      C.POINTER(u32)]),
     "fcdp_nic_selftest": (C.c_int, [C.c_char_p, i32, i32, i32, f64, u64, i32, C.POINTER(f64)]),
 }
 

@@ -38,12 +38,18 @@ void check_cuda(cudaError_t e, const char* what) {
 
 void upload_layout(Layout& L, std::uint32_t** d_bits, std::uint32_t** d_tpre) {
   const std::size_t bytes = L.bits.size() * sizeof(std::uint32_t);
+  const std::size_t tw = L.sparse_t() ? L.twords.size() * sizeof(std::uint32_t) : 0;
   check_cuda(cudaMalloc(d_bits, bytes), "cudaMalloc(layout bits)");
-  check_cuda(cudaMalloc(d_tpre, bytes), "cudaMalloc(layout prefix)");
+  check_cuda(cudaMalloc(d_tpre, bytes + tw), "cudaMalloc(layout prefix)");
   check_cuda(cudaMemcpy(*d_bits, L.bits.data(), bytes, cudaMemcpyHostToDevice), "upload layout bits");
   check_cuda(cudaMemcpy(*d_tpre, L.tpre.data(), bytes, cudaMemcpyHostToDevice), "upload layout prefix");
   L.dev.bits = *d_bits;
   L.dev.tpre = *d_tpre;
+  if (tw) {  // the active trainable words ride behind the prefix
+    check_cuda(cudaMemcpy(*d_tpre + L.bits.size(), L.twords.data(), tw, cudaMemcpyHostToDevice), "upload active words");
+    L.dev.twords = *d_tpre + L.bits.size();
+    L.dev.ntwords = static_cast<std::int64_t>(L.twords.size());
+  }
 }
 
 }  // namespace fcdp
@@ -152,6 +158,84 @@ int fcdp_layernorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, c
     check_cuda(fcdp::launch_layernorm_bwd(rows, h, dy, x, w, mean, rstd, dx, dw, db, scratch, splits,
                                           static_cast<cudaStream_t>(stream)),
                "fcdp_layernorm_bwd");
+  });
+}
+
+int fcdp_colsum_splits(int64_t rows, int32_t cols) { return fcdp::colsum_splits(rows, cols); }
+
+int fcdp_bias_grad(int64_t rows, int32_t cols, const void* dy, void* db, float* scratch, int32_t splits,
+                   void* stream) {
+  return guarded([&] {
+    if (cols % 8) throw shardsim::ConfigError("bias_grad: cols must be a multiple of 8");
+    check_cuda(fcdp::launch_colsum(rows, cols, dy, db, scratch, splits, static_cast<cudaStream_t>(stream)),
+               "fcdp_bias_grad");
+  });
+}
+
+int fcdp_bias_gelu_fwd(int64_t rows, int32_t cols, const void* h, const void* b, void* y, void* stream) {
+  return guarded([&] {
+    if (cols % 8) throw shardsim::ConfigError("bias_gelu: cols must be a multiple of 8");
+    check_cuda(fcdp::launch_bias_gelu_fwd(rows, cols, h, b, y, static_cast<cudaStream_t>(stream)),
+               "fcdp_bias_gelu_fwd");
+  });
+}
+
+int fcdp_bias_gelu_bwd(int64_t rows, int32_t cols, const void* dy, const void* h, const void* b, void* dh, void* db,
+                       float* scratch, int32_t splits, void* stream) {
+  return guarded([&] {
+    if (cols % 8) throw shardsim::ConfigError("bias_gelu: cols must be a multiple of 8");
+    check_cuda(fcdp::launch_bias_gelu_bwd(rows, cols, dy, h, b, dh, db, scratch, splits,
+                                          static_cast<cudaStream_t>(stream)),
+               "fcdp_bias_gelu_bwd");
+  });
+}
+
+int fcdp_xent_fwd(int64_t rows, int32_t vocab, const void* logits, const int64_t* labels, float* loss, float* lse,
+                  void* stream) {
+  return guarded([&] {
+    if (vocab % 8) throw shardsim::ConfigError("xent: vocab must be a multiple of 8");
+    check_cuda(fcdp::launch_xent_fwd(rows, vocab, logits, labels, loss, lse, static_cast<cudaStream_t>(stream)),
+               "fcdp_xent_fwd");
+  });
+}
+
+int fcdp_xent_bwd(int64_t rows, int32_t vocab, const void* logits, const int64_t* labels, const float* lse,
+                  const float* scale, void* dlogits, void* stream) {
+  return guarded([&] {
+    if (vocab % 8) throw shardsim::ConfigError("xent: vocab must be a multiple of 8");
+    check_cuda(fcdp::launch_xent_bwd(rows, vocab, logits, labels, lse, scale, dlogits,
+                                     static_cast<cudaStream_t>(stream)),
+               "fcdp_xent_bwd");
+  });
+}
+
+int fcdp_rope(int64_t batch, int32_t seq, int32_t heads, int32_t dim, const void* x, const float* cos_table,
+              const float* sin_table, int32_t inverse, void* y, void* stream) {
+  return guarded([&] {
+    if (dim % 8) throw shardsim::ConfigError("rope: head dim must be a multiple of 8");
+    check_cuda(fcdp::launch_rope(batch, seq, heads, dim, x, cos_table, sin_table, inverse != 0, y,
+                                 static_cast<cudaStream_t>(stream)),
+               "fcdp_rope");
+  });
+}
+
+int fcdp_swiglu_fwd(int64_t rows, int32_t f, const void* g, int64_t g_stride, const void* u, int64_t u_stride, void* y,
+                    void* stream) {
+  return guarded([&] {
+    if (f % 8 || g_stride % 8 || u_stride % 8) throw shardsim::ConfigError("swiglu: f and strides must be multiples of 8");
+    check_cuda(fcdp::launch_swiglu_fwd(rows, f, g, g_stride, u, u_stride, y, static_cast<cudaStream_t>(stream)),
+               "fcdp_swiglu_fwd");
+  });
+}
+
+int fcdp_swiglu_bwd(int64_t rows, int32_t f, const void* dy, const void* g, int64_t g_stride, const void* u,
+                    int64_t u_stride, void* dg, int64_t dg_stride, void* du, int64_t du_stride, void* stream) {
+  return guarded([&] {
+    if (f % 8 || g_stride % 8 || u_stride % 8 || dg_stride % 8 || du_stride % 8)
+      throw shardsim::ConfigError("swiglu: f and strides must be multiples of 8");
+    check_cuda(fcdp::launch_swiglu_bwd(rows, f, dy, g, g_stride, u, u_stride, dg, dg_stride, du, du_stride,
+                                       static_cast<cudaStream_t>(stream)),
+               "fcdp_swiglu_bwd");
   });
 }
 

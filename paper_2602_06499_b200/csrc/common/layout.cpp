@@ -61,6 +61,16 @@ Layout build_layout(std::int64_t chunks, const std::uint8_t* mask, int elem_byte
     while (we < L.dev.words && L.tpre[we] < k1) ++we;
     L.rs_word_end[j] = we;
   }
+  for (std::int64_t i = 0; i < L.dev.words; ++i)
+    if (L.bits[i]) L.twords.push_back(static_cast<std::uint32_t>(i));
+  L.rs_tw_begin.assign(local, 0);
+  L.rs_tw_end.assign(local, 0);
+  for (int j = 0; j < local; ++j) {
+    auto lo = std::lower_bound(L.twords.begin(), L.twords.end(), static_cast<std::uint32_t>(L.rs_word_begin[j]));
+    auto hi = std::lower_bound(L.twords.begin(), L.twords.end(), static_cast<std::uint32_t>(L.rs_word_end[j]));
+    L.rs_tw_begin[j] = lo - L.twords.begin();
+    L.rs_tw_end[j] = hi - L.twords.begin();
+  }
   return L;
 }
 

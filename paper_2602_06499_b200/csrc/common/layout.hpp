@@ -28,6 +28,13 @@ struct LayoutDev {
   std::int64_t slice_t = 0, slice_f = 0;  // chunks per intra slice (N shards)
   int nodes = 1, local = 1;       // N, g
   int elem_bytes = 2;
+  // Sparse trainable mask (e.g. LoRA: 0.26% of a Llama-7B block): the mask
+  // words holding at least one trainable chunk, ascending.  ntwords > 0 only
+  // when they are under half of all words; the trainable-only gather and the
+  // reduce-scatter then walk this list, so their work follows the trainable
+  // bytes instead of the layer size.
+  const std::uint32_t* twords = nullptr;
+  std::int64_t ntwords = 0;
 };
 
 // Host-side layout: owns the mask metadata and its device copy.
@@ -37,6 +44,11 @@ struct Layout {
   // For the reduce-scatter: mask-word range [word_begin[j], word_end[j]) that
   // holds every trainable chunk of intra slice j.
   std::vector<std::int64_t> rs_word_begin, rs_word_end;
+  // Active trainable words (see LayoutDev::twords) and, per slice j, the
+  // index range [rs_tw_begin[j], rs_tw_end[j]) of them it covers.
+  std::vector<std::uint32_t> twords;
+  std::vector<std::int64_t> rs_tw_begin, rs_tw_end;
+  bool sparse_t() const { return !twords.empty() && 2 * static_cast<std::int64_t>(twords.size()) < dev.words; }
 
   bool dense_trainable() const { return dev.pt == dev.chunks; }
   bool dense_frozen() const { return dev.pf == dev.chunks; }

@@ -78,31 +78,36 @@ __device__ __forceinline__ const uint4* pick_g(const SlicePtrs& s, int j) {
 // 32-bit chunk indices (the launcher rejects layers of >= 2^31 chunks, 32 GiB):
 // this loop is issue-bound as much as memory-bound, and 64-bit index math
 // doubled its instruction count.
-template <bool kWriteT, bool kWriteF, int kG>
+// kSparse (trainable-only gathers of a sparse mask): warps walk the active
+// trainable words L.twords instead of every mask word.
+template <bool kWriteT, bool kWriteF, int kG, bool kSparse = false>
 __global__ void __launch_bounds__(kThreads) expand_kernel(LayoutDev L, SlicePtrs ts, SlicePtrs fs,
                                                           uint4* __restrict__ out) {
+  static_assert(!kSparse || (kWriteT && !kWriteF), "the active-word list covers trainable chunks only");
   const int lane = threadIdx.x & 31;
   const int warp = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int nwarps = static_cast<int>((gridDim.x * blockDim.x) >> 5);
   const unsigned below = (1u << lane) - 1u;
-  const int words = static_cast<int>(L.words), chunks = static_cast<int>(L.chunks);
+  const int words = static_cast<int>(kSparse ? L.ntwords : L.words), chunks = static_cast<int>(L.chunks);
   const int per_t = static_cast<int>(L.slice_t), per_f = static_cast<int>(L.slice_f);
   for (int w0 = warp; w0 < words; w0 += nwarps * kUnroll) {
     // phase 1: the mask words and prefixes of all kUnroll groups (independent loads)
     unsigned bits[kUnroll];
-    int pre[kUnroll];
+    int pre[kUnroll], wid[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int w = w0 + u * nwarps;
-      bits[u] = w < words ? __ldg(L.bits + w) : 0u;
-      pre[u] = w < words ? static_cast<int>(__ldg(L.tpre + w)) : 0;
+      const int i = w0 + u * nwarps;
+      const int w = i < words ? (kSparse ? static_cast<int>(__ldg(L.twords + i)) : i) : 0;
+      wid[u] = w;
+      bits[u] = i < words ? __ldg(L.bits + w) : 0u;
+      pre[u] = i < words ? static_cast<int>(__ldg(L.tpre + w)) : 0;
     }
     // phase 2: ranks -> source addresses; phase 3: all data loads in flight
     uint4 v[kUnroll];
     int dst[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const int c = (w0 + u * nwarps) * 32 + lane;
+      const int c = (w0 + u * nwarps < words) ? wid[u] * 32 + lane : chunks;
       const bool valid = c < chunks;
       const bool tr = valid && ((bits[u] >> lane) & 1u);
       // the mask word's own bits are the ballot of the lanes' predicates
@@ -378,7 +383,8 @@ __device__ __forceinline__ void rs_emit(const RsArgs& a, const GradPtrs& g, std:
   rs_emit_q<T, kG>(a, q, rel, own_out, wire_out);
 }
 
-template <typename T, int kG>
+// [wb, we): mask words, or (sparse mask) indices into the active-word list L.twords
+template <typename T, int kG, bool kSparse = false>
 __global__ void __launch_bounds__(kThreads) rs_masked_kernel(LayoutDev L, GradPtrs g, RsArgs a,
                                                              std::int64_t wb, std::int64_t we,
                                                              float* __restrict__ own_out,
@@ -387,7 +393,8 @@ __global__ void __launch_bounds__(kThreads) rs_masked_kernel(LayoutDev L, GradPt
   const std::int64_t warp = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const std::int64_t nwarps = (static_cast<std::int64_t>(gridDim.x) * blockDim.x) >> 5;
   const unsigned below = (1u << lane) - 1u;
-  for (std::int64_t w = wb + warp; w < we; w += nwarps) {
+  for (std::int64_t i = wb + warp; i < we; i += nwarps) {
+    const std::int64_t w = kSparse ? static_cast<std::int64_t>(__ldg(L.twords + i)) : i;
     const std::int64_t c = w * 32 + lane;
     const bool valid = c < L.chunks;
     const bool tr = valid && ((__ldg(L.bits + w) >> lane) & 1u);
@@ -705,11 +712,14 @@ cudaError_t launch_expand(const Layout& L, const SlicePtrs& ts, const SlicePtrs&
   }
   if (L.dev.words * 32 >= (std::int64_t{1} << 31) - (std::int64_t{1} << 24))
     return cudaErrorInvalidValue;  // 32-bit chunk indices (+ grid-stride headroom)
-  const int grid = grid_for(L.dev.words * 32, kThreads * kUnroll);
+  const bool sparse = want_t && !want_f && L.dev.ntwords > 0;
+  const int grid = grid_for((sparse ? L.dev.ntwords : L.dev.words) * 32, kThreads * kUnroll);
   auto go = [&](auto tag_g) {
     constexpr int G = decltype(tag_g)::value;
     if (want_t && want_f)
       expand_kernel<true, true, G><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
+    else if (sparse)
+      expand_kernel<true, false, G, true><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
     else if (want_t)
       expand_kernel<true, false, G><<<grid, kThreads, 0, s>>>(L.dev, ts, fs, out);
     else
@@ -742,7 +752,9 @@ cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n
   uint4* wire = static_cast<uint4*>(wire_out);
   const bool bf16 = L.dev.elem_bytes == 2;
   const bool dense = L.dense_trainable();
-  const std::int64_t wb = dense ? 0 : L.rs_word_begin[j], we = dense ? 0 : L.rs_word_end[j];
+  const bool sparse = !dense && L.dev.ntwords > 0;
+  const std::int64_t wb = dense ? 0 : (sparse ? L.rs_tw_begin[j] : L.rs_word_begin[j]);
+  const std::int64_t we = dense ? 0 : (sparse ? L.rs_tw_end[j] : L.rs_word_end[j]);
   const int grid = dense ? grid_for(a.k1 - a.k0, kThreads * std::max(1, 8 / L.dev.local))
                          : grid_for((we - wb) * 32, kThreads);
   auto go = [&](auto tag_t, auto tag_g) {
@@ -750,6 +762,8 @@ cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n
     constexpr int G = decltype(tag_g)::value;
     if (dense)
       rs_dense_kernel<T, G><<<grid, kThreads, 0, s>>>(grads, a, own_out, wire);
+    else if (sparse)
+      rs_masked_kernel<T, G, true><<<grid, kThreads, 0, s>>>(L.dev, grads, a, wb, we, own_out, wire);
     else
       rs_masked_kernel<T, G><<<grid, kThreads, 0, s>>>(L.dev, grads, a, wb, we, own_out, wire);
   };

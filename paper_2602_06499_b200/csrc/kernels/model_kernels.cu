@@ -1,4 +1,7 @@
-// LayerNorm forward / backward for the driving model (GPT-2 blocks, bf16).
+// Driving-model kernels (GPT-2 blocks and the LM head, bf16): LayerNorm
+// forward / backward, bias gradients (column sums), bias + GELU forward and
+// GELU backward fused with the bias gradient, the fused cross-entropy, and
+// the Llama blocks' rotary embedding and SwiGLU (forward / backward).
 //
 // Not part of the parameter-movement path: the driving model is its consumer.
 // PyTorch's LayerNorm kernels ran at ~2 TB/s forward and the backward's
@@ -14,6 +17,8 @@
 //           deterministic, no atomics.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 
 #include "kernels/model_kernels.hpp"
@@ -204,6 +209,325 @@ __global__ void ln_bwd_dw_final_kernel(int h, int splits, const float* __restric
   db[col] = __float2bfloat16_rn(sb);
 }
 
+
+// ------------------------------------------------- column sums (bias grads)
+// out[c] = sum_r dy[r, c] for a bf16 [rows x cols] matrix (the bias gradient
+// of a linear layer).  Same two-stage, fixed-order scheme as the LayerNorm
+// dgamma/dbeta: block (256-column group, row split), 32 column vectors x 8 row
+// lanes, kRowUnroll rows in flight per lane; the split partials are summed in
+// split order.  kGelu: the tensor summed is the GELU backward of the MLP's
+// first linear, computed here and written out as well:
+//   pre = h + b (fp32), dh = dy * gelu'(pre) rounded to bf16, sum the rounded dh
+// (torch's gelu_backward + bias-grad arithmetic, tanh approximation).
+constexpr int kRowUnroll = 4;
+constexpr float kGeluBeta = 0.7978845608028654f;  // sqrt(2 / pi)
+constexpr float kGeluKappa = 0.044715f;
+
+// tanh(u) = 1 - 2 / (exp(2u) + 1) on the SFU (ex2 + rcp): absolute error ~1e-7,
+// far below a bf16 ulp of the outputs; libm tanhf made these kernels
+// issue-bound (2.9 TB/s) instead of HBM-bound.
+__device__ __forceinline__ float fast_tanh(float u) {
+  return 1.0f - __fdividef(2.0f, __expf(2.0f * u) + 1.0f);
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float inner = kGeluBeta * (x + kGeluKappa * x * x * x);
+  return 0.5f * x * (1.0f + fast_tanh(inner));
+}
+
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float x2 = x * x;
+  const float t = fast_tanh(kGeluBeta * (x + kGeluKappa * x2 * x));
+  const float left = 0.5f * x, right = 1.0f + t;
+  return 0.5f * right + left * (1.0f - t * t) * kGeluBeta * (1.0f + 3.0f * kGeluKappa * x2);
+}
+
+template <bool kGelu>
+__global__ void __launch_bounds__(kColThreads * kRowLanes) colsum_partial_kernel(
+    std::int64_t rows, int cols, int splits, const uint4* __restrict__ dy, const uint4* __restrict__ h,
+    const uint4* __restrict__ bias, uint4* __restrict__ dh, float* __restrict__ part) {
+  __shared__ float red[kRowLanes][kColThreads * 8 + 1];
+  const int cv = blockIdx.x * kColThreads + (threadIdx.x % kColThreads);
+  const int rl = threadIdx.x / kColThreads;
+  const int vpr = cols / 8;  // 16-byte vectors per row
+  const std::int64_t per = (rows + splits - 1) / splits;
+  const std::int64_t r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  float bf[8];
+  if (kGelu && cv < vpr) unpack8(__ldg(bias + cv), bf);
+  if (cv < vpr) {
+    std::int64_t r = r0 + rl;
+    for (; r + (kRowUnroll - 1) * kRowLanes < r1; r += kRowUnroll * kRowLanes) {
+      uint4 q[kRowUnroll], hq[kRowUnroll];
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const std::int64_t i = (r + u * kRowLanes) * vpr + cv;
+        q[u] = __ldcs(dy + i);
+        if (kGelu) hq[u] = __ldcs(h + i);
+      }
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        float d[8];
+        unpack8(q[u], d);
+        if (kGelu) {
+          float hf[8];
+          unpack8(hq[u], hf);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) d[e] *= gelu_tanh_grad(hf[e] + bf[e]);
+          const uint4 o = pack8(d);
+          __stcs(dh + (r + u * kRowLanes) * vpr + cv, o);
+          unpack8(o, d);  // sum what was stored (bf16-rounded), like gelu_backward then sum
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += d[e];
+      }
+    }
+    for (; r < r1; r += kRowLanes) {
+      const std::int64_t i = r * vpr + cv;
+      float d[8];
+      unpack8(__ldcs(dy + i), d);
+      if (kGelu) {
+        float hf[8];
+        unpack8(__ldcs(h + i), hf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d[e] *= gelu_tanh_grad(hf[e] + bf[e]);
+        const uint4 o = pack8(d);
+        __stcs(dh + i, o);
+        unpack8(o, d);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += d[e];
+    }
+  }
+  const int c = threadIdx.x % kColThreads;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red[rl][c * 8 + e] = acc[e];
+  __syncthreads();
+  for (int col = threadIdx.x; col < kColThreads * 8; col += blockDim.x) {
+    float sacc = 0.f;
+#pragma unroll
+    for (int l = 0; l < kRowLanes; ++l) sacc += red[l][col];
+    const int gcol = blockIdx.x * kColThreads * 8 + col;
+    if (gcol < cols) part[static_cast<std::int64_t>(blockIdx.y) * cols + gcol] = sacc;
+  }
+}
+
+__global__ void colsum_final_kernel(int cols, int splits, const float* __restrict__ part,
+                                    __nv_bfloat16* __restrict__ out) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= cols) return;
+  float s = 0.f;
+  for (int k = 0; k < splits; ++k) s += part[static_cast<std::int64_t>(k) * cols + col];  // fixed order
+  out[col] = __float2bfloat16_rn(s);
+}
+
+// y = gelu(h + b): the MLP's first linear runs without its bias epilogue and the
+// bias add is fused here (one read of h, one write of y).
+__global__ void __launch_bounds__(256) bias_gelu_fwd_kernel(std::int64_t nvec, int vpr,
+                                                            const uint4* __restrict__ h,
+                                                            const uint4* __restrict__ bias,
+                                                            uint4* __restrict__ y) {
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + step < nvec; i += 2 * step) {
+    const uint4 qa = __ldcs(h + i), qb = __ldcs(h + i + step);
+    float a[8], b[8], ba[8], bb[8];
+    unpack8(qa, a);
+    unpack8(qb, b);
+    unpack8(__ldg(bias + i % vpr), ba);
+    unpack8(__ldg(bias + (i + step) % vpr), bb);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      a[e] = gelu_tanh(a[e] + ba[e]);
+      b[e] = gelu_tanh(b[e] + bb[e]);
+    }
+    __stcs(y + i, pack8(a));
+    __stcs(y + i + step, pack8(b));
+  }
+  for (; i < nvec; i += step) {
+    float a[8], ba[8];
+    unpack8(__ldcs(h + i), a);
+    unpack8(__ldg(bias + i % vpr), ba);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] = gelu_tanh(a[e] + ba[e]);
+    __stcs(y + i, pack8(a));
+  }
+}
+
+// ------------------------------------------------------------ cross-entropy
+// Mean cross-entropy over rows of bf16 logits [rows x V] (V a multiple of 8),
+// fp32 arithmetic.  One block per row, kXentThreads threads:
+//   fwd  one read of the row: per-thread online (max, sum exp) over 16-byte
+//        vectors, merged across the block; lse[row] and loss[row] = lse - x[label]
+//   bwd  one read + one write: dx = (exp(x - lse) - [c == label]) * scale[0]
+// label < 0 = ignored row (loss 0, gradient 0).  Replaces logits.float() +
+// log_softmax + nll (fp32 copies of the whole logits matrix) of the head.
+constexpr int kXentThreads = 512;
+
+__device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  if (mn == -INFINITY) return;
+  s = s * __expf(m - mn) + s2 * __expf(m2 - mn);
+  m = mn;
+}
+
+__global__ void __launch_bounds__(kXentThreads) xent_fwd_kernel(int vpr, const uint4* __restrict__ x,
+                                                                const std::int64_t* __restrict__ labels,
+                                                                float* __restrict__ loss, float* __restrict__ lse) {
+  __shared__ float sm[kXentThreads / 32], ss[kXentThreads / 32];
+  const std::int64_t row = blockIdx.x;
+  const uint4* xr = x + row * vpr;
+  float m = -INFINITY, s = 0.f;
+  int i = threadIdx.x;
+  for (; i + kXentThreads < vpr; i += 2 * kXentThreads) {
+    float a[8], b[8];
+    unpack8(__ldcs(xr + i), a);
+    unpack8(__ldcs(xr + i + kXentThreads), b);
+    float lm = a[0];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) lm = fmaxf(lm, fmaxf(a[e], b[e]));
+    const float mn = fmaxf(m, lm);
+    float t = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) t += __expf(a[e] - mn) + __expf(b[e] - mn);
+    s = s * __expf(m - mn) + t;
+    m = mn;
+  }
+  for (; i < vpr; i += kXentThreads) {
+    float a[8];
+    unpack8(__ldcs(xr + i), a);
+    float lm = a[0];
+#pragma unroll
+    for (int e = 1; e < 8; ++e) lm = fmaxf(lm, a[e]);
+    const float mn = fmaxf(m, lm);
+    float t = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) t += __expf(a[e] - mn);
+    s = s * __expf(m - mn) + t;
+    m = mn;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(kFull, m, o), s2 = __shfl_xor_sync(kFull, s, o);
+    ms_merge(m, s, m2, s2);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sm[warp] = m;
+    ss[warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = sm[0], Ssum = ss[0];
+    for (int w = 1; w < kXentThreads / 32; ++w) ms_merge(M, Ssum, sm[w], ss[w]);  // fixed order
+    const float l = M + logf(Ssum);
+    lse[row] = l;
+    const std::int64_t lab = labels[row];
+    const float xl = lab >= 0 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xr)[lab]) : 0.f;
+    loss[row] = lab >= 0 ? l - xl : 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(kXentThreads) xent_bwd_kernel(int vpr, const uint4* __restrict__ x,
+                                                                const std::int64_t* __restrict__ labels,
+                                                                const float* __restrict__ lse,
+                                                                const float* __restrict__ scale,
+                                                                uint4* __restrict__ dx) {
+  const std::int64_t row = blockIdx.x;
+  const std::int64_t lab = labels[row];
+  const float l = lse[row], sc = lab >= 0 ? __ldg(scale) : 0.f;
+  const uint4* xr = x + row * vpr;
+  uint4* dr = dx + row * vpr;
+  for (int i = threadIdx.x; i < vpr; i += kXentThreads) {
+    float a[8];
+    unpack8(__ldcs(xr + i), a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float p = __expf(a[e] - l);
+      a[e] = (p - (static_cast<std::int64_t>(i) * 8 + e == lab ? 1.0f : 0.0f)) * sc;
+    }
+    __stcs(dr + i, pack8(a));
+  }
+}
+
+// --------------------------------------------------------- Llama: RoPE, SwiGLU
+// Rotary embedding of x [batch, seq, heads, dim] (bf16, contiguous): pairs
+// (2i, 2i+1) rotated by pos * base^(-2i/dim), angles from fp32 cos / sin tables
+// [seq, dim/2]; sign = -1 applies the inverse rotation (the backward).  One
+// 16-byte vector (4 pairs) per thread, fp32 arithmetic, one rounding.
+__global__ void __launch_bounds__(256) rope_kernel(std::int64_t nvec, int seq, int heads, int dim,
+                                                   const uint4* __restrict__ x, const float* __restrict__ cs,
+                                                   const float* __restrict__ sn, float sign,
+                                                   uint4* __restrict__ y) {
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  const int vrow = heads * dim / 8;  // vectors per token
+  const int vdim = dim / 8;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += step) {
+    const std::int64_t tok = i / vrow;
+    const int pos = static_cast<int>(tok % seq);
+    const int d0 = static_cast<int>(i % vdim) * 4;  // first pair index
+    const float4 c = __ldg(reinterpret_cast<const float4*>(cs + static_cast<std::int64_t>(pos) * (dim / 2) + d0));
+    const float4 s4 = __ldg(reinterpret_cast<const float4*>(sn + static_cast<std::int64_t>(pos) * (dim / 2) + d0));
+    const float cc[4] = {c.x, c.y, c.z, c.w};
+    const float ss[4] = {sign * s4.x, sign * s4.y, sign * s4.z, sign * s4.w};
+    float v[8], o[8];
+    unpack8(__ldcs(x + i), v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      o[2 * k] = v[2 * k] * cc[k] - v[2 * k + 1] * ss[k];
+      o[2 * k + 1] = v[2 * k] * ss[k] + v[2 * k + 1] * cc[k];
+    }
+    __stcs(y + i, pack8(o));
+  }
+}
+
+// SwiGLU y = silu(g) * u over [rows x f] (g, u with their own row strides, in
+// 16-byte vectors, so one [rows x 2f] gate|up GEMM output feeds it directly).
+__device__ __forceinline__ float sigmoid_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+
+__global__ void __launch_bounds__(256) swiglu_fwd_kernel(std::int64_t rows, int fv, const uint4* __restrict__ g,
+                                                         std::int64_t gs, const uint4* __restrict__ u,
+                                                         std::int64_t us, uint4* __restrict__ y) {
+  const std::int64_t n = rows * fv;
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += step) {
+    const std::int64_t r = i / fv, c = i % fv;
+    float a[8], b[8];
+    unpack8(__ldcs(g + r * gs + c), a);
+    unpack8(__ldcs(u + r * us + c), b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] = a[e] * sigmoid_fast(a[e]) * b[e];
+    __stcs(y + i, pack8(a));
+  }
+}
+
+// dg = dy * u * silu'(g), du = dy * silu(g);  silu'(g) = s (1 + g (1 - s)), s = sigmoid(g)
+__global__ void __launch_bounds__(256) swiglu_bwd_kernel(std::int64_t rows, int fv, const uint4* __restrict__ dy,
+                                                         const uint4* __restrict__ g, std::int64_t gs,
+                                                         const uint4* __restrict__ u, std::int64_t us,
+                                                         uint4* __restrict__ dg, std::int64_t dgs,
+                                                         uint4* __restrict__ du, std::int64_t dus) {
+  const std::int64_t n = rows * fv;
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += step) {
+    const std::int64_t r = i / fv, c = i % fv;
+    float d[8], a[8], b[8], og[8], ou[8];
+    unpack8(__ldcs(dy + i), d);
+    unpack8(__ldcs(g + r * gs + c), a);
+    unpack8(__ldcs(u + r * us + c), b);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float sg = sigmoid_fast(a[e]);
+      ou[e] = d[e] * a[e] * sg;
+      og[e] = d[e] * b[e] * sg * (1.0f + a[e] * (1.0f - sg));
+    }
+    __stcs(dg + r * dgs + c, pack8(og));
+    __stcs(du + r * dus + c, pack8(ou));
+  }
+}
+
 }  // namespace
 
 // the row lives in registers: 8 x h/256 floats per lane (h <= 2048)
@@ -256,6 +580,103 @@ cudaError_t launch_layernorm_bwd(std::int64_t rows, int h, const void* dy, const
                                                            static_cast<__nv_bfloat16*>(dw),
                                                            static_cast<__nv_bfloat16*>(db));
   }
+  return cudaGetLastError();
+}
+
+int colsum_splits(std::int64_t rows, int cols) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int groups = (cols / 8 + kColThreads - 1) / kColThreads;
+  const std::int64_t want = (4LL * sms + groups - 1) / groups;
+  const std::int64_t cap = std::max<std::int64_t>(1, rows / (kRowLanes * kRowUnroll));
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>({want, cap, 1024})));
+}
+
+cudaError_t launch_colsum(std::int64_t rows, int cols, const void* dy, void* out, float* part, int splits,
+                          cudaStream_t s) {
+  if (cols % 8 || splits < 1 || rows < 1) return cudaErrorInvalidValue;
+  const dim3 g((cols / 8 + kColThreads - 1) / kColThreads, splits);
+  colsum_partial_kernel<false><<<g, kColThreads * kRowLanes, 0, s>>>(rows, cols, splits,
+                                                                     static_cast<const uint4*>(dy), nullptr,
+                                                                     nullptr, nullptr, part);
+  colsum_final_kernel<<<(cols + 255) / 256, 256, 0, s>>>(cols, splits, part, static_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bias_gelu_fwd(std::int64_t rows, int cols, const void* h, const void* b, void* y,
+                                 cudaStream_t s) {
+  if (cols % 8 || rows < 1) return cudaErrorInvalidValue;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const std::int64_t nvec = rows * (cols / 8);
+  const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((nvec + 511) / 512, 8LL * sms)));
+  bias_gelu_fwd_kernel<<<grid, 256, 0, s>>>(nvec, cols / 8, static_cast<const uint4*>(h),
+                                            static_cast<const uint4*>(b), static_cast<uint4*>(y));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bias_gelu_bwd(std::int64_t rows, int cols, const void* dy, const void* h, const void* b, void* dh,
+                                 void* db, float* part, int splits, cudaStream_t s) {
+  if (cols % 8 || splits < 1 || rows < 1) return cudaErrorInvalidValue;
+  const dim3 g((cols / 8 + kColThreads - 1) / kColThreads, splits);
+  colsum_partial_kernel<true><<<g, kColThreads * kRowLanes, 0, s>>>(
+      rows, cols, splits, static_cast<const uint4*>(dy), static_cast<const uint4*>(h),
+      static_cast<const uint4*>(b), static_cast<uint4*>(dh), part);
+  colsum_final_kernel<<<(cols + 255) / 256, 256, 0, s>>>(cols, splits, part, static_cast<__nv_bfloat16*>(db));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xent_fwd(std::int64_t rows, int V, const void* logits, const std::int64_t* labels, float* loss,
+                            float* lse, cudaStream_t s) {
+  if (V % 8 || rows < 1 || rows > 0x7fffffff) return cudaErrorInvalidValue;
+  xent_fwd_kernel<<<static_cast<unsigned>(rows), kXentThreads, 0, s>>>(V / 8, static_cast<const uint4*>(logits),
+                                                                       labels, loss, lse);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xent_bwd(std::int64_t rows, int V, const void* logits, const std::int64_t* labels,
+                            const float* lse, const float* scale, void* dlogits, cudaStream_t s) {
+  if (V % 8 || rows < 1 || rows > 0x7fffffff) return cudaErrorInvalidValue;
+  xent_bwd_kernel<<<static_cast<unsigned>(rows), kXentThreads, 0, s>>>(
+      V / 8, static_cast<const uint4*>(logits), labels, lse, scale, static_cast<uint4*>(dlogits));
+  return cudaGetLastError();
+}
+
+namespace {
+int elementwise_grid(std::int64_t nvec) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((nvec + 255) / 256, 8LL * sms)));
+}
+}  // namespace
+
+cudaError_t launch_rope(std::int64_t batch, int seq, int heads, int dim, const void* x, const float* cs,
+                        const float* sn, bool inverse, void* y, cudaStream_t s) {
+  if (dim % 8 || batch < 1 || seq < 1 || heads < 1) return cudaErrorInvalidValue;
+  const std::int64_t nvec = batch * seq * static_cast<std::int64_t>(heads) * dim / 8;
+  rope_kernel<<<elementwise_grid(nvec), 256, 0, s>>>(nvec, seq, heads, dim, static_cast<const uint4*>(x), cs, sn,
+                                                     inverse ? -1.0f : 1.0f, static_cast<uint4*>(y));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_swiglu_fwd(std::int64_t rows, int f, const void* g, std::int64_t g_stride, const void* u,
+                              std::int64_t u_stride, void* y, cudaStream_t s) {
+  if (f % 8 || g_stride % 8 || u_stride % 8 || rows < 1) return cudaErrorInvalidValue;
+  swiglu_fwd_kernel<<<elementwise_grid(rows * (f / 8)), 256, 0, s>>>(
+      rows, f / 8, static_cast<const uint4*>(g), g_stride / 8, static_cast<const uint4*>(u), u_stride / 8,
+      static_cast<uint4*>(y));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_swiglu_bwd(std::int64_t rows, int f, const void* dy, const void* g, std::int64_t g_stride,
+                              const void* u, std::int64_t u_stride, void* dg, std::int64_t dg_stride, void* du,
+                              std::int64_t du_stride, cudaStream_t s) {
+  if (f % 8 || g_stride % 8 || u_stride % 8 || dg_stride % 8 || du_stride % 8 || rows < 1)
+    return cudaErrorInvalidValue;
+  swiglu_bwd_kernel<<<elementwise_grid(rows * (f / 8)), 256, 0, s>>>(
+      rows, f / 8, static_cast<const uint4*>(dy), static_cast<const uint4*>(g), g_stride / 8,
+      static_cast<const uint4*>(u), u_stride / 8, static_cast<uint4*>(dg), dg_stride / 8, static_cast<uint4*>(du),
+      du_stride / 8);
   return cudaGetLastError();
 }
 

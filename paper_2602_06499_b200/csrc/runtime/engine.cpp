@@ -323,12 +323,18 @@ void Engine::build_layouts(const std::uint8_t* const* masks) {
                                   std::to_string(lr.L.dev.pt * V_) + " trainable params, trainable_fraction gives " +
                                   std::to_string(trainable));
     const std::size_t wb = lr.L.bits.size() * sizeof(std::uint32_t);
+    const std::size_t tw = lr.L.sparse_t() ? lr.L.twords.size() * sizeof(std::uint32_t) : 0;
     CK(cudaMalloc(&lr.d_bits, wb));
-    CK(cudaMalloc(&lr.d_tpre, wb));
+    CK(cudaMalloc(&lr.d_tpre, wb + tw));  // prefix, then the active trainable words (sparse masks)
     CK(cudaMemcpy(lr.d_bits, lr.L.bits.data(), wb, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(lr.d_tpre, lr.L.tpre.data(), wb, cudaMemcpyHostToDevice));
     lr.L.dev.bits = lr.d_bits;
     lr.L.dev.tpre = lr.d_tpre;
+    if (tw) {
+      CK(cudaMemcpy(lr.d_tpre + lr.L.bits.size(), lr.L.twords.data(), tw, cudaMemcpyHostToDevice));
+      lr.L.dev.twords = lr.d_tpre + lr.L.bits.size();
+      lr.L.dev.ntwords = static_cast<std::int64_t>(lr.L.twords.size());
+    }
     lr.has_t = lr.L.dev.pt > 0;
     lr.has_f = lr.L.dev.pf > 0;
     lr.off_t = arena_t_;

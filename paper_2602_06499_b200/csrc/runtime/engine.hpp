@@ -93,6 +93,8 @@ class Engine {
   void set_timing(bool on) { timing_ = on; }
   void kernel_stats(fcdp_kernel_stats* out, bool reset);
   void set_trace(bool on) { trace_ = on; }
+  void set_nic_log(bool on) { nic_->set_log(on); }
+  std::size_t nic_log(WireRecord* out, std::size_t capacity) { return nic_->take_log(out, capacity); }
   std::uint32_t trace(float* begin_ms, float* end_ms, std::uint32_t capacity);
 
   void read_shard(int layer, bool frozen, void* host, std::size_t bytes);

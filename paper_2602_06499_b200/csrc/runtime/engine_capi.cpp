@@ -124,6 +124,23 @@ int fcdp_engine_trace(fcdp_engine* e, float* begin_ms, float* end_ms, uint32_t c
   return guarded([&] { *count = E(e).trace(begin_ms, end_ms, capacity); });
 }
 
+int fcdp_engine_set_nic_log(fcdp_engine* e, int32_t on) { return guarded([&] { E(e).set_nic_log(on != 0); }); }
+
+int fcdp_engine_nic_log(fcdp_engine* e, uint64_t* start_ns, uint64_t* end_ns, uint64_t* bytes, int32_t* kind,
+                        uint32_t capacity, uint32_t* count) {
+  return guarded([&] {
+    std::vector<fcdp::WireRecord> v(capacity);
+    const std::size_t n = E(e).nic_log(v.data(), capacity);
+    for (std::size_t i = 0; i < n; ++i) {
+      start_ns[i] = v[i].start_ns;
+      end_ns[i] = v[i].end_ns;
+      bytes[i] = v[i].bytes;
+      kind[i] = v[i].kind;
+    }
+    *count = static_cast<uint32_t>(n);
+  });
+}
+
 int fcdp_numa_parse_cpulist(const char* list, int32_t* out, int32_t capacity, int32_t* count) {
   return guarded([&] {
     const std::vector<int> v = fcdp::parse_cpulist(list ? list : "");

@@ -1,5 +1,6 @@
 #include "runtime/nic.hpp"
 
+#include <algorithm>
 #include <chrono>
 
 namespace fcdp {
@@ -26,6 +27,20 @@ void NicEmulator::submit(const NicJob& job) {
   cv_.notify_all();
 }
 
+void NicEmulator::set_log(bool on) {
+  std::lock_guard<std::mutex> g(mu_);
+  log_on_ = on;
+  if (!on) log_.clear();
+}
+
+std::size_t NicEmulator::take_log(WireRecord* out, std::size_t capacity) {
+  std::lock_guard<std::mutex> g(mu_);
+  const std::size_t n = std::min(capacity, log_.size());
+  std::copy(log_.begin(), log_.begin() + static_cast<std::ptrdiff_t>(n), out);
+  log_.erase(log_.begin(), log_.begin() + static_cast<std::ptrdiff_t>(n));
+  return n;
+}
+
 std::uint64_t NicEmulator::published(int cls) const {
   return *shm_.flag(rank_, cls == 0 ? kAgTxReady : kRsTxReady);
 }
@@ -45,6 +60,7 @@ void NicEmulator::loop() {
             pacing_ && bytes_per_ns_ > 0 ? static_cast<std::uint64_t>(j.wire_bytes / bytes_per_ns_) : 0;
         const std::uint64_t finish = ns ? shm_.reserve_nic(node_, ns) : SharedBlock::now_ns();
         shm_.add(rank_, kNicBusyNs, ns);
+        if (log_on_) log_.push_back({finish - ns, finish, j.wire_bytes, static_cast<std::int32_t>(j.counter), node_});
         flight_[c].push_back({j, finish});
         queue_[c].pop_front();
         idle = false;

@@ -12,6 +12,7 @@
 #include <deque>
 #include <mutex>
 #include <thread>
+#include <vector>
 
 #include "runtime/shm.hpp"
 
@@ -27,12 +28,24 @@ struct NicJob {
   Counter counter;       // which tx counter to charge
 };
 
+// One paced payload on the emulated wire (the NIC bandwidth profile, PAPER.md
+// Fig. 10 "peak inter-node network bandwidth during forward and backward"):
+// [start_ns, end_ns) of steady_clock on the node's NIC clock, its bytes and
+// the traffic kind (the tx Counter it is charged to).
+struct WireRecord {
+  std::uint64_t start_ns, end_ns, bytes;
+  std::int32_t kind, node;
+};
+
 class NicEmulator {
  public:
   NicEmulator(SharedBlock& shm, int rank, int node, double bytes_per_s, bool pacing);
   ~NicEmulator();
   void submit(const NicJob& job);
   std::uint64_t published(int cls) const;
+  // Wire log: off by default; take_log drains what was recorded since the last call.
+  void set_log(bool on);
+  std::size_t take_log(WireRecord* out, std::size_t capacity);
 
  private:
   void loop();
@@ -49,6 +62,8 @@ class NicEmulator {
   std::deque<NicJob> queue_[2];
   std::deque<Flight> flight_[2];
   bool stop_ = false;
+  bool log_on_ = false;
+  std::vector<WireRecord> log_;
   std::thread thread_;
 };
 

@@ -232,6 +232,229 @@ def _make_layernorm():
     return LayerNormFn
 
 
+_FNS = None
+
+
+def _fused_ok(*ts) -> bool:
+    import torch
+    return all(t.is_cuda and t.dtype == torch.bfloat16 for t in ts)
+
+
+def _fns():
+    """autograd Functions over libfcdp's driving-model kernels (model_kernels.cu)."""
+    global _FNS
+    if _FNS is not None:
+        return _FNS
+    import ctypes as C
+    import torch
+    from ._capi import check, lib
+
+    P = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+    S = lambda dev: C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+    def bias_grad(dy2):
+        rows, cols = dy2.shape
+        splits = lib().fcdp_colsum_splits(rows, cols)
+        part = torch.empty(splits * cols, dtype=torch.float32, device=dy2.device)
+        db = torch.empty(cols, dtype=dy2.dtype, device=dy2.device)
+        check(lib().fcdp_bias_grad(rows, cols, P(dy2), P(db), P(part), splits, S(dy2.device)))
+        return db
+
+    class LinearBias(torch.autograd.Function):
+        """y = x W^T + b (cuBLAS, bias in the GEMM epilogue); backward: the two
+        cuBLAS GEMMs torch's addmm backward issues, and db by fcdp_bias_grad
+        (torch's column reduction ran at ~2 TB/s)."""
+
+        @staticmethod
+        def forward(ctx, x, w, b):
+            ctx.save_for_backward(x, w)
+            return torch.nn.functional.linear(x, w, b)
+
+        @staticmethod
+        def backward(ctx, dy):
+            x, w = ctx.saved_tensors
+            dy2 = dy.reshape(-1, dy.shape[-1])
+            if not dy2.is_contiguous():
+                dy2 = dy2.contiguous()
+            dx = dw = db = None
+            if ctx.needs_input_grad[0]:
+                dx = dy2.mm(w).view(x.shape)
+            if ctx.needs_input_grad[1]:
+                dw = dy2.t().mm(x.reshape(-1, x.shape[-1]))
+            if ctx.needs_input_grad[2]:
+                db = bias_grad(dy2)
+            return dx, dw, db
+
+    class BiasGelu(torch.autograd.Function):
+        """y = gelu_tanh(h + b) in one pass; backward dh and db = sum_r dh in one pass."""
+
+        @staticmethod
+        def forward(ctx, h, b):
+            hc = h.contiguous()
+            cols = hc.shape[-1]
+            rows = hc.numel() // cols
+            y = torch.empty_like(hc)
+            check(lib().fcdp_bias_gelu_fwd(rows, cols, P(hc), P(b), P(y), S(hc.device)))
+            ctx.save_for_backward(hc, b)
+            return y
+
+        @staticmethod
+        def backward(ctx, dy):
+            hc, b = ctx.saved_tensors
+            cols = hc.shape[-1]
+            rows = hc.numel() // cols
+            dyc = dy.contiguous()
+            dh = torch.empty_like(hc)
+            splits = lib().fcdp_colsum_splits(rows, cols)
+            part = torch.empty(splits * cols, dtype=torch.float32, device=hc.device)
+            db = torch.empty(cols, dtype=b.dtype, device=b.device)
+            check(lib().fcdp_bias_gelu_bwd(rows, cols, P(dyc), P(hc), P(b), P(dh), P(db), P(part), splits,
+                                           S(hc.device)))
+            return dh, (db if ctx.needs_input_grad[1] else None)
+
+    class CrossEntropy(torch.autograd.Function):
+        """Mean cross-entropy of bf16 logits in fp32 without an fp32 copy of the
+        logits: one read forward, one read + one write backward."""
+
+        @staticmethod
+        def forward(ctx, logits, labels):
+            lc = logits.contiguous()
+            V = lc.shape[-1]
+            rows = lc.numel() // V
+            lab = labels.reshape(-1).contiguous()
+            loss = torch.empty(rows, dtype=torch.float32, device=lc.device)
+            lse = torch.empty_like(loss)
+            check(lib().fcdp_xent_fwd(rows, V, P(lc), P(lab), P(loss), P(lse), S(lc.device)))
+            valid = (lab >= 0).sum().clamp_min(1).to(torch.float32)
+            ctx.save_for_backward(lc, lab, lse, valid)
+            return loss.sum() / valid
+
+        @staticmethod
+        def backward(ctx, g):
+            lc, lab, lse, valid = ctx.saved_tensors
+            V = lc.shape[-1]
+            rows = lc.numel() // V
+            scale = (g.float() / valid).reshape(1).contiguous()
+            dl = torch.empty_like(lc)
+            check(lib().fcdp_xent_bwd(rows, V, P(lc), P(lab), P(lse), P(scale), P(dl), S(lc.device)))
+            return dl, None
+
+    tables = {}
+
+    def rope_tables(seq, dim, device, base=10000.0):
+        key = (seq, dim, device, base)
+        if key not in tables:
+            pos = torch.arange(seq, device=device, dtype=torch.float32)
+            inv = base ** (-torch.arange(0, dim, 2, device=device, dtype=torch.float32) / dim)
+            ang = pos[:, None] * inv[None, :]
+            tables[key] = (ang.cos().contiguous(), ang.sin().contiguous())
+        return tables[key]
+
+    class Rope(torch.autograd.Function):
+        """Rotary embedding of [b, s, nh, d] in one pass (fp32 tables); the
+        backward is the inverse rotation."""
+
+        @staticmethod
+        def forward(ctx, x):
+            xc = x.contiguous()
+            b, sq, nh, d = xc.shape
+            cs, sn = rope_tables(sq, d, xc.device)
+            y = torch.empty_like(xc)
+            check(lib().fcdp_rope(b, sq, nh, d, P(xc), P(cs), P(sn), 0, P(y), S(xc.device)))
+            ctx.shape = (b, sq, nh, d)
+            return y
+
+        @staticmethod
+        def backward(ctx, dy):
+            b, sq, nh, d = ctx.shape
+            dyc = dy.contiguous()
+            cs, sn = rope_tables(sq, d, dyc.device)
+            dx = torch.empty_like(dyc)
+            check(lib().fcdp_rope(b, sq, nh, d, P(dyc), P(cs), P(sn), 1, P(dx), S(dyc.device)))
+            return dx
+
+    class GateUpSwiGLU(torch.autograd.Function):
+        """silu(m Wg^T) * (m Wu^T) with Wg, Wu adjacent in the layer buffer: ONE
+        [rows x 2f] GEMM, one fused SwiGLU pass; backward one fused pass giving
+        d[gate|up], then one GEMM each for dm and (if trainable) d[Wg|Wu]."""
+
+        @staticmethod
+        def forward(ctx, m, wg, wu):
+            f, hdim = wg.shape
+            w2 = torch.as_strided(wg, (2 * f, hdim), (hdim, 1))
+            m2 = m.reshape(-1, hdim)
+            h2 = m2.mm(w2.t())
+            rows = h2.shape[0]
+            y = torch.empty(rows, f, dtype=m.dtype, device=m.device)
+            check(lib().fcdp_swiglu_fwd(rows, f, P(h2), 2 * f, C.c_void_p(h2.data_ptr() + f * h2.element_size()), 2 * f,
+                                        P(y), S(m.device)))
+            ctx.save_for_backward(m, wg, wu, h2)
+            return y.view(*m.shape[:-1], f)
+
+        @staticmethod
+        def backward(ctx, dy):
+            m, wg, wu, h2 = ctx.saved_tensors
+            f, hdim = wg.shape
+            rows = h2.shape[0]
+            dyc = dy.reshape(rows, f).contiguous()
+            dh2 = torch.empty_like(h2)
+            off = f * h2.element_size()
+            check(lib().fcdp_swiglu_bwd(rows, f, P(dyc), P(h2), 2 * f, C.c_void_p(h2.data_ptr() + off), 2 * f,
+                                        P(dh2), 2 * f, C.c_void_p(dh2.data_ptr() + off), 2 * f, S(m.device)))
+            w2 = torch.as_strided(wg, (2 * f, hdim), (hdim, 1))
+            dm = dwg = dwu = None
+            if ctx.needs_input_grad[0]:
+                dm = dh2.mm(w2).view(m.shape)
+            if ctx.needs_input_grad[1] or ctx.needs_input_grad[2]:
+                dw2 = dh2.t().mm(m.reshape(-1, hdim))
+                dwg, dwu = dw2[:f], dw2[f:]
+            return dm, dwg, dwu
+
+    _FNS = (LinearBias, BiasGelu, CrossEntropy, Rope, GateUpSwiGLU)
+    return _FNS
+
+
+def _adjacent(a, b) -> bool:
+    """b starts where a ends in the same storage (consecutive tensors of a layer buffer)."""
+    return (a.is_contiguous() and b.is_contiguous() and a.untyped_storage().data_ptr() == b.untyped_storage().data_ptr()
+            and b.data_ptr() == a.data_ptr() + a.numel() * a.element_size() and a.shape == b.shape)
+
+
+def _swiglu_mlp(m, wg, wu):
+    import torch.nn.functional as F
+    if _fused_ok(m, wg, wu) and wg.shape[0] % 8 == 0 and _adjacent(wg, wu):
+        return _fns()[4].apply(m, wg, wu)
+    return F.silu(F.linear(m, wg)) * F.linear(m, wu)
+
+
+def _rope_fn(x):
+    if _fused_ok(x) and x.shape[-1] % 8 == 0:
+        return _fns()[3].apply(x)
+    return _rope(x)
+
+
+def _linear_bias(x, w, b):
+    import torch.nn.functional as F
+    if _fused_ok(x, w, b) and w.shape[0] % 8 == 0:
+        return _fns()[0].apply(x, w, b)
+    return F.linear(x, w, b)
+
+
+def _mlp_gelu(m, w, b):
+    """gelu_tanh(m W^T + b): the GEMM without its bias, bias + GELU fused."""
+    import torch.nn.functional as F
+    if _fused_ok(m, w, b) and w.shape[0] % 8 == 0:
+        return _fns()[1].apply(F.linear(m, w), b)
+    return F.gelu(F.linear(m, w, b), approximate="tanh")
+
+
+def _cross_entropy(logits, labels):
+    import torch.nn.functional as F
+    if _fused_ok(logits) and logits.shape[-1] % 8 == 0:
+        return _fns()[2].apply(logits.reshape(-1, logits.shape[-1]), labels.reshape(-1))
+    return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), labels.reshape(-1))
+
+
 def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=None):
     """Forward of one layer.  x: [b, s, h] (None for the embedding)."""
     import torch
@@ -248,11 +471,11 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         # q, k, v stay [b, s, nh, hd] in memory and reach SDPA as transposed views;
         # the output comes back in the same layout, so neither direction needs a
         # strided copy (tools/attn_layout_probe.py: 0.85 vs 1.29 ms per block fwd+bwd)
-        q, k, v = F.linear(a, p["qkv_w"], p["qkv_b"]).view(b, s, 3, nh, h // nh).unbind(2)
+        q, k, v = _linear_bias(a, p["qkv_w"], p["qkv_b"]).view(b, s, 3, nh, h // nh).unbind(2)
         o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), is_causal=True)
-        x = x + F.linear(o.transpose(1, 2).reshape(b, s, h), p["proj_w"], p["proj_b"])
+        x = x + _linear_bias(o.transpose(1, 2).reshape(b, s, h), p["proj_w"], p["proj_b"])
         m = _layer_norm(x, p["ln2_w"], p["ln2_b"])
-        return x + F.linear(F.gelu(F.linear(m, p["fc_w"], p["fc_b"]), approximate="tanh"), p["fc2_w"], p["fc2_b"])
+        return x + _linear_bias(_mlp_gelu(m, p["fc_w"], p["fc_b"]), p["fc2_w"], p["fc2_b"])
     if ldef.kind == "llama_block":
         b, s, _ = x.shape
         a = F.rms_norm(x, (h,), p["attn_norm"], eps=1e-5)
@@ -260,20 +483,23 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         def proj(name, inp):
             y = F.linear(inp, p[f"{name}_w"])
             if f"{name}_A" in p:
-                y = y + F.linear(F.linear(inp, p[f"{name}_A"]), p[f"{name}_B"])
+                # y + (x A^T) B^T with the add in the LoRA GEMM's epilogue (addmm, beta = 1)
+                xa = F.linear(inp, p[f"{name}_A"])
+                y = torch.addmm(y.reshape(-1, y.shape[-1]), xa.reshape(-1, xa.shape[-1]),
+                                p[f"{name}_B"].t()).view(y.shape)
             return y
-        q = _rope(proj("q", a).view(b, s, nh, h // nh)).transpose(1, 2)
-        k = _rope(proj("k", a).view(b, s, nh, h // nh)).transpose(1, 2)
+        q = _rope_fn(proj("q", a).view(b, s, nh, h // nh)).transpose(1, 2)
+        k = _rope_fn(proj("k", a).view(b, s, nh, h // nh)).transpose(1, 2)
         v = proj("v", a).view(b, s, nh, h // nh).transpose(1, 2)
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
         x = x + proj("o", o.transpose(1, 2).reshape(b, s, h))
         m = F.rms_norm(x, (h,), p["mlp_norm"], eps=1e-5)
-        return x + F.linear(F.silu(F.linear(m, p["gate_w"])) * F.linear(m, p["up_w"]), p["down_w"])
+        return x + F.linear(_swiglu_mlp(m, p["gate_w"], p["up_w"]), p["down_w"])
     if ldef.kind == "head":
         if "lnf_w" in p:
             a = _layer_norm(x, p["lnf_w"], p["lnf_b"])
         else:
             a = F.rms_norm(x, (h,), p["norm_w"], eps=1e-5)
         logits = F.linear(a, p["lm_w"])
-        return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), labels.reshape(-1))
+        return _cross_entropy(logits, labels)
     raise ValueError(ldef.kind)

@@ -181,6 +181,26 @@ class Engine:
         check(lib().fcdp_engine_trace(self._h, b, e, n, C.byref(cnt)))
         return [(ev, b[i], e[i]) for i, ev in enumerate(program.events[:cnt.value])]
 
+    def set_nic_log(self, on: bool) -> None:
+        check(lib().fcdp_engine_set_nic_log(self._h, int(on)))
+
+    def nic_log(self, capacity: int = 1 << 16) -> np.ndarray:
+        """Drain this rank's NIC wire log: structured array (start_ns, end_ns, bytes, kind)."""
+        st = np.zeros(capacity, np.uint64)
+        en = np.zeros(capacity, np.uint64)
+        by = np.zeros(capacity, np.uint64)
+        kd = np.zeros(capacity, np.int32)
+        cnt = C.c_uint32()
+        u64p = C.POINTER(C.c_uint64)
+        check(lib().fcdp_engine_nic_log(self._h, st.ctypes.data_as(u64p), en.ctypes.data_as(u64p),
+                                        by.ctypes.data_as(u64p), kd.ctypes.data_as(C.POINTER(C.c_int32)),
+                                        capacity, C.byref(cnt)))
+        n = cnt.value
+        out = np.zeros(n, dtype=[("start_ns", np.uint64), ("end_ns", np.uint64), ("bytes", np.uint64),
+                                 ("kind", np.int32)])
+        out["start_ns"], out["end_ns"], out["bytes"], out["kind"] = st[:n], en[:n], by[:n], kd[:n]
+        return out
+
     # ----------------------------------------------------------- readback
     def read_shard(self, layer: int, frozen: bool, nbytes: int) -> np.ndarray:
         out = np.zeros(nbytes, np.uint8)

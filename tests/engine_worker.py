@@ -69,6 +69,8 @@ def main():
     eng.set_compute(compute)
     if cfg.get("trace"):
         eng.set_trace(True)
+    if cfg.get("nic_log"):
+        eng.set_nic_log(True)
     states = S.init_param_states(model)
     dumps = []
     mut = cfg.get("mutate")
@@ -115,6 +117,8 @@ def main():
                                      for k, l, t in captures],
              "counters": eng.counters(), "host": {}, "grad": {}, "master": {}, "shard_t": {}, "shard_f": {},
              "retained": prog.layer_flags(model.num_layers())}
+        if cfg.get("nic_log"):
+            d["nic_log"] = eng.nic_log()
         if cfg.get("trace"):
             tr = eng.trace(prog)
             d["trace"] = [(e.id, int(e.kind), e.layer, list(e.deps), b, t) for e, b, t in tr]

@@ -57,13 +57,14 @@ def _masks(chunks_list, kind, seed=0):
 
 
 def run_job(tmp_path, N, g, strategy, eb=2, kind="dense", iters=3, chunks=(1000, 1537, 777), pacing=False,
-            use_ce=False, tau=0.0, capacity=0, stepwise=False, trace=False, mutate=None):
+            use_ce=False, tau=0.0, capacity=0, stepwise=False, trace=False, mutate=None, nic_log=False,
+            inter="ib100-rdma-measured"):
     world = N * g
     V = 16 // eb
-    cfg = {"N": N, "g": g, "world": world, "strategy": strategy, "eb": eb, "iters": iters, "seed": 0x5EED,
+    cfg = {"N": N, "g": g, "world": world, "inter": inter, "strategy": strategy, "eb": eb, "iters": iters, "seed": 0x5EED,
            "params": [c * V for c in chunks], "masks": _masks(chunks, kind), "shm": f"fcdp_test_{uuid.uuid4().hex[:12]}",
            "out": str(tmp_path), "pacing": pacing, "use_ce": use_ce, "tau": tau, "capacity": capacity,
-           "stepwise": stepwise, "trace": trace, "mutate": mutate}
+           "stepwise": stepwise, "trace": trace, "mutate": mutate, "nic_log": nic_log}
     procs = []
     for r in range(world):
         c = dict(cfg, rank=r)
@@ -165,6 +166,41 @@ def test_engine_even_shards_match_comm_volume(tmp_path, built):
     G = N * g
     cfg, dumps = run_job(tmp_path, N, g, "fcdp-comm", 2, "lora", chunks=(64 * G, 96 * G, 32 * G))
     check_job(cfg, dumps)
+
+
+@pytest.mark.parametrize("N,g,strategy", [(2, 2, "zero3"), (2, 2, "fcdp"), (4, 1, "fcdp-comm")])
+def test_engine_nic_wire_log(tmp_path, built, N, g, strategy):
+    """NIC bandwidth profile (Fig. 10) from the paced emulator's wire
+    log: per rank, the logged bytes of each kind equal the NIC counters; the
+    payloads of one node never overlap on its wire (one NIC per node,
+    topology.hpp:23-25) and each occupies bytes / B_nic of it; FCDP puts no
+    backward all-gather on the wire, ZeRO-3 does."""
+    _need_gpu()
+    cfg, dumps = run_job(tmp_path, N, g, strategy, 2, "lora" if strategy == "fcdp-comm" else "dense",
+                         pacing=True, nic_log=True, inter="eth10g-measured")
+    check_job(cfg, dumps)
+    from paper_2602_06499_b200 import shardsim as S
+    bw = S.make_topology(N, g, inter_preset="eth10g-measured").inter_node.bandwidth_bytes_per_s
+    kinds = {0: "nic_tx_fwd_ag", 1: "nic_tx_bwd_ag", 2: "nic_tx_rs", 15: "nic_tx_grad_sync"}
+    for it in range(cfg["iters"]):
+        bwd_ag = 0
+        for n in range(N):
+            recs = np.concatenate([dumps[n * g + j][it]["nic_log"] for j in range(g)])
+            for j in range(g):
+                d = dumps[n * g + j][it]
+                log = d["nic_log"]
+                assert set(np.unique(log["kind"]).tolist()) <= set(kinds)
+                for k, name in kinds.items():
+                    assert int(log["bytes"][log["kind"] == k].sum()) == d["counters"][name], (n, j, name)
+            recs = np.sort(recs, order="start_ns")
+            dur = (recs["end_ns"] - recs["start_ns"]).astype(np.float64)
+            assert np.all(np.abs(dur - recs["bytes"] / bw * 1e9) <= 1.0 + 1e-6 * dur)
+            assert np.all(recs["start_ns"][1:] >= recs["end_ns"][:-1]), "two payloads overlap on one node's NIC"
+            bwd_ag += int(recs["bytes"][recs["kind"] == 1].sum())
+        if strategy == "zero3":
+            assert bwd_ag > 0
+        else:
+            assert bwd_ag == 0
 
 
 @pytest.mark.parametrize("N,g,strategy,kind", [(1, 1, "fcdp", "dense"), (1, 1, "fcdp-comm", "lora"),

@@ -1,9 +1,10 @@
-"""Driving-model LayerNorm kernels (libfcdp model_kernels.cu) against an fp32
-torch reference: forward y and backward dx, dgamma, dbeta for bf16 rows.
+"""Driving-model kernels (libfcdp model_kernels.cu) against fp32 torch
+references: LayerNorm forward / backward, bias gradients, bias + GELU forward /
+backward (+ bias gradient) and the fused cross-entropy, all on bf16 tensors.
 Tolerance: the error of the kernel's bf16 outputs against the fp32 reference
-must be within 1.5x of torch's own bf16 LayerNorm error plus one bf16 ulp
-scale (relative L2 <= 8e-3); the backward is deterministic (bit-identical
-across runs)."""
+must be within 1.5x of torch's own bf16 op's error, or within one bf16 ulp
+scale (relative L2 <= 8e-3); the cross-entropy loss (fp32) within 1e-5
+relative; reductions are deterministic (bit-identical across runs)."""
 import pytest
 
 torch = pytest.importorskip("torch")
@@ -46,3 +47,135 @@ def test_layernorm_matches_fp32(built, rows, h):
     x.grad = w.grad = b.grad = None
     _layer_norm(x, w, b).backward(dy)
     assert torch.equal(x.grad, dx1) and torch.equal(w.grad, dw1)
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    return torch.device("cuda", 0)
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 6144), (8192, 2048), (1000, 264), (5, 8), (37, 4096)])
+def test_bias_grad_matches_fp32(built, rows, cols):
+    from paper_2602_06499_b200.driving_model import _linear_bias
+    import torch.nn.functional as F
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(rows * 7 + cols)
+    k = 64
+    x = torch.randn(rows, k, device=dev, generator=g).to(torch.bfloat16).requires_grad_(True)
+    w = (0.1 * torch.randn(cols, k, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    b = (0.1 * torch.randn(cols, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    dy = torch.randn(rows, cols, device=dev, generator=g).to(torch.bfloat16)
+    xr, wr, br = (t.detach().float().requires_grad_(True) for t in (x, w, b))
+    F.linear(xr, wr, br).backward(dy.float())
+    xt, wt, bt = (t.detach().clone().requires_grad_(True) for t in (x, w, b))
+    yt = F.linear(xt, wt, bt)
+    yt.backward(dy)
+    y = _linear_bias(x, w, b)
+    y.backward(dy)
+    assert torch.equal(y, yt)  # same cuBLAS forward
+    for ours, theirs, ref, name in ((x.grad, xt.grad, xr.grad, "dx"), (w.grad, wt.grad, wr.grad, "dw"),
+                                    (b.grad, bt.grad, br.grad, "db")):
+        e_ours, e_torch = _rel(ours, ref), _rel(theirs, ref)
+        assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
+    db1 = b.grad.clone()
+    x.grad = w.grad = b.grad = None
+    _linear_bias(x, w, b).backward(dy)
+    assert torch.equal(b.grad, db1)
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 8192), (333, 1024), (4, 8)])
+def test_bias_gelu_matches_fp32(built, rows, cols):
+    from paper_2602_06499_b200.driving_model import _fns
+    import torch.nn.functional as F
+    dev = _dev()
+    BiasGelu = _fns()[1]
+    g = torch.Generator(device=dev).manual_seed(rows + 3 * cols)
+    h = (2 * torch.randn(rows, cols, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    b = (0.5 * torch.randn(cols, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    dy = torch.randn(rows, cols, device=dev, generator=g).to(torch.bfloat16)
+    hr, br = (t.detach().float().requires_grad_(True) for t in (h, b))
+    yr = F.gelu(hr + br, approximate="tanh")
+    yr.backward(dy.float())
+    ht, bt = (t.detach().clone().requires_grad_(True) for t in (h, b))
+    yt = F.gelu(ht + bt, approximate="tanh")
+    yt.backward(dy)
+    y = BiasGelu.apply(h, b)
+    y.backward(dy)
+    for ours, theirs, ref, name in ((y, yt, yr, "y"), (h.grad, ht.grad, hr.grad, "dh"), (b.grad, bt.grad, br.grad, "db")):
+        e_ours, e_torch = _rel(ours, ref), _rel(theirs, ref)
+        assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
+    db1 = b.grad.clone()
+    h.grad = b.grad = None
+    BiasGelu.apply(h, b).backward(dy)
+    assert torch.equal(b.grad, db1)
+
+
+@pytest.mark.parametrize("rows,V,ignore", [(8192, 50304, False), (100, 1024, True), (3, 8, False), (64, 32000, True)])
+def test_cross_entropy_matches_fp32(built, rows, V, ignore):
+    from paper_2602_06499_b200.driving_model import _cross_entropy
+    import torch.nn.functional as F
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(rows + V)
+    logits = (3 * torch.randn(rows, V, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    labels = torch.randint(0, V, (rows,), device=dev, generator=g)
+    if ignore:
+        labels[::3] = -100
+    lr_ = logits.detach().float().requires_grad_(True)
+    ref = F.cross_entropy(lr_, labels)
+    (ref * 0.5).backward()
+    loss = _cross_entropy(logits, labels)
+    (loss * 0.5).backward()
+    assert loss.dtype == torch.float32
+    assert abs(float(loss) - float(ref)) <= 1e-5 * abs(float(ref)), (float(loss), float(ref))
+    assert _rel(logits.grad, lr_.grad) <= 8e-3
+    if ignore:
+        assert torch.count_nonzero(logits.grad[::3]) == 0
+
+
+@pytest.mark.parametrize("b,s,nh,d", [(2, 2048, 32, 128), (3, 17, 4, 32), (1, 5, 1, 8)])
+def test_rope_matches_fp32(built, b, s, nh, d):
+    from paper_2602_06499_b200.driving_model import _rope, _rope_fn
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(b * s + nh * d)
+    x = torch.randn(b, s, nh, d, device=dev, generator=g).to(torch.bfloat16).requires_grad_(True)
+    dy = torch.randn(b, s, nh, d, device=dev, generator=g).to(torch.bfloat16)
+    xr = x.detach().float().requires_grad_(True)
+    yr = _rope(xr)
+    yr.backward(dy.float())
+    xt = x.detach().clone().requires_grad_(True)
+    yt = _rope(xt)  # torch's bf16 ops (the old path)
+    yt.backward(dy)
+    y = _rope_fn(x)
+    y.backward(dy)
+    for ours, theirs, ref, name in ((y, yt, yr, "y"), (x.grad, xt.grad, xr.grad, "dx")):
+        e_ours, e_torch = _rel(ours, ref), _rel(theirs, ref)
+        assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
+
+
+@pytest.mark.parametrize("rows,h,f,train", [(4096, 4096, 11008, False), (300, 128, 352, True), (8, 64, 8, True)])
+def test_gate_up_swiglu_matches_fp32(built, rows, h, f, train):
+    from paper_2602_06499_b200.driving_model import _swiglu_mlp
+    import torch.nn.functional as F
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(rows + f)
+    m = torch.randn(rows, h, device=dev, generator=g).to(torch.bfloat16).requires_grad_(True)
+    flat = (torch.randn(2 * f * h, device=dev, generator=g) / h ** 0.5).to(torch.bfloat16)
+    wg = flat[: f * h].view(f, h).detach().requires_grad_(train)
+    wu = flat[f * h:].view(f, h).detach().requires_grad_(train)
+    dy = torch.randn(rows, f, device=dev, generator=g).to(torch.bfloat16)
+    mr, wgr, wur = (t.detach().float().requires_grad_(True) for t in (m, wg, wu))
+    (F.silu(F.linear(mr, wgr)) * F.linear(mr, wur)).backward(dy.float())
+    mt, wgt, wut = (t.detach().clone().requires_grad_(True) for t in (m, wg, wu))
+    yt = F.silu(F.linear(mt, wgt)) * F.linear(mt, wut)
+    yt.backward(dy)
+    y = _swiglu_mlp(m, wg, wu)
+    y.backward(dy)
+    yr = F.silu(F.linear(mr.detach(), wgr.detach())) * F.linear(mr.detach(), wur.detach())
+    pairs = [(y, yt, yr, "y"), (m.grad, mt.grad, mr.grad, "dm")]
+    if train:
+        assert wg.grad.is_contiguous() and wu.grad.is_contiguous()
+        pairs += [(wg.grad, wgt.grad, wgr.grad, "dwg"), (wu.grad, wut.grad, wur.grad, "dwu")]
+    for ours, theirs, ref, name in pairs:
+        e_ours, e_torch = _rel(ours, ref), _rel(theirs, ref)
+        assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
