@@ -282,6 +282,11 @@ int fcdp_swiglu_fwd(int64_t rows, int32_t f, const void* g, int64_t g_stride, co
 int fcdp_swiglu_bwd(int64_t rows, int32_t f, const void* dy, const void* g, int64_t g_stride, const void* u,
                     int64_t u_stride, void* dg, int64_t dg_stride, void* du, int64_t du_stride, void* stream);
 
+/* n device copies (src[i] -> dst[i], bytes[i]; 16-byte aligned, sizes multiples
+ * of 16) in ceil(n / 32) kernel launches: the gradient hand-off of a masked
+ * (LoRA) layer into the engine's natural gradient slot. */
+int fcdp_copy_segments(int32_t n, const void* const* src, void* const* dst, const int64_t* bytes, void* stream);
+
 /* Let kernels launched on `device` dereference `peer`'s memory over NVLink
  * (single-process multi-GPU use of the stateless kernels; the engine itself
  * maps peers through CUDA IPC). */

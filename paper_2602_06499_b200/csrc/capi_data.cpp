@@ -239,6 +239,14 @@ int fcdp_swiglu_bwd(int64_t rows, int32_t f, const void* dy, const void* g, int6
   });
 }
 
+int fcdp_copy_segments(int32_t n, const void* const* src, void* const* dst, const int64_t* bytes, void* stream) {
+  return guarded([&] {
+    if (n < 0) throw shardsim::ConfigError("copy_segments: negative count");
+    check_cuda(fcdp::launch_copy_segments(n, src, dst, bytes, static_cast<cudaStream_t>(stream)),
+               "fcdp_copy_segments (16-byte aligned pointers and sizes)");
+  });
+}
+
 int fcdp_enable_peer_access(int32_t device, int32_t peer) {
   return guarded([&] {
     int can = 0;

@@ -647,6 +647,30 @@ __global__ void __launch_bounds__(kThreads) init_kernel(std::int64_t n, std::uin
   }
 }
 
+// Gradient hand-off of a masked (LoRA) layer: up to kMaxCopySegs small
+// tensors copied into their places in the natural gradient slot by ONE launch
+// (blockIdx.y = segment) instead of one memcpy each (launch-bound: 12 per layer).
+struct CopySegs {
+  const uint4* src[kMaxCopySegs];
+  uint4* dst[kMaxCopySegs];
+  std::int64_t chunks[kMaxCopySegs];
+};
+
+__global__ void __launch_bounds__(kThreads) seg_copy_kernel(CopySegs c) {
+  const int k = blockIdx.y;
+  const std::int64_t n = c.chunks[k];
+  const uint4* __restrict__ src = c.src[k];
+  uint4* __restrict__ dst = c.dst[k];
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; i + step < n; i += 2 * step) {
+    const uint4 a = __ldcs(src + i), b = __ldcs(src + i + step);
+    dst[i] = a;
+    dst[i + step] = b;
+  }
+  for (; i < n; i += step) dst[i] = __ldcs(src + i);
+}
+
 __global__ void __launch_bounds__(kThreads) copy_kernel(const uint4* __restrict__ s, uint4* __restrict__ d,
                                                         std::int64_t n) {
   constexpr std::int64_t kTile = static_cast<std::int64_t>(kThreads) * kUnroll;
@@ -871,6 +895,32 @@ cudaError_t launch_widen(std::int64_t n, const void* src, int elem_bytes, float*
   else
     widen_kernel<float><<<grid, kThreads, 0, s>>>(n, src, dst);
   return cudaGetLastError();
+}
+
+cudaError_t launch_copy_segments(int n, const void* const* src, void* const* dst, const std::int64_t* bytes,
+                                 cudaStream_t s) {
+  for (int base = 0; base < n; base += kMaxCopySegs) {
+    CopySegs c{};
+    const int m = std::min(kMaxCopySegs, n - base);
+    std::int64_t most = 0;
+    for (int k = 0; k < m; ++k) {
+      const auto sp = reinterpret_cast<std::uintptr_t>(src[base + k]);
+      const auto dp = reinterpret_cast<std::uintptr_t>(dst[base + k]);
+      if (bytes[base + k] % kChunkBytes || sp % 16 || dp % 16 || bytes[base + k] < 0) return cudaErrorInvalidValue;
+      c.src[k] = static_cast<const uint4*>(src[base + k]);
+      c.dst[k] = static_cast<uint4*>(dst[base + k]);
+      c.chunks[k] = bytes[base + k] / kChunkBytes;
+      most = std::max(most, c.chunks[k]);
+    }
+    if (most == 0) continue;
+    const dim3 grid(static_cast<unsigned>(std::max<std::int64_t>(
+                        1, std::min<std::int64_t>((most + 2 * kThreads - 1) / (2 * kThreads), sm_count()))),
+                    static_cast<unsigned>(m));
+    seg_copy_kernel<<<grid, kThreads, 0, s>>>(c);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_copy(const void* src, void* dst, std::int64_t bytes, cudaStream_t s) {

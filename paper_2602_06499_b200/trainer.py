@@ -124,6 +124,31 @@ class FcdpTrainer:
         self._held_grads.extend(g for g in grads if g is not None)
         return True
 
+    def _copy_grads(self, g: int, ldef: LayerDef, train, grads, p) -> None:
+        """Autograd's gradients into the engine's natural gradient slot: every
+        16-byte aligned contiguous tensor in one fcdp_copy_segments launch."""
+        import ctypes as C
+        from ._capi import check, lib
+        G = device_view(g, ldef.numel, self.dtype, self.device)
+        eb = G.element_size()
+        src, dst, nbytes = [], [], []
+        for n, gr in zip(train, grads):
+            o = ldef.offsets[n]
+            if gr is None:
+                G[o:o + p[n].numel()].zero_()
+            elif gr.is_contiguous() and gr.dtype == self.dtype and gr.data_ptr() % 16 == 0 and \
+                    (o * eb) % 16 == 0 and (gr.numel() * eb) % 16 == 0:
+                src.append(gr.data_ptr())
+                dst.append(g + o * eb)
+                nbytes.append(gr.numel() * eb)
+            else:
+                G[o:o + gr.numel()].copy_(gr.reshape(-1))
+        if src:
+            n = len(src)
+            check(lib().fcdp_copy_segments(n, (C.c_void_p * n)(*src), (C.c_void_p * n)(*dst),
+                                           (C.c_int64 * n)(*nbytes),
+                                           C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+
     def _params(self, flat: torch.Tensor, ldef: LayerDef, grad: bool):
         out = {}
         for t in ldef.tensors:
@@ -169,14 +194,7 @@ class FcdpTrainer:
                     grads = grads[1:]
                 if g:
                     if not self._hand_over(layer, ldef, train, grads):
-                        G = device_view(g, ldef.numel, self.dtype, self.device)
-                        for n, gr in zip(train, grads):
-                            o = ldef.offsets[n]
-                            dst = G[o:o + gr.numel() if gr is not None else o]
-                            if gr is None:
-                                G[o:o + p[n].numel()].zero_()
-                            else:
-                                dst.copy_(gr.reshape(-1))
+                        self._copy_grads(g, ldef, train, grads, p)
                 if layer == 0:
                     self._grad_act = None
                     self._saved_out = None
