@@ -223,11 +223,13 @@ constexpr int kRowUnroll = 4;
 constexpr float kGeluBeta = 0.7978845608028654f;  // sqrt(2 / pi)
 constexpr float kGeluKappa = 0.044715f;
 
-// tanh(u) = 1 - 2 / (exp(2u) + 1) on the SFU (ex2 + rcp): absolute error ~1e-7,
-// far below a bf16 ulp of the outputs; libm tanhf made these kernels
-// issue-bound (2.9 TB/s) instead of HBM-bound.
+// tanh on the SFU: one tanh.approx.f32 (max relative error 2^-10.99, under a
+// quarter of a bf16 ulp of the outputs).  libm tanhf made these kernels
+// issue-bound (2.9 TB/s), and exp + rcp still cost two SFU ops per element.
 __device__ __forceinline__ float fast_tanh(float u) {
-  return 1.0f - __fdividef(2.0f, __expf(2.0f * u) + 1.0f);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return t;
 }
 
 __device__ __forceinline__ float gelu_tanh(float x) {
@@ -324,35 +326,39 @@ __global__ void colsum_final_kernel(int cols, int splits, const float* __restric
 }
 
 // y = gelu(h + b): the MLP's first linear runs without its bias epilogue and the
-// bias add is fused here (one read of h, one write of y).
-__global__ void __launch_bounds__(256) bias_gelu_fwd_kernel(std::int64_t nvec, int vpr,
+// bias add is fused here (one read of h, one write of y).  A thread owns one
+// column vector (its bias loaded once) and walks rows gridDim.y apart, 4 in
+// flight: no per-element index division.
+constexpr int kGeluRows = 4;
+__global__ void __launch_bounds__(256) bias_gelu_fwd_kernel(std::int64_t rows, int vpr,
                                                             const uint4* __restrict__ h,
                                                             const uint4* __restrict__ bias,
                                                             uint4* __restrict__ y) {
-  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  for (; i + step < nvec; i += 2 * step) {
-    const uint4 qa = __ldcs(h + i), qb = __ldcs(h + i + step);
-    float a[8], b[8], ba[8], bb[8];
-    unpack8(qa, a);
-    unpack8(qb, b);
-    unpack8(__ldg(bias + i % vpr), ba);
-    unpack8(__ldg(bias + (i + step) % vpr), bb);
+  const int cv = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cv >= vpr) return;
+  float bf[8];
+  unpack8(__ldg(bias + cv), bf);
+  std::int64_t r = blockIdx.y;
+  const std::int64_t step = gridDim.y;
+  for (; r + (kGeluRows - 1) * step < rows; r += kGeluRows * step) {
+    uint4 q[kGeluRows];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      a[e] = gelu_tanh(a[e] + ba[e]);
-      b[e] = gelu_tanh(b[e] + bb[e]);
+    for (int u = 0; u < kGeluRows; ++u) q[u] = __ldcs(h + (r + u * step) * vpr + cv);
+#pragma unroll
+    for (int u = 0; u < kGeluRows; ++u) {
+      float a[8];
+      unpack8(q[u], a);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = gelu_tanh(a[e] + bf[e]);
+      __stcs(y + (r + u * step) * vpr + cv, pack8(a));
     }
-    __stcs(y + i, pack8(a));
-    __stcs(y + i + step, pack8(b));
   }
-  for (; i < nvec; i += step) {
-    float a[8], ba[8];
-    unpack8(__ldcs(h + i), a);
-    unpack8(__ldg(bias + i % vpr), ba);
+  for (; r < rows; r += step) {
+    float a[8];
+    unpack8(__ldcs(h + r * vpr + cv), a);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) a[e] = gelu_tanh(a[e] + ba[e]);
-    __stcs(y + i, pack8(a));
+    for (int e = 0; e < 8; ++e) a[e] = gelu_tanh(a[e] + bf[e]);
+    __stcs(y + r * vpr + cv, pack8(a));
   }
 }
 
@@ -608,10 +614,13 @@ cudaError_t launch_bias_gelu_fwd(std::int64_t rows, int cols, const void* h, con
   if (cols % 8 || rows < 1) return cudaErrorInvalidValue;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const std::int64_t nvec = rows * (cols / 8);
-  const int grid = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>((nvec + 511) / 512, 8LL * sms)));
-  bias_gelu_fwd_kernel<<<grid, 256, 0, s>>>(nvec, cols / 8, static_cast<const uint4*>(h),
-                                            static_cast<const uint4*>(b), static_cast<uint4*>(y));
+  const int vpr = cols / 8;
+  const int gx = (vpr + 255) / 256;
+  // about 8 resident blocks of 256 per SM over the whole grid, each row group >= 4 rows deep
+  const std::int64_t gy = std::max<std::int64_t>(
+      1, std::min<std::int64_t>((8LL * sms + gx - 1) / gx, (rows + kGeluRows - 1) / kGeluRows));
+  bias_gelu_fwd_kernel<<<dim3(gx, static_cast<unsigned>(std::min<std::int64_t>(gy, 65535))), 256, 0, s>>>(
+      rows, vpr, static_cast<const uint4*>(h), static_cast<const uint4*>(b), static_cast<uint4*>(y));
   return cudaGetLastError();
 }
 

@@ -206,6 +206,8 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   {
     const char* e = std::getenv("FCDP_OPT_PRIO");
     opt_low_ = e && std::strcmp(e, "low") == 0;
+    const char* c = std::getenv("FCDP_OPT_STREAM");
+    opt_on_compute_ = c && std::strcmp(c, "compute") == 0;
   }
   for (auto& e : fin_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1131,9 +1133,9 @@ void Engine::ev_reduce_scatter(const Event& e) {
   if (fused_grad_ok(li)) {
     // G = 1: the RS is the identity up to widen + scale; fused into AdamW,
     // reading the gradient where backward left it (the slot or the segments)
-    if (opt_low_) {
+    if (opt_low_ || opt_on_compute_) {
       CK(cudaEventRecord(opt_fork_, s));
-      s = s_opt_;
+      s = opt_on_compute_ ? s_comp_ : s_opt_;
       CK(cudaStreamWaitEvent(s, opt_fork_, 0));
       done_s_ = s;
     }

@@ -220,6 +220,7 @@ class Engine {
   cudaStream_t s_opt_ = nullptr;   // G = 1 fused RS + AdamW when FCDP_OPT_PRIO=low
   cudaEvent_t opt_fork_ = nullptr;
   bool opt_low_ = false;
+  bool opt_on_compute_ = false;  // FCDP_OPT_STREAM=compute: the fused update serialised on the compute stream
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, u_ = 0;

@@ -42,11 +42,46 @@ def main():
         tr.step(*batches[i])
     tr.sync()
     torch.cuda.synchronize()
+    # host enqueue time vs device time per step: is the Python/engine host side
+    # keeping ahead of the GPU?
+    import time
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host = []
+    e0.record(tr.stream)
+    for i in range(a.steps):
+        t0 = time.perf_counter()
+        tr.step(*batches[3 + i])
+        host.append((time.perf_counter() - t0) * 1e3)
+    e1.record(tr.stream)
+    tr.sync()
+    torch.cuda.synchronize()
+    print(f"host enqueue ms/step: {sum(host) / len(host):.2f} (each {[round(h, 1) for h in host]}); "
+          f"device ms/step: {e0.elapsed_time(e1) / a.steps:.2f}")
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         for i in range(a.steps):
             tr.step(*batches[3 + i])
         tr.sync()
         torch.cuda.synchronize()
+    # device busy time (union of kernel / memcpy intervals over all streams) vs the span
+    import json
+    import tempfile
+    with tempfile.NamedTemporaryFile(suffix=".json") as f:
+        prof.export_chrome_trace(f.name)
+        tr_ev = json.load(open(f.name)).get("traceEvents", [])
+    iv = sorted((e["ts"], e["ts"] + e.get("dur", 0)) for e in tr_ev
+                if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset") and e.get("dur", 0) > 0)
+    if iv:
+        busy, cur_s, cur_e = 0.0, iv[0][0], iv[0][1]
+        for s_, e_ in iv[1:]:
+            if s_ > cur_e:
+                busy += cur_e - cur_s
+                cur_s, cur_e = s_, e_
+            else:
+                cur_e = max(cur_e, e_)
+        busy += cur_e - cur_s
+        span = iv[-1][1] - iv[0][0]
+        print(f"device busy (any stream) {busy / 1e3 / a.steps:.2f} ms/step of a {span / 1e3 / a.steps:.2f} ms/step "
+              f"span: idle {(span - busy) / 1e3 / a.steps:.2f} ms/step")
     ka = prof.key_averages()
     rows = sorted(ka, key=lambda e: -getattr(e, "self_device_time_total", getattr(e, "self_cuda_time_total", 0)))
     tot = sum(getattr(e, "self_device_time_total", getattr(e, "self_cuda_time_total", 0)) for e in ka)
