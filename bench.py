@@ -642,6 +642,9 @@ def main():
     if per_launch_bytes < 64e6:
         # a few MB per launch (PEFT trainable slices): launch latency, not bandwidth, bounds it
         roofline["note"] = f"{per_launch_bytes / 1e6:.1f} MB per launch: launch-latency regime"
+    elif dom == "adamw" and world == 1:
+        roofline["note"] = ("G = 1 fused reduce-scatter + AdamW, on the compute stream after each layer's backward "
+                            "(live = CUDA events around each launch in the step); isolated = the same launch alone")
     elif dom in ("adamw", "rs_slice"):
         # the per-layer update / reduce-scatter runs on its own stream beside the
         # backward GEMMs of the next layers, off the compute stream's critical path;

@@ -197,17 +197,23 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   CK(cudaStreamCreateWithPriority(&s_agsend_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_rssend_, cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&s_rsrecv_, cudaStreamNonBlocking, hi));
-  // G = 1 fused RS + AdamW runs on s_rs_ (high priority: its CTAs are placed
-  // ahead of the backward GEMMs', measured equal step time and a better live
-  // rate than the low-priority stream).  FCDP_OPT_PRIO=low moves it to s_opt_,
+  // G = 1 fused RS + AdamW: on the compute stream by default (below);
+  // FCDP_OPT_STREAM=rs keeps it on s_rs_, FCDP_OPT_PRIO=low moves it to s_opt_
   // at the compute stream's priority.
   CK(cudaStreamCreateWithPriority(&s_opt_, cudaStreamNonBlocking, lo));
   CK(cudaEventCreateWithFlags(&opt_fork_, cudaEventDisableTiming));
   {
     const char* e = std::getenv("FCDP_OPT_PRIO");
     opt_low_ = e && std::strcmp(e, "low") == 0;
+    // Default: the fused update runs on the compute stream right after the
+    // layer's backward.  On the high-priority side stream its CTAs could not
+    // co-reside with the backward GEMMs' anyway (they queued for whole SMs), so
+    // the step time is the same (A/B on one box: 69.46-69.55 ms both ways,
+    // profiles/r02_ab_opt_stream.json) while its own launches run unqueued:
+    // 0.85 instead of 0.63 of the HBM roofline.  FCDP_OPT_STREAM=rs restores
+    // the side stream, FCDP_OPT_PRIO=low the low-priority one.
     const char* c = std::getenv("FCDP_OPT_STREAM");
-    opt_on_compute_ = c && std::strcmp(c, "compute") == 0;
+    opt_on_compute_ = !opt_low_ && !(c && std::strcmp(c, "rs") == 0);
   }
   for (auto& e : fin_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

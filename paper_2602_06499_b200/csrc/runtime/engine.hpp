@@ -217,10 +217,10 @@ class Engine {
   cudaEvent_t rs_done_[2] = {nullptr, nullptr};
   cudaEvent_t iter_done_ = nullptr;
   cudaEvent_t join_[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  cudaStream_t s_opt_ = nullptr;   // G = 1 fused RS + AdamW when FCDP_OPT_PRIO=low
+  cudaStream_t s_opt_ = nullptr;   // G = 1 fused RS + AdamW when FCDP_OPT_PRIO=low (else compute stream)
   cudaEvent_t opt_fork_ = nullptr;
   bool opt_low_ = false;
-  bool opt_on_compute_ = false;  // FCDP_OPT_STREAM=compute: the fused update serialised on the compute stream
+  bool opt_on_compute_ = true;  // the G = 1 fused update on the compute stream (FCDP_OPT_STREAM=rs: side stream)
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, u_ = 0;
