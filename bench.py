@@ -476,7 +476,8 @@ def main():
 
     capacity = torch.cuda.get_device_properties(dev).total_memory
 
-    def measure(strategy: str, steps: int, warmup: int, timing: bool, e2e_steps: int, tau: float = 0.0):
+    def measure(strategy: str, steps: int, warmup: int, timing: bool, e2e_steps: int, tau: float = 0.0,
+                stats: bool = None):
         plan = S.StrategyPlan(S.StrategyKind.from_string(strategy), tau=tau)
         shm = bcast(f"fcdp_bench_{uuid.uuid4().hex[:12]}" if rank == 0 else None)
         tr = FcdpTrainer(mc, topo, plan, rank=rank, world_size=world, device=local, shm_name=shm,
@@ -519,7 +520,7 @@ def main():
         launches = tr.engine.kernel_stats(reset=True)  # launch counts of the timed region
         gpu_launches = sum(launches[k]["launches"] for k in tr.engine.KERNEL_CLASSES)
         kst, kst_steps = None, 0
-        if timing:
+        if timing if stats is None else stats:
             # kernel statistics pass: CUDA events around every engine launch
             kst_steps = min(steps, 5)
             tr.engine.kernel_stats(reset=True)
@@ -576,7 +577,7 @@ def main():
     main_run = measure(args.strategy, args.steps, args.warmup, True, 0 if args.no_e2e else args.steps, args.tau)
     tau_run = None
     if args.tau_variant >= 0 and args.strategy in ("fcdp", "fcdp-comm") and args.tau_variant != args.tau:
-        tau_run = measure(args.strategy, args.zero3_steps, 2, False, 0, args.tau_variant)
+        tau_run = measure(args.strategy, args.zero3_steps, 2, False, 0, args.tau_variant, stats=True)
     z3 = None
     if not args.no_zero3 and args.strategy != "zero3":
         z3 = measure("zero3", args.zero3_steps, 2, False, 0)
@@ -677,14 +678,18 @@ def main():
     # host-link copies (FCDP-Cache and NIC staging): achieved GB/s of the copies
     # themselves (bytes / their CUDA-event durations) against the PCIe rate
     # measured in this run with every rank copying at once
-    copies = {}
-    for k, v in cst.items():
-        if not v["launches"]:
-            continue
-        gbs = v["alg_bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None
-        peak_c = pcie["d2h"] if k.endswith("d2h") else pcie["h2d"]
-        copies[k] = {"bytes_per_step": v["alg_bytes"] / ks, "copies_per_step": v["launches"] / ks,
-                     "GBps": gbs, "pcie_peak_gbps": peak_c, "frac": gbs / peak_c if gbs else None}
+    def copy_fracs(stats, nsteps):
+        out = {}
+        for k, v in stats.items():
+            if k not in _E.COPY_CLASSES or not v["launches"]:
+                continue
+            gbs = v["alg_bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None
+            peak_c = pcie["d2h"] if k.endswith("d2h") else pcie["h2d"]
+            out[k] = {"bytes_per_step": v["alg_bytes"] / nsteps, "copies_per_step": v["launches"] / nsteps,
+                      "GBps": gbs, "pcie_peak_gbps": peak_c, "frac": gbs / peak_c if gbs else None}
+        return out
+
+    copies = copy_fracs(cst, ks)
     kernels = {k: {"launches_per_step": v["launches"] / ks, "ms_per_step": v["ms"] / ks,
                    "GBps": (v["alg_bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None} for k, v in kst.items()}
     line = {
@@ -710,6 +715,10 @@ def main():
         "cache_bytes_per_step_per_node": main_run["cache"],
         "fcdp_variant": ({"tau": args.tau_variant, "tokens_per_s": tokens_per_step / (tau_run["ms"] / args.zero3_steps / 1e3),
                                 "ms_per_step": tau_run["ms"] / args.zero3_steps, "cache": tau_run["cache"],
+                                "copies": (copy_fracs(tau_run["kernels"], max(tau_run["kst_steps"], 1))
+                                           if tau_run["kernels"] else None),
+                                "vs_zero3": ((z3["ms"] / z3_steps(args)) / (tau_run["ms"] / args.zero3_steps)
+                                             if z3 else None),
                                 "ag_inter_fwd_bwd": [tau_run["node_tx"]["nic_tx_fwd_ag"], tau_run["node_tx"]["nic_tx_bwd_ag"]]}
                                if tau_run else None),
         "host_numa": main_run["numa"], "kernels": kernels,

@@ -272,11 +272,13 @@ int fcdp_xent_bwd(int64_t rows, int32_t vocab, const void* logits, const int64_t
 
 /* Driving-model Llama blocks: rotary embedding of x [batch, seq, heads, dim]
  * (bf16; pairs (2i, 2i+1); fp32 cos / sin tables [seq, dim / 2]; inverse != 0
- * rotates back - the backward), and SwiGLU y = silu(g) * u over [rows x f]
+ * rotates back - the backward; x_stride / y_stride = elements between tokens,
+ * 0 = heads * dim), and SwiGLU y = silu(g) * u over [rows x f]
  * with its backward (row strides in elements, multiples of 8, so g and u may
  * be the two halves of one [rows x 2f] GEMM output). */
-int fcdp_rope(int64_t batch, int32_t seq, int32_t heads, int32_t dim, const void* x, const float* cos_table,
-              const float* sin_table, int32_t inverse, void* y, void* stream);
+int fcdp_rope(int64_t batch, int32_t seq, int32_t heads, int32_t dim, const void* x, int64_t x_stride,
+              const float* cos_table, const float* sin_table, int32_t inverse, void* y, int64_t y_stride,
+              void* stream);
 int fcdp_swiglu_fwd(int64_t rows, int32_t f, const void* g, int64_t g_stride, const void* u, int64_t u_stride, void* y,
                     void* stream);
 int fcdp_swiglu_bwd(int64_t rows, int32_t f, const void* dy, const void* g, int64_t g_stride, const void* u,

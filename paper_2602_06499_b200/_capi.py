@@ -158,7 +158,7 @@ SIGNATURES = {
     "fcdp_bias_gelu_bwd": (C.c_int, [i64, i32, P, P, P, P, P, P, i32, P]),
     "fcdp_xent_fwd": (C.c_int, [i64, i32, P, P, P, P, P]),
     "fcdp_xent_bwd": (C.c_int, [i64, i32, P, P, P, P, P, P]),
-    "fcdp_rope": (C.c_int, [i64, i32, i32, i32, P, P, P, i32, P, P]),
+    "fcdp_rope": (C.c_int, [i64, i32, i32, i32, P, i64, P, P, i32, P, i64, P]),
     "fcdp_swiglu_fwd": (C.c_int, [i64, i32, P, i64, P, i64, P, P]),
     "fcdp_swiglu_bwd": (C.c_int, [i64, i32, P, P, i64, P, i64, P, i64, P, i64, P]),
     "fcdp_copy_segments": (C.c_int, [i32, PP, PP, C.POINTER(C.c_int64), P]),

@@ -209,11 +209,17 @@ int fcdp_xent_bwd(int64_t rows, int32_t vocab, const void* logits, const int64_t
   });
 }
 
-int fcdp_rope(int64_t batch, int32_t seq, int32_t heads, int32_t dim, const void* x, const float* cos_table,
-              const float* sin_table, int32_t inverse, void* y, void* stream) {
+int fcdp_rope(int64_t batch, int32_t seq, int32_t heads, int32_t dim, const void* x, int64_t x_stride,
+              const float* cos_table, const float* sin_table, int32_t inverse, void* y, int64_t y_stride,
+              void* stream) {
   return guarded([&] {
+    const int64_t row = static_cast<int64_t>(heads) * dim;
     if (dim % 8) throw shardsim::ConfigError("rope: head dim must be a multiple of 8");
-    check_cuda(fcdp::launch_rope(batch, seq, heads, dim, x, cos_table, sin_table, inverse != 0, y,
+    if (x_stride == 0) x_stride = row;
+    if (y_stride == 0) y_stride = row;
+    if (x_stride % 8 || y_stride % 8 || x_stride < row || y_stride < row)
+      throw shardsim::ConfigError("rope: token strides must be multiples of 8 and >= heads * dim");
+    check_cuda(fcdp::launch_rope(batch, seq, heads, dim, x, x_stride, cos_table, sin_table, inverse != 0, y, y_stride,
                                  static_cast<cudaStream_t>(stream)),
                "fcdp_rope");
   });

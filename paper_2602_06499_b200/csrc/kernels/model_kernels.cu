@@ -463,29 +463,32 @@ __global__ void __launch_bounds__(kXentThreads) xent_bwd_kernel(int vpr, const u
 // (2i, 2i+1) rotated by pos * base^(-2i/dim), angles from fp32 cos / sin tables
 // [seq, dim/2]; sign = -1 applies the inverse rotation (the backward).  One
 // 16-byte vector (4 pairs) per thread, fp32 arithmetic, one rounding.
+// xs / ys: token strides of x and y in 16-byte vectors (heads * dim / 8 when
+// contiguous; larger for one third of a joint [tokens x 3h] q|k|v projection).
 __global__ void __launch_bounds__(256) rope_kernel(std::int64_t nvec, int seq, int heads, int dim,
-                                                   const uint4* __restrict__ x, const float* __restrict__ cs,
-                                                   const float* __restrict__ sn, float sign,
-                                                   uint4* __restrict__ y) {
+                                                   const uint4* __restrict__ x, std::int64_t xs,
+                                                   const float* __restrict__ cs, const float* __restrict__ sn,
+                                                   float sign, uint4* __restrict__ y, std::int64_t ys) {
   const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
   const int vrow = heads * dim / 8;  // vectors per token
   const int vdim = dim / 8;
   for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += step) {
     const std::int64_t tok = i / vrow;
+    const int col = static_cast<int>(i - tok * vrow);
     const int pos = static_cast<int>(tok % seq);
-    const int d0 = static_cast<int>(i % vdim) * 4;  // first pair index
+    const int d0 = (col % vdim) * 4;  // first pair index
     const float4 c = __ldg(reinterpret_cast<const float4*>(cs + static_cast<std::int64_t>(pos) * (dim / 2) + d0));
     const float4 s4 = __ldg(reinterpret_cast<const float4*>(sn + static_cast<std::int64_t>(pos) * (dim / 2) + d0));
     const float cc[4] = {c.x, c.y, c.z, c.w};
     const float ss[4] = {sign * s4.x, sign * s4.y, sign * s4.z, sign * s4.w};
     float v[8], o[8];
-    unpack8(__ldcs(x + i), v);
+    unpack8(__ldcs(x + tok * xs + col), v);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       o[2 * k] = v[2 * k] * cc[k] - v[2 * k + 1] * ss[k];
       o[2 * k + 1] = v[2 * k] * ss[k] + v[2 * k + 1] * cc[k];
     }
-    __stcs(y + i, pack8(o));
+    __stcs(y + tok * ys + col, pack8(o));
   }
 }
 
@@ -659,12 +662,17 @@ int elementwise_grid(std::int64_t nvec) {
 }
 }  // namespace
 
-cudaError_t launch_rope(std::int64_t batch, int seq, int heads, int dim, const void* x, const float* cs,
-                        const float* sn, bool inverse, void* y, cudaStream_t s) {
-  if (dim % 8 || batch < 1 || seq < 1 || heads < 1) return cudaErrorInvalidValue;
-  const std::int64_t nvec = batch * seq * static_cast<std::int64_t>(heads) * dim / 8;
-  rope_kernel<<<elementwise_grid(nvec), 256, 0, s>>>(nvec, seq, heads, dim, static_cast<const uint4*>(x), cs, sn,
-                                                     inverse ? -1.0f : 1.0f, static_cast<uint4*>(y));
+cudaError_t launch_rope(std::int64_t batch, int seq, int heads, int dim, const void* x, std::int64_t x_stride,
+                        const float* cs, const float* sn, bool inverse, void* y, std::int64_t y_stride,
+                        cudaStream_t s) {
+  const std::int64_t row = static_cast<std::int64_t>(heads) * dim;
+  if (dim % 8 || batch < 1 || seq < 1 || heads < 1 || x_stride % 8 || y_stride % 8 || x_stride < row ||
+      y_stride < row)
+    return cudaErrorInvalidValue;
+  const std::int64_t nvec = batch * seq * row / 8;
+  rope_kernel<<<elementwise_grid(nvec), 256, 0, s>>>(nvec, seq, heads, dim, static_cast<const uint4*>(x),
+                                                     x_stride / 8, cs, sn, inverse ? -1.0f : 1.0f,
+                                                     static_cast<uint4*>(y), y_stride / 8);
   return cudaGetLastError();
 }
 

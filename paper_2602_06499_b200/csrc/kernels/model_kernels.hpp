@@ -32,9 +32,11 @@ cudaError_t launch_xent_fwd(std::int64_t rows, int V, const void* logits, const 
 cudaError_t launch_xent_bwd(std::int64_t rows, int V, const void* logits, const std::int64_t* labels,
                             const float* lse, const float* scale, void* dlogits, cudaStream_t s);
 
-// RoPE of x [batch, seq, heads, dim] with fp32 cos / sin tables [seq, dim / 2]; inverse: the backward
-cudaError_t launch_rope(std::int64_t batch, int seq, int heads, int dim, const void* x, const float* cs,
-                        const float* sn, bool inverse, void* y, cudaStream_t s);
+// RoPE of x [batch, seq, heads, dim] with fp32 cos / sin tables [seq, dim / 2]; inverse: the backward.
+// x_stride / y_stride: elements between consecutive tokens (>= heads * dim, multiples of 8).
+cudaError_t launch_rope(std::int64_t batch, int seq, int heads, int dim, const void* x, std::int64_t x_stride,
+                        const float* cs, const float* sn, bool inverse, void* y, std::int64_t y_stride,
+                        cudaStream_t s);
 // SwiGLU y = silu(g) * u, [rows x f]; strides in elements (multiples of 8)
 cudaError_t launch_swiglu_fwd(std::int64_t rows, int f, const void* g, std::int64_t g_stride, const void* u,
                               std::int64_t u_stride, void* y, cudaStream_t s);

@@ -119,10 +119,14 @@ class ModelConfig:
             defs.append(LayerDef("embed", [TensorSpec("wte", (V, h), scale=0.02, trainable=not peft)]))
             for _ in range(self.layers):
                 ts = [TensorSpec("attn_norm", (h,), "const", 1.0, trainable=not peft)]
+                # q, k, v (and their LoRA A's) adjacent in the layer buffer: one
+                # [tokens x 3h] projection GEMM and one [tokens x 3r] LoRA-A GEMM
                 for p in ("q", "k", "v", "o"):
                     ts.append(TensorSpec(f"{p}_w", (h, h), scale=0.02, trainable=not peft))
-                    if peft:
+                if peft:
+                    for p in ("q", "k", "v", "o"):
                         ts.append(TensorSpec(f"{p}_A", (r, h), scale=0.02, trainable=True))
+                    for p in ("q", "k", "v", "o"):
                         # B != 0 so that A receives gradient from step 1 (parity runs)
                         ts.append(TensorSpec(f"{p}_B", (h, r), scale=1e-3, trainable=True))
                 ts += [TensorSpec("mlp_norm", (h,), "const", 1.0, trainable=not peft),
@@ -360,7 +364,7 @@ def _fns():
             b, sq, nh, d = xc.shape
             cs, sn = rope_tables(sq, d, xc.device)
             y = torch.empty_like(xc)
-            check(lib().fcdp_rope(b, sq, nh, d, P(xc), P(cs), P(sn), 0, P(y), S(xc.device)))
+            check(lib().fcdp_rope(b, sq, nh, d, P(xc), 0, P(cs), P(sn), 0, P(y), 0, S(xc.device)))
             ctx.shape = (b, sq, nh, d)
             return y
 
@@ -370,7 +374,7 @@ def _fns():
             dyc = dy.contiguous()
             cs, sn = rope_tables(sq, d, dyc.device)
             dx = torch.empty_like(dyc)
-            check(lib().fcdp_rope(b, sq, nh, d, P(dyc), P(cs), P(sn), 1, P(dx), S(dyc.device)))
+            check(lib().fcdp_rope(b, sq, nh, d, P(dyc), 0, P(cs), P(sn), 1, P(dx), 0, S(dyc.device)))
             return dx
 
     class GateUpSwiGLU(torch.autograd.Function):
@@ -410,8 +414,90 @@ def _fns():
                 dwg, dwu = dw2[:f], dw2[f:]
             return dm, dwg, dwu
 
-    _FNS = (LinearBias, BiasGelu, CrossEntropy, Rope, GateUpSwiGLU)
+    class LlamaQKV(torch.autograd.Function):
+        """q, k, v of a Llama block from ONE [tokens x 3h] GEMM over the adjacent
+        q|k|v weights (+ LoRA: one [tokens x 3r] GEMM over the adjacent A's and
+        the three B's accumulated into their thirds in the GEMM epilogue), RoPE
+        applied to the q and k thirds in place of a copy.  Backward by hand:
+        one dgrad GEMM for the input (+ one for the LoRA path) instead of three
+        (+ three) and the autograd accumulations between them."""
+
+        @staticmethod
+        def forward(ctx, a, wq, wk, wv, aq, ak, av, bq, bk, bv, nh):
+            b, sq, h = a.shape
+            hd = h // nh
+            a2 = a.reshape(-1, h)
+            w3 = torch.as_strided(wq, (3 * h, h), (h, 1))
+            y3 = a2.mm(w3.t())
+            xa3 = None
+            if aq is not None:
+                r = aq.shape[0]
+                xa3 = a2.mm(torch.as_strided(aq, (3 * r, h), (h, 1)).t())
+                for i, bb in enumerate((bq, bk, bv)):
+                    y3[:, i * h:(i + 1) * h].addmm_(xa3[:, i * r:(i + 1) * r], bb.t())
+            cs, sn = rope_tables(sq, hd, a.device)
+            q = torch.empty(b, sq, nh, hd, dtype=a.dtype, device=a.device)
+            k = torch.empty_like(q)
+            st = S(a.device)
+            check(lib().fcdp_rope(b, sq, nh, hd, P(y3), 3 * h, P(cs), P(sn), 0, P(q), 0, st))
+            check(lib().fcdp_rope(b, sq, nh, hd, C.c_void_p(y3.data_ptr() + h * y3.element_size()), 3 * h, P(cs),
+                                  P(sn), 0, P(k), 0, st))
+            v = y3[:, 2 * h:].contiguous().view(b, sq, nh, hd)  # SDPA keeps its cuDNN path on dense v
+            ctx.save_for_backward(a, wq, aq, bq, bk, bv, xa3)
+            ctx.nh = nh
+            return q, k, v
+
+        @staticmethod
+        def backward(ctx, dq, dk, dv):
+            a, wq, aq, bq, bk, bv, xa3 = ctx.saved_tensors
+            b, sq, h = a.shape
+            nh = ctx.nh
+            hd = h // nh
+            rows = b * sq
+            a2 = a.reshape(-1, h)
+            dy3 = torch.empty(rows, 3 * h, dtype=a.dtype, device=a.device)
+            cs, sn = rope_tables(sq, hd, a.device)
+            st = S(a.device)
+            for i, d in enumerate((dq, dk)):
+                dc = d.contiguous()
+                check(lib().fcdp_rope(b, sq, nh, hd, P(dc), 0, P(cs), P(sn), 1,
+                                      C.c_void_p(dy3.data_ptr() + i * h * dy3.element_size()), 3 * h, st))
+            dy3[:, 2 * h:].view(b, sq, nh, hd).copy_(dv)
+            w3 = torch.as_strided(wq, (3 * h, h), (h, 1))
+            ng = ctx.needs_input_grad
+            da = dy3.mm(w3) if ng[0] else None
+            dw = [None, None, None]
+            if ng[1] or ng[2] or ng[3]:
+                dw3 = dy3.t().mm(a2)
+                dw = [dw3[i * h:(i + 1) * h] for i in range(3)]
+            dA = [None, None, None]
+            dB = [None, None, None]
+            if aq is not None:
+                r = aq.shape[0]
+                dxa3 = torch.cat([dy3[:, i * h:(i + 1) * h].mm(bb) for i, bb in enumerate((bq, bk, bv))], dim=1)
+                if da is not None:
+                    da.addmm_(dxa3, torch.as_strided(aq, (3 * r, h), (h, 1)))
+                if ng[4] or ng[5] or ng[6]:
+                    dA3 = dxa3.t().mm(a2)
+                    dA = [dA3[i * r:(i + 1) * r] for i in range(3)]
+                if ng[7] or ng[8] or ng[9]:
+                    dB = [dy3[:, i * h:(i + 1) * h].t().mm(xa3[:, i * r:(i + 1) * r]) for i in range(3)]
+            return (da.view(a.shape) if da is not None else None, *dw, *dA, *dB, None)
+
+    _FNS = (LinearBias, BiasGelu, CrossEntropy, Rope, GateUpSwiGLU, LlamaQKV)
     return _FNS
+
+
+def _llama_qkv(p, a, nh):
+    """(q, k, v) [b, s, nh, hd] with RoPE on q, k: the joint projection when the
+    q|k|v weights (and LoRA A's) are adjacent in the layer buffer, else per tensor."""
+    lora = "q_A" in p
+    if (_fused_ok(a, p["q_w"]) and a.shape[-1] // nh % 8 == 0 and _adjacent(p["q_w"], p["k_w"])
+            and _adjacent(p["k_w"], p["v_w"])
+            and (not lora or (_adjacent(p["q_A"], p["k_A"]) and _adjacent(p["k_A"], p["v_A"])))):
+        args = [p[f"{n}_A"] for n in "qkv"] + [p[f"{n}_B"] for n in "qkv"] if lora else [None] * 6
+        return _fns()[5].apply(a, p["q_w"], p["k_w"], p["v_w"], *args, nh)
+    return None
 
 
 def _adjacent(a, b) -> bool:
@@ -488,9 +574,13 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
                 y = torch.addmm(y.reshape(-1, y.shape[-1]), xa.reshape(-1, xa.shape[-1]),
                                 p[f"{name}_B"].t()).view(y.shape)
             return y
-        q = _rope_fn(proj("q", a).view(b, s, nh, h // nh)).transpose(1, 2)
-        k = _rope_fn(proj("k", a).view(b, s, nh, h // nh)).transpose(1, 2)
-        v = proj("v", a).view(b, s, nh, h // nh).transpose(1, 2)
+        qkv = _llama_qkv(p, a, nh)
+        if qkv is not None:
+            q, k, v = (t.transpose(1, 2) for t in qkv)
+        else:
+            q = _rope_fn(proj("q", a).view(b, s, nh, h // nh)).transpose(1, 2)
+            k = _rope_fn(proj("k", a).view(b, s, nh, h // nh)).transpose(1, 2)
+            v = proj("v", a).view(b, s, nh, h // nh).transpose(1, 2)
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
         x = x + proj("o", o.transpose(1, 2).reshape(b, s, h))
         m = F.rms_norm(x, (h,), p["mlp_norm"], eps=1e-5)

@@ -179,3 +179,43 @@ def test_gate_up_swiglu_matches_fp32(built, rows, h, f, train):
     for ours, theirs, ref, name in pairs:
         e_ours, e_torch = _rel(ours, ref), _rel(theirs, ref)
         assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
+
+
+@pytest.mark.parametrize("lora", [True, False])
+def test_llama_qkv_matches_fp32(built, lora):
+    """Joint q|k|v (+ LoRA A|A|A, B's in the epilogue) projection with RoPE vs the
+    per-tensor fp32 formulation (F.linear + (xA^T)B^T, torch RoPE)."""
+    from paper_2602_06499_b200.driving_model import ModelConfig, _llama_qkv, _rope
+    import torch.nn.functional as F
+    dev = _dev()
+    cfg = ModelConfig("llama", 256, 1, 4, 512, 64, ffn=704, lora_rank=8 if lora else 0)
+    ldef = cfg.layer_defs()[1]
+    g = torch.Generator(device=dev).manual_seed(11 + lora)
+    flat = (0.05 * torch.randn(ldef.numel, device=dev, generator=g)).to(torch.bfloat16)
+    p = {t.name: flat[ldef.offsets[t.name]:ldef.offsets[t.name] + t.numel].view(t.shape).detach()
+         .requires_grad_(t.trainable) for t in ldef.tensors}
+    b, s, h, nh = 3, 64, 256, 4
+    a = torch.randn(b, s, h, device=dev, generator=g).to(torch.bfloat16).requires_grad_(True)
+    dys = [torch.randn(b, s, nh, h // nh, device=dev, generator=g).to(torch.bfloat16) for _ in range(3)]
+    out = _llama_qkv(p, a, nh)
+    assert out is not None
+    torch.autograd.backward(out, dys)
+    # fp32 reference
+    pr = {k: v.detach().float().requires_grad_(v.requires_grad) for k, v in p.items()}
+    ar = a.detach().float().requires_grad_(True)
+
+    def proj(n):
+        y = F.linear(ar, pr[f"{n}_w"])
+        if lora:
+            y = y + F.linear(F.linear(ar, pr[f"{n}_A"]), pr[f"{n}_B"])
+        return y.view(b, s, nh, h // nh)
+    ref = (_rope(proj("q")), _rope(proj("k")), proj("v"))
+    torch.autograd.backward(ref, [d.float() for d in dys])
+    for o, r_, name in zip(out, ref, "qkv"):
+        assert _rel(o, r_) <= 8e-3, (name, _rel(o, r_))
+    assert _rel(a.grad, ar.grad) <= 8e-3, _rel(a.grad, ar.grad)
+    names = [f"{n}_{w}" for n in "qkv" for w in ("AB" if lora else "w")]
+    for n in names:
+        if p[n].requires_grad:
+            assert p[n].grad is not None and p[n].grad.is_contiguous(), n
+            assert _rel(p[n].grad, pr[n].grad) <= 1.5e-2, (n, _rel(p[n].grad, pr[n].grad))
