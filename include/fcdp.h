@@ -284,6 +284,10 @@ int fcdp_swiglu_fwd(int64_t rows, int32_t f, const void* g, int64_t g_stride, co
 int fcdp_swiglu_bwd(int64_t rows, int32_t f, const void* dy, const void* g, int64_t g_stride, const void* u,
                     int64_t u_stride, void* dg, int64_t dg_stride, void* du, int64_t du_stride, void* stream);
 
+/* rows x row_bytes strided device copy (pitches in bytes; pointers, row bytes and
+ * pitches multiples of 16): e.g. the v third of a joint q|k|v projection. */
+int fcdp_copy_rows(int64_t rows, int64_t row_bytes, const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
+                   void* stream);
 /* n device copies (src[i] -> dst[i], bytes[i]; 16-byte aligned, sizes multiples
  * of 16) in ceil(n / 32) kernel launches: the gradient hand-off of a masked
  * (LoRA) layer into the engine's natural gradient slot. */

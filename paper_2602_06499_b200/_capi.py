@@ -161,6 +161,7 @@ SIGNATURES = {
     "fcdp_rope": (C.c_int, [i64, i32, i32, i32, P, i64, P, P, i32, P, i64, P]),
     "fcdp_swiglu_fwd": (C.c_int, [i64, i32, P, i64, P, i64, P, P]),
     "fcdp_swiglu_bwd": (C.c_int, [i64, i32, P, P, i64, P, i64, P, i64, P, i64, P]),
+    "fcdp_copy_rows": (C.c_int, [i64, i64, P, i64, P, i64, P]),
     "fcdp_copy_segments": (C.c_int, [i32, PP, PP, C.POINTER(C.c_int64), P]),
     "fcdp_numa_parse_cpulist": (C.c_int, [C.c_char_p, C.POINTER(i32), i32, C.POINTER(i32)]),
     "fcdp_numa_selftest": (C.c_int, [i32, C.c_uint64, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),

@@ -245,6 +245,15 @@ int fcdp_swiglu_bwd(int64_t rows, int32_t f, const void* dy, const void* g, int6
   });
 }
 
+int fcdp_copy_rows(int64_t rows, int64_t row_bytes, const void* src, int64_t src_pitch, void* dst, int64_t dst_pitch,
+                   void* stream) {
+  return guarded([&] {
+    check_cuda(fcdp::launch_copy_rows(rows, row_bytes, src, src_pitch, dst, dst_pitch,
+                                      static_cast<cudaStream_t>(stream)),
+               "fcdp_copy_rows (16-byte aligned pointers, row bytes and pitches)");
+  });
+}
+
 int fcdp_copy_segments(int32_t n, const void* const* src, void* const* dst, const int64_t* bytes, void* stream) {
   return guarded([&] {
     if (n < 0) throw shardsim::ConfigError("copy_segments: negative count");

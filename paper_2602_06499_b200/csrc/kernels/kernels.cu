@@ -647,6 +647,19 @@ __global__ void __launch_bounds__(kThreads) init_kernel(std::int64_t n, std::uin
   }
 }
 
+// rows x (row_bytes) strided copy, 16-byte vectors (one third of a joint
+// [tokens x 3h] projection to or from a dense [tokens x h] tensor).
+__global__ void __launch_bounds__(kThreads) copy_rows_kernel(std::int64_t rows, int rv, const uint4* __restrict__ src,
+                                                             std::int64_t ss, uint4* __restrict__ dst,
+                                                             std::int64_t ds) {
+  const std::int64_t n = rows * rv;
+  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += step) {
+    const std::int64_t r = i / rv, c = i - r * rv;
+    dst[r * ds + c] = __ldcs(src + r * ss + c);
+  }
+}
+
 // Gradient hand-off of a masked (LoRA) layer: up to kMaxCopySegs small
 // tensors copied into their places in the natural gradient slot by ONE launch
 // (blockIdx.y = segment) instead of one memcpy each (launch-bound: 12 per layer).
@@ -894,6 +907,19 @@ cudaError_t launch_widen(std::int64_t n, const void* src, int elem_bytes, float*
     widen_kernel<__nv_bfloat16><<<grid, kThreads, 0, s>>>(n, src, dst);
   else
     widen_kernel<float><<<grid, kThreads, 0, s>>>(n, src, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_rows(std::int64_t rows, std::int64_t row_bytes, const void* src, std::int64_t src_pitch,
+                             void* dst, std::int64_t dst_pitch, cudaStream_t s) {
+  if (row_bytes % kChunkBytes || src_pitch % kChunkBytes || dst_pitch % kChunkBytes || rows < 0 ||
+      reinterpret_cast<std::uintptr_t>(src) % 16 || reinterpret_cast<std::uintptr_t>(dst) % 16)
+    return cudaErrorInvalidValue;
+  const std::int64_t n = rows * (row_bytes / kChunkBytes);
+  if (n == 0) return cudaSuccess;
+  copy_rows_kernel<<<grid_for(n, kThreads * 2), kThreads, 0, s>>>(
+      rows, static_cast<int>(row_bytes / kChunkBytes), static_cast<const uint4*>(src), src_pitch / kChunkBytes,
+      static_cast<uint4*>(dst), dst_pitch / kChunkBytes);
   return cudaGetLastError();
 }
 

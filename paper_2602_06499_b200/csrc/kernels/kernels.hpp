@@ -73,6 +73,9 @@ cudaError_t launch_init_natural(std::int64_t n_elems, int elem_bytes, std::uint6
 // Widen a portion shard (param dtype) to fp32 (master init).
 cudaError_t launch_widen(std::int64_t n, const void* src, int elem_bytes, float* dst, cudaStream_t s);
 
+// rows x row_bytes strided device copy (pitches in bytes; all multiples of 16).
+cudaError_t launch_copy_rows(std::int64_t rows, std::int64_t row_bytes, const void* src, std::int64_t src_pitch,
+                             void* dst, std::int64_t dst_pitch, cudaStream_t s);
 // Up to any number of 16-byte aligned (src, dst, bytes) copies, kMaxCopySegs per launch.
 inline constexpr int kMaxCopySegs = 32;
 cudaError_t launch_copy_segments(int n, const void* const* src, void* const* dst, const std::int64_t* bytes,

@@ -439,10 +439,14 @@ def _fns():
             q = torch.empty(b, sq, nh, hd, dtype=a.dtype, device=a.device)
             k = torch.empty_like(q)
             st = S(a.device)
+            rows_of = lambda t: t.numel() // t.shape[-1]
             check(lib().fcdp_rope(b, sq, nh, hd, P(y3), 3 * h, P(cs), P(sn), 0, P(q), 0, st))
             check(lib().fcdp_rope(b, sq, nh, hd, C.c_void_p(y3.data_ptr() + h * y3.element_size()), 3 * h, P(cs),
                                   P(sn), 0, P(k), 0, st))
-            v = y3[:, 2 * h:].contiguous().view(b, sq, nh, hd)  # SDPA keeps its cuDNN path on dense v
+            v = torch.empty(b, sq, nh, hd, dtype=a.dtype, device=a.device)  # dense v: SDPA keeps its cuDNN path
+            eb = y3.element_size()
+            check(lib().fcdp_copy_rows(rows_of(a), h * eb, C.c_void_p(y3.data_ptr() + 2 * h * eb), 3 * h * eb, P(v),
+                                       h * eb, st))
             ctx.save_for_backward(a, wq, aq, bq, bk, bv, xa3)
             ctx.nh = nh
             return q, k, v
@@ -462,7 +466,10 @@ def _fns():
                 dc = d.contiguous()
                 check(lib().fcdp_rope(b, sq, nh, hd, P(dc), 0, P(cs), P(sn), 1,
                                       C.c_void_p(dy3.data_ptr() + i * h * dy3.element_size()), 3 * h, st))
-            dy3[:, 2 * h:].view(b, sq, nh, hd).copy_(dv)
+            dvc = dv.contiguous()
+            eb = dy3.element_size()
+            check(lib().fcdp_copy_rows(rows, h * eb, P(dvc), h * eb, C.c_void_p(dy3.data_ptr() + 2 * h * eb), 3 * h * eb,
+                                       st))
             w3 = torch.as_strided(wq, (3 * h, h), (h, 1))
             ng = ctx.needs_input_grad
             da = dy3.mm(w3) if ng[0] else None
@@ -484,7 +491,33 @@ def _fns():
                     dB = [dy3[:, i * h:(i + 1) * h].t().mm(xa3[:, i * r:(i + 1) * r]) for i in range(3)]
             return (da.view(a.shape) if da is not None else None, *dw, *dA, *dB, None)
 
-    _FNS = (LinearBias, BiasGelu, CrossEntropy, Rope, GateUpSwiGLU, LlamaQKV)
+    class LoraLinear(torch.autograd.Function):
+        """y = x W^T + (x A^T) B^T (the add in the second GEMM's epilogue);
+        backward dx = dy W + (dy B) A with the second term accumulated in the
+        GEMM epilogue too (no autograd accumulation pass)."""
+
+        @staticmethod
+        def forward(ctx, x, w, a_, b_):
+            x2 = x.reshape(-1, x.shape[-1])
+            xa = x2.mm(a_.t())
+            y = torch.addmm(x2.mm(w.t()), xa, b_.t())
+            ctx.save_for_backward(x, w, a_, b_, xa)
+            return y.view(*x.shape[:-1], w.shape[0])
+
+        @staticmethod
+        def backward(ctx, dy):
+            x, w, a_, b_, xa = ctx.saved_tensors
+            x2 = x.reshape(-1, x.shape[-1])
+            dy2 = dy.reshape(-1, dy.shape[-1])
+            dxa = dy2.mm(b_)
+            ng = ctx.needs_input_grad
+            dx = dy2.mm(w).addmm_(dxa, a_).view(x.shape) if ng[0] else None
+            dw = dy2.t().mm(x2) if ng[1] else None
+            da = dxa.t().mm(x2) if ng[2] else None
+            db = dy2.t().mm(xa) if ng[3] else None
+            return dx, dw, da, db
+
+    _FNS = (LinearBias, BiasGelu, CrossEntropy, Rope, GateUpSwiGLU, LlamaQKV, LoraLinear)
     return _FNS
 
 
@@ -567,6 +600,8 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         a = F.rms_norm(x, (h,), p["attn_norm"], eps=1e-5)
 
         def proj(name, inp):
+            if f"{name}_A" in p and _fused_ok(inp, p[f"{name}_w"]):
+                return _fns()[6].apply(inp, p[f"{name}_w"], p[f"{name}_A"], p[f"{name}_B"])
             y = F.linear(inp, p[f"{name}_w"])
             if f"{name}_A" in p:
                 # y + (x A^T) B^T with the add in the LoRA GEMM's epilogue (addmm, beta = 1)

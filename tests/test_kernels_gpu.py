@@ -430,3 +430,19 @@ def test_copy_segments_exact(built):
     for t, x, sz in zip(srcs, offs, sizes):
         ref[x:x + sz] = t.cpu().numpy()[:sz]
     assert np.array_equal(host, ref)
+
+
+def test_copy_rows_exact(built):
+    """fcdp_copy_rows: a strided third of a [rows x 3h] matrix to a dense [rows x h] and back."""
+    from paper_2602_06499_b200._capi import check
+    dev = _dev()
+    lib = built
+    rows, h = 333, 264
+    src = torch.randint(-30000, 30000, (rows, 3 * h), dtype=torch.int16, device=dev)
+    dst = torch.zeros(rows, h, dtype=torch.int16, device=dev)
+    check(lib.fcdp_copy_rows(rows, h * 2, C.c_void_p(src.data_ptr() + 2 * h * 2), 3 * h * 2, _ptr(dst), h * 2, None))
+    back = torch.zeros_like(src)
+    check(lib.fcdp_copy_rows(rows, h * 2, _ptr(dst), h * 2, C.c_void_p(back.data_ptr() + h * 2), 3 * h * 2, None))
+    torch.cuda.synchronize()
+    assert torch.equal(dst, src[:, 2 * h:])
+    assert torch.equal(back[:, h:2 * h], src[:, 2 * h:]) and int(back[:, :h].abs().sum()) == 0

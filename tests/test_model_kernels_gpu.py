@@ -219,3 +219,23 @@ def test_llama_qkv_matches_fp32(built, lora):
         if p[n].requires_grad:
             assert p[n].grad is not None and p[n].grad.is_contiguous(), n
             assert _rel(p[n].grad, pr[n].grad) <= 1.5e-2, (n, _rel(p[n].grad, pr[n].grad))
+
+
+def test_lora_linear_matches_fp32(built):
+    """o projection with LoRA: y = xW^T + (xA^T)B^T, backward with the LoRA dgrad in the GEMM epilogue."""
+    from paper_2602_06499_b200.driving_model import _fns
+    import torch.nn.functional as F
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(5)
+    x = torch.randn(2, 50, 256, device=dev, generator=g).to(torch.bfloat16).requires_grad_(True)
+    w = (0.05 * torch.randn(256, 256, device=dev, generator=g)).to(torch.bfloat16)
+    A = (0.05 * torch.randn(8, 256, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    B = (0.05 * torch.randn(256, 8, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    dy = torch.randn(2, 50, 256, device=dev, generator=g).to(torch.bfloat16)
+    y = _fns()[6].apply(x, w, A, B)
+    y.backward(dy)
+    xr, Ar, Br = (t.detach().float().requires_grad_(True) for t in (x, A, B))
+    yr = F.linear(xr, w.float()) + F.linear(F.linear(xr, Ar), Br)
+    yr.backward(dy.float())
+    for o, r_, n in ((y, yr, "y"), (x.grad, xr.grad, "dx"), (A.grad, Ar.grad, "dA"), (B.grad, Br.grad, "dB")):
+        assert _rel(o, r_) <= 8e-3, (n, _rel(o, r_))
