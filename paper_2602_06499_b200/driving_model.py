@@ -517,7 +517,9 @@ def _fns():
             db = dy2.t().mm(xa) if ng[3] else None
             return dx, dw, da, db
 
-    _FNS = (LinearBias, BiasGelu, CrossEntropy, Rope, GateUpSwiGLU, LlamaQKV, LoraLinear)
+    from types import SimpleNamespace
+    _FNS = SimpleNamespace(LinearBias=LinearBias, BiasGelu=BiasGelu, CrossEntropy=CrossEntropy, Rope=Rope,
+                           GateUpSwiGLU=GateUpSwiGLU, LlamaQKV=LlamaQKV, LoraLinear=LoraLinear)
     return _FNS
 
 
@@ -529,7 +531,7 @@ def _llama_qkv(p, a, nh):
             and _adjacent(p["k_w"], p["v_w"])
             and (not lora or (_adjacent(p["q_A"], p["k_A"]) and _adjacent(p["k_A"], p["v_A"])))):
         args = [p[f"{n}_A"] for n in "qkv"] + [p[f"{n}_B"] for n in "qkv"] if lora else [None] * 6
-        return _fns()[5].apply(a, p["q_w"], p["k_w"], p["v_w"], *args, nh)
+        return _fns().LlamaQKV.apply(a, p["q_w"], p["k_w"], p["v_w"], *args, nh)
     return None
 
 
@@ -542,20 +544,20 @@ def _adjacent(a, b) -> bool:
 def _swiglu_mlp(m, wg, wu):
     import torch.nn.functional as F
     if _fused_ok(m, wg, wu) and wg.shape[0] % 8 == 0 and _adjacent(wg, wu):
-        return _fns()[4].apply(m, wg, wu)
+        return _fns().GateUpSwiGLU.apply(m, wg, wu)
     return F.silu(F.linear(m, wg)) * F.linear(m, wu)
 
 
 def _rope_fn(x):
     if _fused_ok(x) and x.shape[-1] % 8 == 0:
-        return _fns()[3].apply(x)
+        return _fns().Rope.apply(x)
     return _rope(x)
 
 
 def _linear_bias(x, w, b):
     import torch.nn.functional as F
     if _fused_ok(x, w, b) and w.shape[0] % 8 == 0:
-        return _fns()[0].apply(x, w, b)
+        return _fns().LinearBias.apply(x, w, b)
     return F.linear(x, w, b)
 
 
@@ -563,14 +565,14 @@ def _mlp_gelu(m, w, b):
     """gelu_tanh(m W^T + b): the GEMM without its bias, bias + GELU fused."""
     import torch.nn.functional as F
     if _fused_ok(m, w, b) and w.shape[0] % 8 == 0:
-        return _fns()[1].apply(F.linear(m, w), b)
+        return _fns().BiasGelu.apply(F.linear(m, w), b)
     return F.gelu(F.linear(m, w, b), approximate="tanh")
 
 
 def _cross_entropy(logits, labels):
     import torch.nn.functional as F
     if _fused_ok(logits) and logits.shape[-1] % 8 == 0:
-        return _fns()[2].apply(logits.reshape(-1, logits.shape[-1]), labels.reshape(-1))
+        return _fns().CrossEntropy.apply(logits.reshape(-1, logits.shape[-1]), labels.reshape(-1))
     return F.cross_entropy(logits.float().view(-1, logits.shape[-1]), labels.reshape(-1))
 
 
@@ -601,7 +603,7 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
 
         def proj(name, inp):
             if f"{name}_A" in p and _fused_ok(inp, p[f"{name}_w"]):
-                return _fns()[6].apply(inp, p[f"{name}_w"], p[f"{name}_A"], p[f"{name}_B"])
+                return _fns().LoraLinear.apply(inp, p[f"{name}_w"], p[f"{name}_A"], p[f"{name}_B"])
             y = F.linear(inp, p[f"{name}_w"])
             if f"{name}_A" in p:
                 # y + (x A^T) B^T with the add in the LoRA GEMM's epilogue (addmm, beta = 1)

@@ -203,11 +203,11 @@ class FcdpTrainer:
 def activation_bytes(cfg: ModelConfig, d: LayerDef, seq: int) -> int:
     """Activation bytes per sample of one layer, fed to the tau-admission
     projection (reference schedule.cpp:196-208): a bf16 transformer block with
-    flash attention keeps about 34 * seq * hidden bytes, the head its logits
-    (+ an fp32 copy)."""
+    flash attention keeps about 34 * seq * hidden bytes, the head its bf16 logits
+    and their gradient (the fused cross-entropy keeps no fp32 copy)."""
     ffn = cfg.ffn or 4 * cfg.hidden
     if d.kind == "head":
-        return seq * cfg.vocab_rows * 6
+        return seq * cfg.vocab_rows * (4 if cfg.dtype_bytes == 2 else 8)
     if d.kind == "embed":
         return seq * cfg.hidden * 2
     return int(seq * cfg.hidden * 34 * max(1.0, ffn / (4 * cfg.hidden)))

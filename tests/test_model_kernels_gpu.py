@@ -89,7 +89,7 @@ def test_bias_gelu_matches_fp32(built, rows, cols):
     from paper_2602_06499_b200.driving_model import _fns
     import torch.nn.functional as F
     dev = _dev()
-    BiasGelu = _fns()[1]
+    BiasGelu = _fns().BiasGelu
     g = torch.Generator(device=dev).manual_seed(rows + 3 * cols)
     h = (2 * torch.randn(rows, cols, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
     b = (0.5 * torch.randn(cols, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
@@ -232,7 +232,7 @@ def test_lora_linear_matches_fp32(built):
     A = (0.05 * torch.randn(8, 256, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
     B = (0.05 * torch.randn(256, 8, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
     dy = torch.randn(2, 50, 256, device=dev, generator=g).to(torch.bfloat16)
-    y = _fns()[6].apply(x, w, A, B)
+    y = _fns().LoraLinear.apply(x, w, A, B)
     y.backward(dy)
     xr, Ar, Br = (t.detach().float().requires_grad_(True) for t in (x, A, B))
     yr = F.linear(xr, w.float()) + F.linear(F.linear(xr, Ar), Br)
