@@ -368,10 +368,17 @@ def main():
 
     if world != args.gpus and world > 1:
         args.gpus = world
+    ndev = torch.cuda.device_count()
+    shared = world > ndev  # more ranks than GPUs (a functional check only: ranks share a GPU's compute)
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = torch.device("cpu") if shared else dev  # gloo for the bench's own barrier / reductions then
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     if args.topology:
         N, g = (int(x) for x in args.topology.lower().split("x"))
     else:
@@ -395,14 +402,14 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -499,7 +506,7 @@ def main():
         # no instrumentation and ZeRO-3 / FCDP are timed the same way
         tr.engine.set_timing(False)
         barrier()
-        sampler = ClockSampler(world) if (rank == 0 and timing) else None
+        sampler = ClockSampler(min(world, ndev)) if (rank == 0 and timing) else None
         if sampler:
             sampler.start()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
@@ -728,6 +735,8 @@ def main():
                                                    "region itself runs uninstrumented"},
         "loss": main_run["loss"], "ms_each_step_rank0": main_run["per_step"],
     }
+    if shared:  # several ranks per GPU: checks the N-rank flow, not a throughput number
+        line["config"]["ranks_per_gpu"] = world / ndev
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
