@@ -19,7 +19,7 @@ CLASSES = [("adamw_fused_rs", r"adam_grad_kernel"), ("adamw", r"adam_kernel"), (
            ("partition", r"partition_kernel"), ("fcdp_setup", r"(init_kernel|widen_kernel)"),
            ("grad_handoff", r"seg_copy_kernel"),
            # driving-model kernels (model_kernels.cu): the path's consumer, not the path
-           ("model_bias_gelu_fwd", r"bias_gelu_fwd_kernel"), ("model_gelu_bwd_bias_grad", r"colsum_partial_kernel<true>"),
+           ("model_bias_gelu_fwd", r"bias_gelu_fwd_kernel"), ("model_gelu_bwd_bias_grad", r"colsum_partial_kernel<(true|1)>"),
            ("model_bias_grad", r"colsum_(partial|final)_kernel"), ("model_layernorm", r"ln_(fwd|bwd)"),
            ("model_xent", r"xent_(fwd|bwd)_kernel"), ("model_rope", r"rope_kernel"), ("model_swiglu", r"swiglu_")]
 

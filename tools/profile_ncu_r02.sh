@@ -14,8 +14,9 @@ full() {  # name regex skip count
 }
 full adam 'adam_grad_kernel' 30 2
 full gelu_fwd 'bias_gelu_fwd_kernel' 30 1
-full gelu_bwd 'colsum_partial_kernel<true>' 30 1
-full bias_grad 'colsum_partial_kernel<false>' 90 1
+# colsum_partial_kernel per GPT-2 block backward: <false> fc2 bias, <true> GELU + fc bias, <false> proj, <false> qkv
+full gelu_bwd 'colsum_partial_kernel' 41 1
+full bias_grad 'colsum_partial_kernel' 40 1
 full xent 'xent_(fwd|bwd)_kernel' 2 2
 full ln 'ln_(fwd|bwd_dx)_kernel' 60 2
 echo profile-done
