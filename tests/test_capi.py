@@ -43,3 +43,22 @@ def test_no_cpu_fallback_for_data_plane(built):
     out = ctypes.c_void_p()
     rc = L.fcdp_layout_create(64, mask, 2, 1, 1, ctypes.byref(out))
     assert rc == -3, L.fcdp_last_error()
+
+
+def test_model_kernel_argument_errors(built):
+    """Shape / alignment contracts of the driving-model and copy entry points are
+    checked before any launch (FCDP_ERR_CONFIG on a CPU-only box too)."""
+    from paper_2602_06499_b200 import _capi
+    lib = _capi.lib()
+    P = ctypes.c_void_p
+    assert lib.fcdp_bias_grad(8, 12, None, None, None, 1, None) == -1  # cols % 8
+    assert lib.fcdp_bias_gelu_fwd(8, 10, None, None, None, None) == -1
+    assert lib.fcdp_bias_gelu_bwd(8, 10, None, None, None, None, None, None, 1, None) == -1
+    assert lib.fcdp_xent_fwd(8, 50257, None, None, None, None, None) == -1  # vocab % 8
+    assert lib.fcdp_xent_bwd(8, 50257, None, None, None, None, None, None) == -1
+    assert lib.fcdp_rope(1, 4, 2, 12, None, 0, None, None, 0, None, 0, None) == -1  # head dim % 8
+    assert lib.fcdp_rope(1, 4, 2, 16, None, 24, None, None, 0, None, 0, None) == -1  # stride < heads * dim
+    assert lib.fcdp_swiglu_fwd(4, 12, None, 12, None, 12, None, None) == -1
+    assert lib.fcdp_swiglu_bwd(4, 16, None, None, 16, None, 20, None, 16, None, 16, None) == -1  # stride % 8
+    assert lib.fcdp_copy_segments(-1, None, None, None, None) == -1
+    assert b"multiple" in lib.fcdp_last_error() or b"negative" in lib.fcdp_last_error()
