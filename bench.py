@@ -414,23 +414,35 @@ def main():
         return float(t.item())
 
     def pcie_peak() -> dict:
-        """Pinned host <-> this GPU copy rate, all ranks at once (the host link
-        peak the engine's copies are judged against), measured in this run."""
+        """Pinned host <-> this GPU copy rate, measured in this run: each rank
+        alone in turn (the link's peak: the denominator the engine's copies are
+        judged against) and all ranks at once (what a shared host delivers)."""
         n = 256 << 20
         h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
         d = torch.empty(n, dtype=torch.uint8, device=dev)
-        out = {}
-        for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
-            fn()
-            torch.cuda.synchronize()
-            barrier()
+        fns = (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True)))
+
+        def rate(fn):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             for _ in range(4):
                 fn()
             b.record()
             b.synchronize()
-            out[name] = 4 * n / (a.elapsed_time(b) / 1e3) / 1e9
+            return 4 * n / (a.elapsed_time(b) / 1e3) / 1e9
+
+        out = {}
+        for name, fn in fns:
+            fn()
+            torch.cuda.synchronize()
+            alone = None
+            for r in range(world):  # one rank at a time
+                barrier()
+                if r == rank:
+                    alone = rate(fn)
+            barrier()
+            out[name] = alone
+            out[name + "_all_ranks_at_once"] = rate(fn)
         del h, d
         return out
 
