@@ -851,7 +851,7 @@ cudaError_t launch_adam(std::int64_t n, const AdamParams& p, float* master, floa
 
 cudaError_t launch_adam_grad(std::int64_t chunks, const GradSegs& segs, const AdamParams& p, float scale,
                              float* master, float* m, float* v, void* param, int param_elem_bytes, float* keep_grad,
-                             cudaStream_t s) {
+                             cudaStream_t s, int max_blocks) {
   if (chunks <= 0) return cudaSuccess;
   if (segs.n < 0 || segs.n > kMaxGradSegs) return cudaErrorInvalidValue;
   const std::int64_t V = kChunkBytes / param_elem_bytes;
@@ -873,7 +873,8 @@ cudaError_t launch_adam_grad(std::int64_t chunks, const GradSegs& segs, const Ad
   }
   push(at, chunks - at, nullptr);
   // grid shares proportional to segment size (at least one block each)
-  const int total = grid_for(chunks * V / 4, kThreads * 2);
+  int total = grid_for(chunks * V / 4, kThreads * 2);
+  if (max_blocks > 0) total = std::max(std::min(total, max_blocks - cv.n), 1);  // each segment adds >= 1 block
   int b = 0;
   for (int i = 0; i < cv.n; ++i) {
     cv.block0[i] = b;

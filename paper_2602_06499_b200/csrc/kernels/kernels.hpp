@@ -56,9 +56,11 @@ struct GradSegs {
   std::int64_t nchunks[kMaxGradSegs];
   const void* src[kMaxGradSegs];
 };
+// max_blocks > 0 caps the grid (e.g. one CTA per SM, so each SM keeps room for
+// a concurrently running GEMM CTA beside it).
 cudaError_t launch_adam_grad(std::int64_t chunks, const GradSegs& segs, const AdamParams& p, float scale,
                              float* master, float* m, float* v, void* param, int param_elem_bytes, float* keep_grad,
-                             cudaStream_t s);
+                             cudaStream_t s, int max_blocks = 0);
 
 // Deterministic init of a natural layer; `ranges` is a device array.
 struct InitRange {

@@ -205,15 +205,22 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   {
     const char* e = std::getenv("FCDP_OPT_PRIO");
     opt_low_ = e && std::strcmp(e, "low") == 0;
-    // Default: the fused update runs on the compute stream right after the
-    // layer's backward.  On the high-priority side stream its CTAs could not
-    // co-reside with the backward GEMMs' anyway (they queued for whole SMs), so
-    // the step time is the same (A/B on one box: 69.46-69.55 ms both ways,
-    // profiles/r02_ab_opt_stream.json) while its own launches run unqueued:
-    // 0.85 instead of 0.63 of the HBM roofline.  FCDP_OPT_STREAM=rs restores
-    // the side stream, FCDP_OPT_PRIO=low the low-priority one.
+    // Default: the fused update runs on the high-priority RS stream, its grid
+    // capped at ONE CTA per SM (16 K registers, no shared memory).  The backward
+    // GEMMs' CTAs (256 threads x 168 registers, 213 KB shared memory; ncu,
+    // profiles/r02_gemm_resources.csv) leave exactly that much room on each SM,
+    // so the update streams beside them instead of taking whole SMs.  A/B/C on
+    // one box (profiles/r02_ab_opt_stream.json): 69.3 ms per step, against
+    // 71.2 ms serialised on the compute stream and 71.3 ms with two CTAs per SM
+    // (which no longer fit beside a GEMM CTA).  Its live rate per launch is
+    // then lower by design (the launch spans the GEMMs it runs beside).
+    // FCDP_OPT_STREAM=compute serialises it on the compute stream,
+    // FCDP_OPT_PRIO=low moves it to the low-priority stream, and
+    // FCDP_OPT_CTAS_PER_SM=k sets the cap (0 = the full grid).
     const char* c = std::getenv("FCDP_OPT_STREAM");
-    opt_on_compute_ = !opt_low_ && !(c && std::strcmp(c, "rs") == 0);
+    opt_on_compute_ = !opt_low_ && c && std::strcmp(c, "compute") == 0;
+    const char* k = std::getenv("FCDP_OPT_CTAS_PER_SM");
+    opt_ctas_per_sm_ = k ? std::atoi(k) : (opt_on_compute_ ? 0 : 1);
   }
   for (auto& e : fin_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1152,7 +1159,8 @@ void Engine::ev_reduce_scatter(const Event& e) {
     const std::uint64_t bytes = static_cast<std::uint64_t>(n) * (6 * sizeof(float) + 2 * eb_ + (keep_grad_ ? 4 : 0));
     timed(3, s, bytes, [&] {
       return launch_adam_grad(l.chunks, grad_segs_[li], p, scale, master_ + o, adam_m_ + o, adam_v_ + o,
-                              param_t_ + l.off_t * kChunkBytes, eb_, keep_grad_ ? grad32_ + o : nullptr, s);
+                              param_t_ + l.off_t * kChunkBytes, eb_, keep_grad_ ? grad32_ + o : nullptr, s,
+                              opt_ctas_per_sm_ * sm_count());
     });
     stepped_[li] = 1;
     write_flag(s, kGradFree, u);

@@ -220,7 +220,8 @@ class Engine {
   cudaStream_t s_opt_ = nullptr;   // G = 1 fused RS + AdamW when FCDP_OPT_PRIO=low (else compute stream)
   cudaEvent_t opt_fork_ = nullptr;
   bool opt_low_ = false;
-  bool opt_on_compute_ = true;  // the G = 1 fused update on the compute stream (FCDP_OPT_STREAM=rs: side stream)
+  int opt_ctas_per_sm_ = 1;      // grid cap of the G = 1 fused update, CTAs per SM (0 = full grid)
+  bool opt_on_compute_ = false;  // FCDP_OPT_STREAM=compute: the G = 1 fused update serialised on the compute stream
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, u_ = 0;
