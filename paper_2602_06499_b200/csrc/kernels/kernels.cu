@@ -776,7 +776,8 @@ cudaError_t launch_expand(const Layout& L, const SlicePtrs& ts, const SlicePtrs&
 }
 
 cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n, float scale,
-                            bool final_scale, float* own_out, void* wire_out, cudaStream_t s) {
+                            bool final_scale, float* own_out, void* wire_out, cudaStream_t s,
+                            int max_blocks) {
   RsArgs a;
   a.k0 = j * L.dev.slice_t;
   a.k1 = std::min<std::int64_t>((j + 1) * L.dev.slice_t, L.dev.pt);
@@ -792,8 +793,9 @@ cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n
   const bool sparse = !dense && L.dev.ntwords > 0;
   const std::int64_t wb = dense ? 0 : (sparse ? L.rs_tw_begin[j] : L.rs_word_begin[j]);
   const std::int64_t we = dense ? 0 : (sparse ? L.rs_tw_end[j] : L.rs_word_end[j]);
-  const int grid = dense ? grid_for(a.k1 - a.k0, kThreads * std::max(1, 8 / L.dev.local))
-                         : grid_for((we - wb) * 32, kThreads);
+  int grid = dense ? grid_for(a.k1 - a.k0, kThreads * std::max(1, 8 / L.dev.local))
+                   : grid_for((we - wb) * 32, kThreads);
+  if (max_blocks > 0) grid = std::min(grid, max_blocks);
   auto go = [&](auto tag_t, auto tag_g) {
     using T = decltype(tag_t);
     constexpr int G = decltype(tag_g)::value;

@@ -30,8 +30,9 @@ cudaError_t launch_expand(const Layout& L, const SlicePtrs& ts, const SlicePtrs&
                           int set, cudaStream_t s);
 
 // Intra-node reduce-scatter of the trainable gradient for slice `j`.
+// max_blocks > 0 caps the grid (the RS then streams beside concurrently running GEMM CTAs).
 cudaError_t launch_rs_slice(const Layout& L, const GradPtrs& grads, int j, int n, float scale,
-                            bool final_scale, float* own_out, void* wire_out, cudaStream_t s);
+                            bool final_scale, float* own_out, void* wire_out, cudaStream_t s, int max_blocks = 0);
 
 // Inter-node epilogue: out = scale * sum_m part_m (fixed order).
 cudaError_t launch_rs_finalize(std::int64_t n_elems, int nodes, int node, int elem_bytes,

@@ -221,6 +221,8 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
     opt_on_compute_ = !opt_low_ && c && std::strcmp(c, "compute") == 0;
     const char* k = std::getenv("FCDP_OPT_CTAS_PER_SM");
     opt_ctas_per_sm_ = k ? std::atoi(k) : (opt_on_compute_ ? 0 : 1);
+    const char* r = std::getenv("FCDP_RS_CTAS_PER_SM");
+    rs_ctas_per_sm_ = r ? std::atoi(r) : 0;
   }
   for (auto& e : fin_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1168,6 +1170,11 @@ void Engine::ev_reduce_scatter(const Event& e) {
     grad_slot_of_layer_[li] = -1;
     return;
   }
+  // FCDP_RS_CTAS_PER_SM=k caps the RS grid at k CTAs per SM (default 0: the
+  // full grid).  Unlike the G = 1 fused update, capping measured no gain at
+  // N > 1 (2x1 / 2x2: same step time, lower per-launch rate;
+  // profiles/r02_ab_rs_cap.json): the step there is NIC-bound.
+  const int rs_blocks = rs_ctas_per_sm_ * sm_count();
   // algorithmic bytes: g gradient slices read + fp32 own shard + dtype wire for the rest
   const std::uint64_t rs_bytes = static_cast<std::uint64_t>(g_) * l.slice_real_t * C +
                                  static_cast<std::uint64_t>(l.my_real_t) * V_ * sizeof(float) +
@@ -1176,13 +1183,14 @@ void Engine::ev_reduce_scatter(const Event& e) {
     // every contribution (this node's included) in the wire dtype, so all
     // replicas sum identical values in the same order
     timed(1, s, static_cast<std::uint64_t>(g_ + 1) * l.slice_real_t * C, [&] {
-      return launch_rs_slice(l.L, gp, j_, -1, scale, false, nullptr, rx_[gs] + n_ * l.L.dev.shard_t * C, s);
+      return launch_rs_slice(l.L, gp, j_, -1, scale, false, nullptr, rx_[gs] + n_ * l.L.dev.shard_t * C, s, rs_blocks);
     }, static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
   } else if (N_ == 1) {
-    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, 0, scale, true, final_out, wire_[gs], s); },
+    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, 0, scale, true, final_out, wire_[gs], s, rs_blocks); },
           static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
   } else {
-    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, n_, scale, false, own32_[gs], wire_[gs], s); },
+    timed(1, s, rs_bytes, [&] { return launch_rs_slice(l.L, gp, j_, n_, scale, false, own32_[gs], wire_[gs], s,
+                                                       rs_blocks); },
           static_cast<std::uint64_t>(g_ - 1) * l.slice_real_t * C);
   }
   write_flag(s, kGradFree, u);
