@@ -293,6 +293,18 @@ int fcdp_copy_rows(int64_t rows, int64_t row_bytes, const void* src, int64_t src
  * (LoRA) layer into the engine's natural gradient slot. */
 int fcdp_copy_segments(int32_t n, const void* const* src, void* const* dst, const int64_t* bytes, void* stream);
 
+/* Driving-model GPT-2 MLP GEMMs with fused cuBLASLt epilogues (bf16, row-major):
+ * forward act = gelu_tanh(x W^T + b) with aux = x W^T + b kept for the backward;
+ * backward of the second linear's input gradient dpre = (dy W2) * gelu'(aux) with
+ * db1 = sum over rows of dpre.  libcublasLt is resolved at run time;
+ * fcdp_mlp_gemm_available() = 0 when it cannot be (the calls then answer
+ * FCDP_ERR_CONFIG). */
+int fcdp_mlp_gemm_available(void);
+int fcdp_fc_gelu_fwd(int64_t rows, int64_t in, int64_t out, const void* x, const void* w, const void* b, void* act,
+                     void* aux, void* stream);
+int fcdp_fc2_dgrad_dgelu(int64_t rows, int64_t hidden, int64_t ffn, const void* dy, const void* w2, const void* aux,
+                         void* dpre, void* db1, void* stream);
+
 /* Let kernels launched on `device` dereference `peer`'s memory over NVLink
  * (single-process multi-GPU use of the stateless kernels; the engine itself
  * maps peers through CUDA IPC). */

@@ -163,6 +163,9 @@ SIGNATURES = {
     "fcdp_swiglu_bwd": (C.c_int, [i64, i32, P, P, i64, P, i64, P, i64, P, i64, P]),
     "fcdp_copy_rows": (C.c_int, [i64, i64, P, i64, P, i64, P]),
     "fcdp_copy_segments": (C.c_int, [i32, PP, PP, C.POINTER(C.c_int64), P]),
+    "fcdp_mlp_gemm_available": (C.c_int, []),
+    "fcdp_fc_gelu_fwd": (C.c_int, [i64, i64, i64, P, P, P, P, P, P]),
+    "fcdp_fc2_dgrad_dgelu": (C.c_int, [i64, i64, i64, P, P, P, P, P, P]),
     "fcdp_numa_parse_cpulist": (C.c_int, [C.c_char_p, C.POINTER(i32), i32, C.POINTER(i32)]),
     "fcdp_numa_selftest": (C.c_int, [i32, C.c_uint64, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
                                      C.POINTER(i32), C.POINTER(i32)]),

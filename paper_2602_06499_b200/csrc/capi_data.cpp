@@ -9,6 +9,7 @@
 #include "common/layout.hpp"
 #include "fcdp.h"
 #include "kernels/kernels.hpp"
+#include "kernels/model_gemm.hpp"
 #include "kernels/model_kernels.hpp"
 
 struct fcdp_layout {
@@ -259,6 +260,34 @@ int fcdp_copy_segments(int32_t n, const void* const* src, void* const* dst, cons
     if (n < 0) throw shardsim::ConfigError("copy_segments: negative count");
     check_cuda(fcdp::launch_copy_segments(n, src, dst, bytes, static_cast<cudaStream_t>(stream)),
                "fcdp_copy_segments (16-byte aligned pointers and sizes)");
+  });
+}
+
+int fcdp_mlp_gemm_available(void) { return fcdp::mlp_gemm_available(nullptr) ? 1 : 0; }
+
+int fcdp_fc_gelu_fwd(int64_t rows, int64_t in, int64_t out, const void* x, const void* w, const void* b, void* act,
+                     void* aux, void* stream) {
+  return guarded([&] {
+    std::string why;
+    if (!fcdp::mlp_gemm_available(&why)) throw shardsim::ConfigError("fc_gelu: " + why);
+    if (in % 8 || out % 8) throw shardsim::ConfigError("fc_gelu: in and out must be multiples of 8");
+    std::string err;
+    if (fcdp::launch_fc_gelu_fwd(rows, in, out, x, w, b, act, aux, static_cast<cudaStream_t>(stream), &err) !=
+        cudaSuccess)
+      throw fcdp::CudaError("fcdp_fc_gelu_fwd: " + err);
+  });
+}
+
+int fcdp_fc2_dgrad_dgelu(int64_t rows, int64_t hidden, int64_t ffn, const void* dy, const void* w2, const void* aux,
+                         void* dpre, void* db1, void* stream) {
+  return guarded([&] {
+    std::string why;
+    if (!fcdp::mlp_gemm_available(&why)) throw shardsim::ConfigError("fc2_dgrad_dgelu: " + why);
+    if (hidden % 8 || ffn % 8) throw shardsim::ConfigError("fc2_dgrad_dgelu: hidden and ffn must be multiples of 8");
+    std::string err;
+    if (fcdp::launch_fc2_dgrad_dgelu(rows, hidden, ffn, dy, w2, aux, dpre, db1, static_cast<cudaStream_t>(stream),
+                                     &err) != cudaSuccess)
+      throw fcdp::CudaError("fcdp_fc2_dgrad_dgelu: " + err);
   });
 }
 

@@ -517,8 +517,50 @@ def _fns():
             db = dy2.t().mm(xa) if ng[3] else None
             return dx, dw, da, db
 
+    class GptMlp(torch.autograd.Function):
+        """fc2(gelu_tanh(fc(m))) with the bias + GELU in the fc GEMM's cuBLASLt
+        epilogue (GELU_AUX_BIAS, the pre-activation kept as aux) and, in the
+        backward, the GELU derivative and the fc bias gradient in the epilogue of
+        the fc2 input-gradient GEMM (DGELU_BGRAD): no separate elementwise pass
+        on the [tokens x 4h] activations in either direction."""
+
+        @staticmethod
+        def forward(ctx, m, fc_w, fc_b, fc2_w, fc2_b):
+            h = m.shape[-1]
+            ffn = fc_w.shape[0]
+            m2 = m.reshape(-1, h)
+            if not m2.is_contiguous():
+                m2 = m2.contiguous()
+            rows = m2.shape[0]
+            act = torch.empty(rows, ffn, dtype=m.dtype, device=m.device)
+            aux = torch.empty_like(act)
+            check(lib().fcdp_fc_gelu_fwd(rows, h, ffn, P(m2), P(fc_w), P(fc_b), P(act), P(aux), S(m.device)))
+            out = torch.nn.functional.linear(act, fc2_w, fc2_b)
+            ctx.save_for_backward(m2, fc_w, fc2_w, act, aux)
+            ctx.mshape = m.shape
+            return out.view(*m.shape[:-1], fc2_w.shape[0])
+
+        @staticmethod
+        def backward(ctx, dout):
+            m2, fc_w, fc2_w, act, aux = ctx.saved_tensors
+            rows, ffn = act.shape
+            h = m2.shape[1]
+            d2 = dout.reshape(rows, -1)
+            if not d2.is_contiguous():
+                d2 = d2.contiguous()
+            ng = ctx.needs_input_grad
+            d_fc2_b = bias_grad(d2) if ng[4] else None
+            d_fc2_w = d2.t().mm(act) if ng[3] else None
+            dpre = torch.empty_like(aux)
+            d_fc_b = torch.empty(ffn, dtype=aux.dtype, device=aux.device)
+            check(lib().fcdp_fc2_dgrad_dgelu(rows, d2.shape[1], ffn, P(d2), P(fc2_w), P(aux), P(dpre), P(d_fc_b),
+                                             S(aux.device)))
+            d_fc_w = dpre.t().mm(m2) if ng[1] else None
+            dm = dpre.mm(fc_w).view(ctx.mshape) if ng[0] else None
+            return dm, d_fc_w, (d_fc_b if ng[2] else None), d_fc2_w, d_fc2_b
+
     from types import SimpleNamespace
-    _FNS = SimpleNamespace(LinearBias=LinearBias, BiasGelu=BiasGelu, CrossEntropy=CrossEntropy, Rope=Rope,
+    _FNS = SimpleNamespace(GptMlp=GptMlp, LinearBias=LinearBias, BiasGelu=BiasGelu, CrossEntropy=CrossEntropy, Rope=Rope,
                            GateUpSwiGLU=GateUpSwiGLU, LlamaQKV=LlamaQKV, LoraLinear=LoraLinear)
     return _FNS
 
@@ -569,6 +611,23 @@ def _mlp_gelu(m, w, b):
     return F.gelu(F.linear(m, w, b), approximate="tanh")
 
 
+_MLP_LT = None
+
+
+def _gpt2_mlp(m, p):
+    """fc2(gelu_tanh(fc(m) + b1)) + b2: cuBLASLt epilogue fusion when libcublasLt
+    resolves (fcdp_mlp_gemm_available), else the bias + GELU kernels."""
+    global _MLP_LT
+    if _fused_ok(m, p["fc_w"]) and p["fc_w"].shape[0] % 8 == 0 and m.shape[-1] % 8 == 0:
+        if _MLP_LT is None:
+            import os
+            from ._capi import lib
+            _MLP_LT = os.environ.get("FCDP_MLP_LT", "0") != "0" and lib().fcdp_mlp_gemm_available() == 1
+        if _MLP_LT:
+            return _fns().GptMlp.apply(m, p["fc_w"], p["fc_b"], p["fc2_w"], p["fc2_b"])
+    return _linear_bias(_mlp_gelu(m, p["fc_w"], p["fc_b"]), p["fc2_w"], p["fc2_b"])
+
+
 def _cross_entropy(logits, labels):
     import torch.nn.functional as F
     if _fused_ok(logits) and logits.shape[-1] % 8 == 0:
@@ -596,7 +655,7 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), is_causal=True)
         x = x + _linear_bias(o.transpose(1, 2).reshape(b, s, h), p["proj_w"], p["proj_b"])
         m = _layer_norm(x, p["ln2_w"], p["ln2_b"])
-        return x + _linear_bias(_mlp_gelu(m, p["fc_w"], p["fc_b"]), p["fc2_w"], p["fc2_b"])
+        return x + _gpt2_mlp(m, p)
     if ldef.kind == "llama_block":
         b, s, _ = x.shape
         a = F.rms_norm(x, (h,), p["attn_norm"], eps=1e-5)

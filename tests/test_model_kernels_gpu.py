@@ -239,3 +239,68 @@ def test_lora_linear_matches_fp32(built):
     yr.backward(dy.float())
     for o, r_, n in ((y, yr, "y"), (x.grad, xr.grad, "dx"), (A.grad, Ar.grad, "dA"), (B.grad, Br.grad, "dB")):
         assert _rel(o, r_) <= 8e-3, (n, _rel(o, r_))
+
+
+@pytest.mark.parametrize("rows,h", [(8192, 2048), (300, 256)])
+def test_gpt2_mlp_cublaslt_epilogues_match_fp32(built, rows, h):
+    """GPT-2 MLP with bias + tanh-GELU in the fc GEMM epilogue and GELU' + fc bias
+    gradient in the fc2-dgrad GEMM epilogue (cuBLASLt) vs fp32."""
+    from paper_2602_06499_b200._capi import lib
+    from paper_2602_06499_b200.driving_model import _fns
+    import torch.nn.functional as F
+    dev = _dev()
+    if lib().fcdp_mlp_gemm_available() != 1:
+        pytest.skip("libcublasLt not resolvable in this process")
+    g = torch.Generator(device=dev).manual_seed(rows + h)
+    f = 4 * h
+    m = torch.randn(rows, h, device=dev, generator=g).to(torch.bfloat16).requires_grad_(True)
+    ws = [(torch.randn(f, h, device=dev, generator=g) / h ** 0.5), 0.5 * torch.randn(f, device=dev, generator=g),
+          (torch.randn(h, f, device=dev, generator=g) / f ** 0.5), 0.1 * torch.randn(h, device=dev, generator=g)]
+    ws = [w.to(torch.bfloat16).requires_grad_(True) for w in ws]
+    dy = torch.randn(rows, h, device=dev, generator=g).to(torch.bfloat16)
+    y = _fns().GptMlp.apply(m, *ws)
+    y.backward(dy)
+
+    def ref(approx):
+        mr = m.detach().float().requires_grad_(True)
+        wr = [w.detach().float().requires_grad_(True) for w in ws]
+        yr = F.linear(F.gelu(F.linear(mr, wr[0], wr[1]), approximate=approx), wr[2], wr[3])
+        yr.backward(dy.float())
+        return yr, mr.grad, [w.grad for w in wr]
+
+    yr, dmr, dwr = ref("tanh")
+    mt = m.detach().clone().requires_grad_(True)
+    wt = [w.detach().clone().requires_grad_(True) for w in ws]
+    yt = F.linear(F.gelu(F.linear(mt, wt[0], wt[1]), approximate="tanh"), wt[2], wt[3])
+    yt.backward(dy)
+    for ours, theirs, r_, name in [(y, yt, yr, "y"), (m.grad, mt.grad, dmr, "dm")] + \
+            [(w.grad, t.grad, r, f"dw{i}") for i, (w, t, r) in enumerate(zip(ws, wt, dwr))]:
+        e_ours, e_torch = _rel(ours, r_), _rel(theirs, r_)
+        assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
+
+
+def test_cublaslt_gelu_epilogue_is_tanh_gelu(built):
+    """With W = I the fc GEMM is exact, so the epilogue's act = GELU(x + b) can be
+    compared element by element: it rounds to the tanh-approximation GELU, not the erf one."""
+    import ctypes as C
+    from paper_2602_06499_b200._capi import check, lib
+    import torch.nn.functional as F
+    dev = _dev()
+    if lib().fcdp_mlp_gemm_available() != 1:
+        pytest.skip("libcublasLt not resolvable in this process")
+    g = torch.Generator(device=dev).manual_seed(3)
+    n = 256
+    x = (3 * torch.randn(512, n, device=dev, generator=g)).to(torch.bfloat16)
+    b = torch.zeros(n, device=dev, dtype=torch.bfloat16)
+    w = torch.eye(n, device=dev, dtype=torch.bfloat16)
+    act = torch.empty_like(x)
+    aux = torch.empty_like(x)
+    P = lambda t: C.c_void_p(t.data_ptr())
+    check(lib().fcdp_fc_gelu_fwd(512, n, n, P(x), P(w), P(b), P(act), P(aux), None))
+    torch.cuda.synchronize()
+    assert torch.equal(aux, x)
+    tanh_ref = F.gelu(x.float(), approximate="tanh").to(torch.bfloat16)
+    erf_ref = F.gelu(x.float()).to(torch.bfloat16)
+    match_tanh = (act == tanh_ref).float().mean().item()
+    match_erf = (act == erf_ref).float().mean().item()
+    assert match_tanh > 0.97 and match_tanh > match_erf, (match_tanh, match_erf)
