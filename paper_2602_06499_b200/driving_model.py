@@ -615,8 +615,10 @@ _MLP_LT = None
 
 
 def _gpt2_mlp(m, p):
-    """fc2(gelu_tanh(fc(m) + b1)) + b2: cuBLASLt epilogue fusion when libcublasLt
-    resolves (fcdp_mlp_gemm_available), else the bias + GELU kernels."""
+    """fc2(gelu_tanh(fc(m) + b1)) + b2 with the bias + GELU kernels.  FCDP_MLP_LT=1
+    selects the cuBLASLt epilogue fusion instead (GptMlp): correct, but the
+    epilogue GEMMs the heuristic picks are slower on B200 - 80.4-82.0 ms per
+    GPT-2 1.3B step against 68.5-68.7 ms (profiles/r02_ab_mlp_epilogue.json)."""
     global _MLP_LT
     if _fused_ok(m, p["fc_w"]) and p["fc_w"].shape[0] % 8 == 0 and m.shape[-1] % 8 == 0:
         if _MLP_LT is None:
