@@ -325,7 +325,7 @@ def _fns():
             lc = logits.contiguous()
             V = lc.shape[-1]
             rows = lc.numel() // V
-            lab = labels.reshape(-1).contiguous()
+            lab = labels.reshape(-1).to(torch.int64).contiguous()  # the kernel reads int64 labels
             loss = torch.empty(rows, dtype=torch.float32, device=lc.device)
             lse = torch.empty_like(loss)
             check(lib().fcdp_xent_fwd(rows, V, P(lc), P(lab), P(loss), P(lse), S(lc.device)))
