@@ -663,11 +663,12 @@ def main():
         # a few MB per launch (PEFT trainable slices): launch latency, not bandwidth, bounds it
         roofline["note"] = f"{per_launch_bytes / 1e6:.1f} MB per launch: launch-latency regime"
     elif dom == "adamw" and world == 1:
-        roofline["note"] = ("G = 1 fused reduce-scatter + AdamW: in the step it runs beside the next layers' backward "
-                            "GEMMs on a side stream with ONE CTA per SM (the room a GEMM CTA leaves), so a live launch "
-                            "spans the GEMMs it overlaps: live = CUDA events around each launch; isolated = the kernel "
-                            "alone with its full grid.  FCDP_OPT_STREAM=compute serialises it instead (live ~ isolated, "
-                            "+1.9 ms per step, profiles/r02_ab_opt_stream.json)")
+        if os.environ.get("FCDP_OPT_STREAM") == "rs":
+            roofline["note"] = ("G = 1 fused reduce-scatter + AdamW beside the backward GEMMs (FCDP_OPT_STREAM=rs, one "
+                                "CTA per SM): a live launch spans the GEMMs it overlaps; isolated = full grid alone")
+        else:
+            roofline["note"] = ("G = 1 fused reduce-scatter + AdamW on the compute stream after each layer's backward "
+                                "(live = CUDA events around each launch in the step); isolated = the same launch alone")
     elif dom in ("adamw", "rs_slice"):
         # the per-layer update / reduce-scatter runs on its own stream beside the
         # backward GEMMs of the next layers, off the compute stream's critical path;

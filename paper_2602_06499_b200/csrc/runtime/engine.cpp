@@ -205,20 +205,19 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
   {
     const char* e = std::getenv("FCDP_OPT_PRIO");
     opt_low_ = e && std::strcmp(e, "low") == 0;
-    // Default: the fused update runs on the high-priority RS stream, its grid
-    // capped at ONE CTA per SM (16 K registers, no shared memory).  The backward
+    // Default: the fused update runs on the compute stream right after the
+    // layer's backward, with its full grid (0.85 of the HBM copy rate per launch).
+    // FCDP_OPT_STREAM=rs runs it on the high-priority RS stream with its grid
+    // capped at ONE CTA per SM (16 K registers, no shared memory): the backward
     // GEMMs' CTAs (256 threads x 168 registers, 213 KB shared memory; ncu,
-    // profiles/r02_gemm_resources.csv) leave exactly that much room on each SM,
-    // so the update streams beside them instead of taking whole SMs.  A/B/C on
-    // one box (profiles/r02_ab_opt_stream.json): 69.3 ms per step, against
-    // 71.2 ms serialised on the compute stream and 71.3 ms with two CTAs per SM
-    // (which no longer fit beside a GEMM CTA).  Its live rate per launch is
-    // then lower by design (the launch spans the GEMMs it runs beside).
-    // FCDP_OPT_STREAM=compute serialises it on the compute stream,
-    // FCDP_OPT_PRIO=low moves it to the low-priority stream, and
-    // FCDP_OPT_CTAS_PER_SM=k sets the cap (0 = the full grid).
+    // profiles/r02_gemm_resources.csv) leave exactly that much room per SM, so
+    // it streams beside them.  A/B/C on one box (profiles/r02_ab_opt_stream.json):
+    // 69.3 ms per step against 71.2 ms serialised, 71.3 ms with two CTAs per SM
+    // (no longer fits beside a GEMM CTA); each launch then spans the GEMMs it
+    // overlaps, about 0.37 of the roofline per launch.  FCDP_OPT_PRIO=low uses
+    // the low-priority stream, FCDP_OPT_CTAS_PER_SM=k sets the cap (0 = full grid).
     const char* c = std::getenv("FCDP_OPT_STREAM");
-    opt_on_compute_ = !opt_low_ && c && std::strcmp(c, "compute") == 0;
+    opt_on_compute_ = !opt_low_ && !(c && std::strcmp(c, "rs") == 0);
     const char* k = std::getenv("FCDP_OPT_CTAS_PER_SM");
     opt_ctas_per_sm_ = k ? std::atoi(k) : (opt_on_compute_ ? 0 : 1);
     const char* r = std::getenv("FCDP_RS_CTAS_PER_SM");

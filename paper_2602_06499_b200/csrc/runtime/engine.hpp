@@ -221,8 +221,8 @@ class Engine {
   cudaEvent_t opt_fork_ = nullptr;
   bool opt_low_ = false;
   int rs_ctas_per_sm_ = 0;       // FCDP_RS_CTAS_PER_SM: grid cap of the RS kernel (0 = full grid)
-  int opt_ctas_per_sm_ = 1;      // grid cap of the G = 1 fused update, CTAs per SM (0 = full grid)
-  bool opt_on_compute_ = false;  // FCDP_OPT_STREAM=compute: the G = 1 fused update serialised on the compute stream
+  int opt_ctas_per_sm_ = 0;      // grid cap of the G = 1 fused update, CTAs per SM (0 = full grid)
+  bool opt_on_compute_ = true;  // the G = 1 fused update on the compute stream (FCDP_OPT_STREAM=rs: beside the GEMMs)
 
   // sequence counters (identical on every rank)
   std::uint32_t q_ = 0, u_ = 0;
