@@ -17,7 +17,6 @@ from __future__ import annotations
 import os
 from typing import Dict, List, Optional
 
-import numpy as np
 import torch
 
 from . import shardsim as S

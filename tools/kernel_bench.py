@@ -11,7 +11,6 @@ Short enough to run under `ncu --set full`.
 import argparse
 import ctypes as C
 import json
-import os
 import sys
 from pathlib import Path
 

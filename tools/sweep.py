@@ -8,7 +8,6 @@ records tokens/s and the measured inter-group bytes per node per step.
 """
 import argparse
 import json
-import os
 import subprocess
 import sys
 from pathlib import Path
