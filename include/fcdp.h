@@ -305,6 +305,10 @@ int fcdp_fc_gelu_fwd(int64_t rows, int64_t in, int64_t out, const void* x, const
 int fcdp_fc2_dgrad_dgelu(int64_t rows, int64_t hidden, int64_t ffn, const void* dy, const void* w2, const void* aux,
                          void* dpre, void* db1, void* stream);
 
+/* Kernels launched so far through the driving-model and copy entry points above
+ * (the engine's own launches are in fcdp_engine_kernel_stats); reset != 0 zeroes it. */
+uint64_t fcdp_model_kernel_launches(int32_t reset);
+
 /* Let kernels launched on `device` dereference `peer`'s memory over NVLink
  * (single-process multi-GPU use of the stateless kernels; the engine itself
  * maps peers through CUDA IPC). */
