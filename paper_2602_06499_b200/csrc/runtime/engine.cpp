@@ -262,8 +262,6 @@ Engine::~Engine() {
   }
   if (iter_done_) cudaEventDestroy(iter_done_);
   if (alias_fence_) cudaEventDestroy(alias_fence_);
-  for (cudaEvent_t e : {fwd_t0_, fwd_t1_})
-    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : join_)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : rs_kernel_done_)
@@ -448,11 +446,7 @@ void Engine::allocate() {
   {
     const char* e = std::getenv("FCDP_DEFER_D2H");
     defer_d2h_ = !(e && std::strcmp(e, "0") == 0);
-    const char* g = std::getenv("FCDP_STORE_EAGER");
-    store_eager_ = !(g && std::strcmp(g, "0") == 0);
   }
-  CK(cudaEventCreate(&fwd_t0_));
-  CK(cudaEventCreate(&fwd_t1_));
 }
 
 void Engine::exchange_handles() {
@@ -1061,15 +1055,7 @@ void Engine::ev_d2h(const Event& e) {
   // reloads - behind every other (about 50 ms of PCIe for GPT-2 1.3B).  So the
   // stores are queued and issued in reverse at the forward->backward turn (or
   // as soon as anything depends on one): same bytes, same deps, LIFO order.
-  // The first stores, as many as the forward itself can carry (its time in the
-  // previous iteration x 40 GB/s x 0.8), go out at once in forward order instead,
-  // so the turn has fewer stores left to interleave with the reloads.
   const bool alias_src = (!wt || slot_t == kAliasX) && (!wf || slot_f == kAliasX);
-  if (defer_d2h_ && G_ == 1 && alias_src && store_eager_ && eager_used_ + bytes <= eager_budget_) {
-    eager_used_ += bytes;  // the forward can carry this store: out now, in forward order
-    store_d2h(e.layer, wt, wf, slot_t, slot_f);
-    return;
-  }
   if (defer_d2h_ && G_ == 1 && alias_src) {
     deferred_d2h_.push_back({e.id, e.layer, wt, wf});
     d2h_deferred_id_[e.id] = 1;
@@ -1476,22 +1462,9 @@ void Engine::begin(const shardsim::EventProgram& prog) {
   }
   stream_of_.assign(n_ev, nullptr);
   last_fwd_ = 0;
-  first_fwd_ = ~0u;
-  // eager-store budget from the previous iteration's forward (G = 1 host cache)
-  eager_used_ = 0;
-  eager_budget_ = 0.0;
-  if (fwd_timed_ && cudaEventQuery(fwd_t1_) == cudaSuccess) {
-    float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, fwd_t0_, fwd_t1_) == cudaSuccess)
-      eager_budget_ = 0.8 * static_cast<double>(ms) * 1e-3 * 40e9;  // 40 GB/s: below the measured 55 one-way
-  }
-  cudaGetLastError();
   for (const Event& e : prog.events) {
     stream_of_[e.id] = stream_for(e.kind);
-    if (e.kind == EventKind::ComputeFwd) {
-      last_fwd_ = e.id;
-      first_fwd_ = std::min(first_fwd_, e.id);
-    }
+    if (e.kind == EventKind::ComputeFwd) last_fwd_ = e.id;
   }
   next_event_ = 0;
   for (cudaStream_t s : {s_gather_, s_cache_, s_rs_, s_agsend_, s_rssend_, s_rsrecv_, s_opt_})
@@ -1574,7 +1547,6 @@ void Engine::exec(std::uint32_t event_id) {
     //  reuse on it is guarded by the receivers' consumed markers - so the NIC
     //  keeps streaming the next layers while this one is expanded)
     const bool bwd = e.id > last_fwd;
-    if (e.kind == EventKind::ComputeFwd && e.id == first_fwd_) CK(cudaEventRecord(fwd_t0_, s_comp_));
     if (trace_) CK(cudaEventRecord(trace_begin_[e.id], s));
     try {
     switch (e.kind) {
@@ -1597,10 +1569,6 @@ void Engine::exec(std::uint32_t event_id) {
     const cudaStream_t ds = done_s_ ? done_s_ : s;
     done_s_ = nullptr;
     stream_of[e.id] = ds;
-    if (e.kind == EventKind::ComputeFwd && e.id == last_fwd) {
-      CK(cudaEventRecord(fwd_t1_, s_comp_));
-      fwd_timed_ = true;
-    }
     if (!d2h_deferred_id_[e.id]) {  // a deferred store records these when it is issued
       CK(cudaEventRecord(ev_done_[e.id], ds));
       if (trace_) CK(cudaEventRecord(trace_end_[e.id], ds));

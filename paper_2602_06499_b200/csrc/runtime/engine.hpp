@@ -267,15 +267,6 @@ class Engine {
   std::vector<cudaEvent_t> d2h_done_;       // per layer: its FCDP-Cache store finished (this iteration)
   std::vector<char> d2h_done_valid_;
   bool defer_d2h_ = true;
-  // Eager FCDP-Cache stores at G = 1: the stores the forward can finish on its
-  // own (forward time of the previous iteration x a conservative PCIe rate) go
-  // out in forward order as each layer's forward ends; the rest stay deferred
-  // to the LIFO flush at the turn (FCDP_STORE_EAGER=0 defers all).
-  bool store_eager_ = true;
-  cudaEvent_t fwd_t0_ = nullptr, fwd_t1_ = nullptr;
-  bool fwd_timed_ = false;
-  double eager_budget_ = 0.0;
-  std::uint64_t eager_used_ = 0;
   void store_d2h(int layer, bool wt, bool wf, int slot_t, int slot_f);
   void flush_deferred_d2h();
 
@@ -296,7 +287,7 @@ class Engine {
   std::vector<std::uint32_t> u_of_layer_;
   const shardsim::EventProgram* prog_ = nullptr;
   std::vector<cudaStream_t> stream_of_;  // per event: stream its completion is recorded on
-  std::uint32_t last_fwd_ = 0, next_event_ = 0, first_fwd_ = ~0u;
+  std::uint32_t last_fwd_ = 0, next_event_ = 0;
 
   fcdp_adam_config adam_{1e-4f, 0.9f, 0.95f, 1e-8f, 0.0f, 0};
   fcdp_compute_fn compute_fn_ = nullptr;
