@@ -250,9 +250,10 @@ int fcdp_layernorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, c
                        const float* rstd, void* dx, void* dw, void* db, float* scratch, int32_t splits,
                        void* stream);
 
-/* Driving-model bias gradient (bf16 [rows x cols], cols a multiple of 8):
- * db[c] = sum_r dy[r, c] in fp32, deterministic two-stage reduction through
- * `scratch` (splits * cols floats; splits from fcdp_colsum_splits). */
+/* Driving-model bias gradient (bf16 [rows x cols], cols a multiple of 8 and
+ * <= 16384): db[c] = sum_r dy[r, c] in fp32; row-split partials in `scratch`
+ * (splits * cols floats; splits from fcdp_colsum_splits), summed in split order
+ * by the last block of each column group (deterministic, one launch). */
 int fcdp_colsum_splits(int64_t rows, int32_t cols);
 int fcdp_bias_grad(int64_t rows, int32_t cols, const void* dy, void* db, float* scratch, int32_t splits,
                    void* stream);

@@ -166,7 +166,7 @@ int fcdp_layernorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, c
     check_cuda(fcdp::launch_layernorm_bwd(rows, h, dy, x, w, mean, rstd, dx, dw, db, scratch, splits,
                                           static_cast<cudaStream_t>(stream)),
                "fcdp_layernorm_bwd");
-    fcdp::g_model_launches += (dw && db) ? 3 : 1;
+    fcdp::g_model_launches += (dw && db) ? 2 : 1;
   });
 }
 
@@ -175,10 +175,10 @@ int fcdp_colsum_splits(int64_t rows, int32_t cols) { return fcdp::colsum_splits(
 int fcdp_bias_grad(int64_t rows, int32_t cols, const void* dy, void* db, float* scratch, int32_t splits,
                    void* stream) {
   return guarded([&] {
-    if (cols % 8) throw shardsim::ConfigError("bias_grad: cols must be a multiple of 8");
+    if (cols % 8 || cols > 16384) throw shardsim::ConfigError("bias_grad: cols must be a multiple of 8 and <= 16384");
     check_cuda(fcdp::launch_colsum(rows, cols, dy, db, scratch, splits, static_cast<cudaStream_t>(stream)),
                "fcdp_bias_grad");
-    fcdp::g_model_launches += 2;
+    fcdp::g_model_launches += 1;
   });
 }
 
@@ -194,11 +194,11 @@ int fcdp_bias_gelu_fwd(int64_t rows, int32_t cols, const void* h, const void* b,
 int fcdp_bias_gelu_bwd(int64_t rows, int32_t cols, const void* dy, const void* h, const void* b, void* dh, void* db,
                        float* scratch, int32_t splits, void* stream) {
   return guarded([&] {
-    if (cols % 8) throw shardsim::ConfigError("bias_gelu: cols must be a multiple of 8");
+    if (cols % 8 || cols > 16384) throw shardsim::ConfigError("bias_gelu: cols must be a multiple of 8 and <= 16384");
     check_cuda(fcdp::launch_bias_gelu_bwd(rows, cols, dy, h, b, dh, db, scratch, splits,
                                           static_cast<cudaStream_t>(stream)),
                "fcdp_bias_gelu_bwd");
-    fcdp::g_model_launches += 2;
+    fcdp::g_model_launches += 1;
   });
 }
 

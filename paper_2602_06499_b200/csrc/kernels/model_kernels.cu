@@ -18,6 +18,8 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdint>
 
@@ -139,6 +141,24 @@ __global__ void __launch_bounds__(kWarps * 32) ln_bwd_dx_kernel(std::int64_t row
   }
 }
 
+// Split-sum epilogue shared by the column reductions: every (column group,
+// row split) block writes its partial row, and the LAST block of a column group
+// to finish (an arrival counter per group, threadfence-published partials)
+// sums that group's partials over the splits in split order and writes the
+// result.  The sum order is fixed whatever order the blocks ran in, so the
+// result is deterministic, and no second launch is needed.  The counters come
+// from a small per-device pool (one slot range per launch) and are reset to 0
+// by the block that consumes them.
+__device__ __forceinline__ bool last_split_block(unsigned int* counter) {
+  __shared__ bool last;
+  __threadfence();  // this block's partials are visible before it arrives
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter + blockIdx.x, 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (last) __threadfence();  // and the others' before it reads them
+  return last;
+}
+
 // dgamma / dbeta partials: block (column group of 256 columns, row split r);
 // each thread owns 8 columns (one 16-byte vector), a warp covers the block's
 // 256 columns of one row (512 contiguous bytes), and the block's 8 warps walk
@@ -148,7 +168,8 @@ constexpr int kRowLanes = 8;     // rows processed concurrently per block
 __global__ void __launch_bounds__(kColThreads * kRowLanes) ln_bwd_dw_partial_kernel(
     std::int64_t rows, int h, int splits, const uint4* __restrict__ dy, const uint4* __restrict__ x,
     const float* __restrict__ mean_in, const float* __restrict__ rstd_in, float* __restrict__ part_w,
-    float* __restrict__ part_b) {
+    float* __restrict__ part_b, unsigned int* __restrict__ counter, __nv_bfloat16* __restrict__ dw,
+    __nv_bfloat16* __restrict__ db) {
   __shared__ float red_w[kRowLanes][kColThreads * 8 + 1];
   __shared__ float red_b[kRowLanes][kColThreads * 8 + 1];
   const int cv = blockIdx.x * kColThreads + (threadIdx.x % kColThreads);  // column vector index
@@ -193,22 +214,20 @@ __global__ void __launch_bounds__(kColThreads * kRowLanes) ln_bwd_dw_partial_ker
       part_b[static_cast<std::int64_t>(split) * h + gcol] = sb;
     }
   }
-}
-
-__global__ void ln_bwd_dw_final_kernel(int h, int splits, const float* __restrict__ part_w,
-                                       const float* __restrict__ part_b, __nv_bfloat16* __restrict__ dw,
-                                       __nv_bfloat16* __restrict__ db) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= h) return;
-  float sw = 0.f, sb = 0.f;
-  for (int s = 0; s < splits; ++s) {  // fixed order: deterministic
-    sw += part_w[static_cast<std::int64_t>(s) * h + col];
-    sb += part_b[static_cast<std::int64_t>(s) * h + col];
+  if (!last_split_block(counter)) return;
+  for (int col = threadIdx.x; col < kColThreads * 8; col += blockDim.x) {
+    const int gcol = blockIdx.x * kColThreads * 8 + col;
+    if (gcol >= h) continue;
+    float sw = 0.f, sb = 0.f;
+    for (int k = 0; k < splits; ++k) {  // fixed order: deterministic
+      sw += __ldcg(part_w + static_cast<std::int64_t>(k) * h + gcol);
+      sb += __ldcg(part_b + static_cast<std::int64_t>(k) * h + gcol);
+    }
+    dw[gcol] = __float2bfloat16_rn(sw);
+    db[gcol] = __float2bfloat16_rn(sb);
   }
-  dw[col] = __float2bfloat16_rn(sw);
-  db[col] = __float2bfloat16_rn(sb);
+  if (threadIdx.x == 0) counter[blockIdx.x] = 0;
 }
-
 
 // ------------------------------------------------- column sums (bias grads)
 // out[c] = sum_r dy[r, c] for a bf16 [rows x cols] matrix (the bias gradient
@@ -247,7 +266,8 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
 template <bool kGelu>
 __global__ void __launch_bounds__(kColThreads * kRowLanes) colsum_partial_kernel(
     std::int64_t rows, int cols, int splits, const uint4* __restrict__ dy, const uint4* __restrict__ h,
-    const uint4* __restrict__ bias, uint4* __restrict__ dh, float* __restrict__ part) {
+    const uint4* __restrict__ bias, uint4* __restrict__ dh, float* __restrict__ part,
+    unsigned int* __restrict__ counter, __nv_bfloat16* __restrict__ out) {
   __shared__ float red[kRowLanes][kColThreads * 8 + 1];
   const int cv = blockIdx.x * kColThreads + (threadIdx.x % kColThreads);
   const int rl = threadIdx.x / kColThreads;
@@ -314,15 +334,15 @@ __global__ void __launch_bounds__(kColThreads * kRowLanes) colsum_partial_kernel
     const int gcol = blockIdx.x * kColThreads * 8 + col;
     if (gcol < cols) part[static_cast<std::int64_t>(blockIdx.y) * cols + gcol] = sacc;
   }
-}
-
-__global__ void colsum_final_kernel(int cols, int splits, const float* __restrict__ part,
-                                    __nv_bfloat16* __restrict__ out) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= cols) return;
-  float s = 0.f;
-  for (int k = 0; k < splits; ++k) s += part[static_cast<std::int64_t>(k) * cols + col];  // fixed order
-  out[col] = __float2bfloat16_rn(s);
+  if (!last_split_block(counter)) return;
+  for (int col = threadIdx.x; col < kColThreads * 8; col += blockDim.x) {
+    const int gcol = blockIdx.x * kColThreads * 8 + col;
+    if (gcol >= cols) continue;
+    float sacc = 0.f;
+    for (int k = 0; k < splits; ++k) sacc += __ldcg(part + static_cast<std::int64_t>(k) * cols + gcol);  // fixed order
+    out[gcol] = __float2bfloat16_rn(sacc);
+  }
+  if (threadIdx.x == 0) counter[blockIdx.x] = 0;
 }
 
 // y = gelu(h + b): the MLP's first linear runs without its bias epilogue and the
@@ -539,6 +559,31 @@ __global__ void __launch_bounds__(256) swiglu_bwd_kernel(std::int64_t rows, int 
 
 }  // namespace
 
+
+namespace {
+// Arrival counters of the split-sum epilogue: a zeroed per-device pool, a
+// fresh slot range per launch (consumers reset their slots to 0).
+constexpr unsigned kCounterPool = 1u << 16;
+constexpr unsigned kCounterSlots = 64;  // column groups per launch (cols <= 64 * 256)
+unsigned int* counter_slots() {
+  static unsigned int* pool[64] = {};
+  static std::atomic<unsigned> cursor{0};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!pool[dev]) {
+    unsigned int* p = nullptr;
+    if (cudaMalloc(&p, kCounterPool * sizeof(unsigned)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, kCounterPool * sizeof(unsigned)) != cudaSuccess) return nullptr;  // before any stream uses it
+    pool[dev] = p;
+  }
+  const unsigned slot = (cursor.fetch_add(kCounterSlots) % kCounterPool);
+  return pool[dev] + slot;
+}
+}  // namespace
+
 // the row lives in registers: 8 x h/256 floats per lane (h <= 2048)
 bool layernorm_supported(int h) { return h % 256 == 0 && h / 256 >= 1 && h / 256 <= 8; }
 
@@ -582,12 +627,11 @@ cudaError_t launch_layernorm_bwd(std::int64_t rows, int h, const void* dy, const
   if (e != cudaSuccess) return e;
   if (dw && db) {
     const dim3 g2((h / 8 + kColThreads - 1) / kColThreads, splits);
-    ln_bwd_dw_partial_kernel<<<g2, kColThreads * kRowLanes, 0, s>>>(rows, h, splits, DY, X, mean, rstd, part,
-                                                                     part + static_cast<std::int64_t>(splits) * h);
-    ln_bwd_dw_final_kernel<<<(h + 255) / 256, 256, 0, s>>>(h, splits, part,
-                                                           part + static_cast<std::int64_t>(splits) * h,
-                                                           static_cast<__nv_bfloat16*>(dw),
-                                                           static_cast<__nv_bfloat16*>(db));
+    unsigned int* ctr = counter_slots();
+    if (!ctr || g2.x > kCounterSlots) return cudaErrorInvalidValue;
+    ln_bwd_dw_partial_kernel<<<g2, kColThreads * kRowLanes, 0, s>>>(
+        rows, h, splits, DY, X, mean, rstd, part, part + static_cast<std::int64_t>(splits) * h, ctr,
+        static_cast<__nv_bfloat16*>(dw), static_cast<__nv_bfloat16*>(db));
   }
   return cudaGetLastError();
 }
@@ -605,10 +649,11 @@ cudaError_t launch_colsum(std::int64_t rows, int cols, const void* dy, void* out
                           cudaStream_t s) {
   if (cols % 8 || splits < 1 || rows < 1) return cudaErrorInvalidValue;
   const dim3 g((cols / 8 + kColThreads - 1) / kColThreads, splits);
-  colsum_partial_kernel<false><<<g, kColThreads * kRowLanes, 0, s>>>(rows, cols, splits,
-                                                                     static_cast<const uint4*>(dy), nullptr,
-                                                                     nullptr, nullptr, part);
-  colsum_final_kernel<<<(cols + 255) / 256, 256, 0, s>>>(cols, splits, part, static_cast<__nv_bfloat16*>(out));
+  unsigned int* ctr = counter_slots();
+  if (!ctr || g.x > kCounterSlots) return cudaErrorInvalidValue;
+  colsum_partial_kernel<false><<<g, kColThreads * kRowLanes, 0, s>>>(
+      rows, cols, splits, static_cast<const uint4*>(dy), nullptr, nullptr, nullptr, part, ctr,
+      static_cast<__nv_bfloat16*>(out));
   return cudaGetLastError();
 }
 
@@ -631,10 +676,11 @@ cudaError_t launch_bias_gelu_bwd(std::int64_t rows, int cols, const void* dy, co
                                  void* db, float* part, int splits, cudaStream_t s) {
   if (cols % 8 || splits < 1 || rows < 1) return cudaErrorInvalidValue;
   const dim3 g((cols / 8 + kColThreads - 1) / kColThreads, splits);
+  unsigned int* ctr = counter_slots();
+  if (!ctr || g.x > kCounterSlots) return cudaErrorInvalidValue;
   colsum_partial_kernel<true><<<g, kColThreads * kRowLanes, 0, s>>>(
       rows, cols, splits, static_cast<const uint4*>(dy), static_cast<const uint4*>(h),
-      static_cast<const uint4*>(b), static_cast<uint4*>(dh), part);
-  colsum_final_kernel<<<(cols + 255) / 256, 256, 0, s>>>(cols, splits, part, static_cast<__nv_bfloat16*>(db));
+      static_cast<const uint4*>(b), static_cast<uint4*>(dh), part, ctr, static_cast<__nv_bfloat16*>(db));
   return cudaGetLastError();
 }
 

@@ -52,6 +52,7 @@ def test_model_kernel_argument_errors(built):
     lib = _capi.lib()
     P = ctypes.c_void_p
     assert lib.fcdp_bias_grad(8, 12, None, None, None, 1, None) == -1  # cols % 8
+    assert lib.fcdp_bias_grad(8, 16392, None, None, None, 1, None) == -1  # > 64 column groups
     assert lib.fcdp_bias_gelu_fwd(8, 10, None, None, None, None) == -1
     assert lib.fcdp_bias_gelu_bwd(8, 10, None, None, None, None, None, None, 1, None) == -1
     assert lib.fcdp_xent_fwd(8, 50257, None, None, None, None, None) == -1  # vocab % 8
