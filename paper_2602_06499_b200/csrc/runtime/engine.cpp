@@ -222,6 +222,8 @@ Engine::Engine(const fcdp_engine_config& cfg, const shardsim::ModelSpec& model,
     opt_ctas_per_sm_ = k ? std::atoi(k) : (opt_on_compute_ ? 0 : 1);
     const char* r = std::getenv("FCDP_RS_CTAS_PER_SM");
     rs_ctas_per_sm_ = r ? std::atoi(r) : 0;
+    const char* rsx = std::getenv("FCDP_RS_STREAM");
+    rs_on_compute_ = rsx && std::strcmp(rsx, "compute") == 0;
   }
   for (auto& e : fin_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : rs_kernel_done_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -571,7 +573,7 @@ cudaStream_t Engine::stream_for(EventKind k) const {
     case EventKind::D2H:
       return s_cache_;
     case EventKind::ReduceScatter:
-      return s_rs_;
+      return rs_stream();
     default:
       return s_comp_;
   }
@@ -1131,7 +1133,7 @@ void Engine::ev_reduce_scatter(const Event& e) {
   const std::uint32_t u = u_of_layer_[li];
   const int gs = grad_slot_of_layer_[li];
   if (gs < 0) throw shardsim::ProtocolError("reduce_scatter before compute_bwd of layer " + std::to_string(li));
-  cudaStream_t s = s_rs_;
+  cudaStream_t s = rs_stream();
   const std::size_t C = kChunkBytes;
   write_flag(s, kGradReady, u);
   for (int jj = 0; jj < g_; ++jj)
@@ -1252,7 +1254,7 @@ void Engine::mics_grad_sync(LayerRt& l, int gs, float scale, float* final_out) {
   // so it has its own counter.
   const std::size_t C = kChunkBytes;
   const std::size_t stride = static_cast<std::size_t>(l.L.dev.shard_t) * C;
-  CK(cudaEventRecord(rs_kernel_done_[gs], s_rs_));
+  CK(cudaEventRecord(rs_kernel_done_[gs], rs_stream()));
   CK(cudaStreamWaitEvent(s_rssend_, rs_kernel_done_[gs], 0));
   cudaStream_t s = s_rsrecv_;
   CK(cudaStreamWaitEvent(s, rs_kernel_done_[gs], 0));

@@ -220,6 +220,9 @@ class Engine {
   cudaStream_t s_opt_ = nullptr;   // G = 1 fused RS + AdamW when FCDP_OPT_PRIO=low (else compute stream)
   cudaEvent_t opt_fork_ = nullptr;
   bool opt_low_ = false;
+  // FCDP_RS_STREAM=compute: the reduce-scatter (G > 1) serialised on the compute stream
+  bool rs_on_compute_ = false;
+  cudaStream_t rs_stream() const { return rs_on_compute_ ? s_comp_ : s_rs_; }
   int rs_ctas_per_sm_ = 0;       // FCDP_RS_CTAS_PER_SM: grid cap of the RS kernel (0 = full grid)
   int opt_ctas_per_sm_ = 0;      // grid cap of the G = 1 fused update, CTAs per SM (0 = full grid)
   bool opt_on_compute_ = true;  // the G = 1 fused update on the compute stream (FCDP_OPT_STREAM=rs: beside the GEMMs)
