@@ -250,6 +250,14 @@ int fcdp_layernorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, c
                        const float* rstd, void* dx, void* dw, void* db, float* scratch, int32_t splits,
                        void* stream);
 
+/* Residual add fused into the LayerNorm: s = x + r (bf16, written to s_out) and
+ * y = LN(s) in one pass; backward with the residual's downstream gradient dres
+ * added into dx (nullable: plain LayerNorm backward). */
+int fcdp_add_layernorm_fwd(int64_t rows, int32_t h, float eps, const void* x, const void* r, const void* w,
+                           const void* b, void* s_out, void* y, float* mean, float* rstd, void* stream);
+int fcdp_layernorm_bwd_res(int64_t rows, int32_t h, const void* dy, const void* x, const void* w, const float* mean,
+                           const float* rstd, const void* dres, void* dx, void* dw, void* db, float* scratch,
+                           int32_t splits, void* stream);
 /* Driving-model bias gradient (bf16 [rows x cols], cols a multiple of 8 and
  * <= 16384): db[c] = sum_r dy[r, c] in fp32; row-split partials in `scratch`
  * (splits * cols floats; splits from fcdp_colsum_splits), summed in split order

@@ -170,6 +170,30 @@ int fcdp_layernorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, c
   });
 }
 
+int fcdp_add_layernorm_fwd(int64_t rows, int32_t h, float eps, const void* x, const void* r, const void* w,
+                           const void* b, void* s_out, void* y, float* mean, float* rstd, void* stream) {
+  return guarded([&] {
+    if (!fcdp::layernorm_supported(h)) throw shardsim::ConfigError("layernorm: h must be a multiple of 256, <= 2048");
+    if (!r || !s_out) throw shardsim::ConfigError("add_layernorm: r and s_out are required");
+    check_cuda(fcdp::launch_layernorm_fwd(rows, h, eps, x, w, b, y, mean, rstd, static_cast<cudaStream_t>(stream), r,
+                                          s_out),
+               "fcdp_add_layernorm_fwd");
+    fcdp::g_model_launches += 1;
+  });
+}
+
+int fcdp_layernorm_bwd_res(int64_t rows, int32_t h, const void* dy, const void* x, const void* w, const float* mean,
+                           const float* rstd, const void* dres, void* dx, void* dw, void* db, float* scratch,
+                           int32_t splits, void* stream) {
+  return guarded([&] {
+    if (!fcdp::layernorm_supported(h)) throw shardsim::ConfigError("layernorm: h must be a multiple of 256, <= 2048");
+    check_cuda(fcdp::launch_layernorm_bwd(rows, h, dy, x, w, mean, rstd, dx, dw, db, scratch, splits,
+                                          static_cast<cudaStream_t>(stream), dres),
+               "fcdp_layernorm_bwd_res");
+    fcdp::g_model_launches += (dw && db) ? 2 : 1;
+  });
+}
+
 int fcdp_colsum_splits(int64_t rows, int32_t cols) { return fcdp::colsum_splits(rows, cols); }
 
 int fcdp_bias_grad(int64_t rows, int32_t cols, const void* dy, void* db, float* scratch, int32_t splits,

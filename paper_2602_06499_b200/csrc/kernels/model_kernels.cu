@@ -55,12 +55,16 @@ __device__ __forceinline__ uint4 pack8(const float* f) {
   return q;
 }
 
-// kV = 16-byte vectors per lane (h = 256 * kV)
-template <int kV>
+// kV = 16-byte vectors per lane (h = 256 * kV).  kRes: the input is the
+// residual sum s = x + r (rounded to bf16 as the unfused add would, and
+// written out for the residual stream), normalised in the same pass.
+template <int kV, bool kRes = false>
 __global__ void __launch_bounds__(kWarps * 32) ln_fwd_kernel(std::int64_t rows, int h, float eps,
                                                              const uint4* __restrict__ x, const uint4* __restrict__ w,
                                                              const uint4* __restrict__ b, uint4* __restrict__ y,
-                                                             float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+                                                             float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                             const uint4* __restrict__ r = nullptr,
+                                                             uint4* __restrict__ s_out = nullptr) {
   const int lane = threadIdx.x & 31;
   const std::int64_t row = static_cast<std::int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -68,6 +72,18 @@ __global__ void __launch_bounds__(kWarps * 32) ln_fwd_kernel(std::int64_t rows, 
   float v[kV][8];
 #pragma unroll
   for (int k = 0; k < kV; ++k) unpack8(__ldcs(x + base + k * 32 + lane), v[k]);
+  if constexpr (kRes) {
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+      float rf[8];
+      unpack8(__ldcs(r + base + k * 32 + lane), rf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[k][e] += rf[e];
+      const uint4 q = pack8(v[k]);
+      __stcs(s_out + base + k * 32 + lane, q);
+      unpack8(q, v[k]);  // normalise the stored (bf16) sum
+    }
+  }
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < kV; ++k)
@@ -98,13 +114,15 @@ __global__ void __launch_bounds__(kWarps * 32) ln_fwd_kernel(std::int64_t rows, 
   }
 }
 
-template <int kV>
+// kRes: dx += dres (the gradient reaching the residual sum from downstream)
+template <int kV, bool kRes = false>
 __global__ void __launch_bounds__(kWarps * 32) ln_bwd_dx_kernel(std::int64_t rows, int h, const uint4* __restrict__ dy,
                                                                 const uint4* __restrict__ x,
                                                                 const uint4* __restrict__ w,
                                                                 const float* __restrict__ mean_in,
                                                                 const float* __restrict__ rstd_in,
-                                                                uint4* __restrict__ dx) {
+                                                                uint4* __restrict__ dx,
+                                                                const uint4* __restrict__ dres = nullptr) {
   const int lane = threadIdx.x & 31;
   const std::int64_t row = static_cast<std::int64_t>(blockIdx.x) * kWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -137,6 +155,12 @@ __global__ void __launch_bounds__(kWarps * 32) ln_bwd_dx_kernel(std::int64_t row
     float o[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) o[e] = rstd * (g[k][e] - c2 - xh[k][e] * c1);
+    if constexpr (kRes) {
+      float rf[8];
+      unpack8(__ldcs(dres + base + k * 32 + lane), rf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] += rf[e];
+    }
     __stcs(dx + base + k * 32 + lane, pack8(o));
   }
 }
@@ -588,16 +612,23 @@ unsigned int* counter_slots() {
 bool layernorm_supported(int h) { return h % 256 == 0 && h / 256 >= 1 && h / 256 <= 8; }
 
 cudaError_t launch_layernorm_fwd(std::int64_t rows, int h, float eps, const void* x, const void* w, const void* b,
-                                 void* y, float* mean, float* rstd, cudaStream_t s) {
-  if (!layernorm_supported(h)) return cudaErrorInvalidValue;
+                                 void* y, float* mean, float* rstd, cudaStream_t s, const void* r, void* s_out) {
+  if (!layernorm_supported(h) || (r == nullptr) != (s_out == nullptr)) return cudaErrorInvalidValue;
   const int grid = static_cast<int>((rows + kWarps - 1) / kWarps);
   auto X = static_cast<const uint4*>(x);
   auto W = static_cast<const uint4*>(w);
   auto B = static_cast<const uint4*>(b);
   auto Y = static_cast<uint4*>(y);
+  auto R = static_cast<const uint4*>(r);
+  auto SO = static_cast<uint4*>(s_out);
   switch (h / 256) {
-#define FCDP_LN_FWD(V) \
-  case V: ln_fwd_kernel<V><<<grid, kWarps * 32, 0, s>>>(rows, h, eps, X, W, B, Y, mean, rstd); break;
+#define FCDP_LN_FWD(V)                                                                                     \
+  case V:                                                                                                  \
+    if (r)                                                                                                 \
+      ln_fwd_kernel<V, true><<<grid, kWarps * 32, 0, s>>>(rows, h, eps, X, W, B, Y, mean, rstd, R, SO);     \
+    else                                                                                                   \
+      ln_fwd_kernel<V><<<grid, kWarps * 32, 0, s>>>(rows, h, eps, X, W, B, Y, mean, rstd);                  \
+    break;
     FCDP_LN_FWD(1) FCDP_LN_FWD(2) FCDP_LN_FWD(3) FCDP_LN_FWD(4) FCDP_LN_FWD(5) FCDP_LN_FWD(6) FCDP_LN_FWD(7)
     FCDP_LN_FWD(8)
 #undef FCDP_LN_FWD
@@ -608,7 +639,7 @@ cudaError_t launch_layernorm_fwd(std::int64_t rows, int h, float eps, const void
 
 cudaError_t launch_layernorm_bwd(std::int64_t rows, int h, const void* dy, const void* x, const void* w,
                                  const float* mean, const float* rstd, void* dx, void* dw, void* db, float* part,
-                                 int splits, cudaStream_t s) {
+                                 int splits, cudaStream_t s, const void* dres) {
   if (!layernorm_supported(h) || splits < 1) return cudaErrorInvalidValue;
   const int grid = static_cast<int>((rows + kWarps - 1) / kWarps);
   auto DY = static_cast<const uint4*>(dy);
@@ -616,8 +647,14 @@ cudaError_t launch_layernorm_bwd(std::int64_t rows, int h, const void* dy, const
   auto W = static_cast<const uint4*>(w);
   auto DX = static_cast<uint4*>(dx);
   switch (h / 256) {
-#define FCDP_LN_BWD(V) \
-  case V: ln_bwd_dx_kernel<V><<<grid, kWarps * 32, 0, s>>>(rows, h, DY, X, W, mean, rstd, DX); break;
+#define FCDP_LN_BWD(V)                                                                                   \
+  case V:                                                                                                \
+    if (dres)                                                                                            \
+      ln_bwd_dx_kernel<V, true><<<grid, kWarps * 32, 0, s>>>(rows, h, DY, X, W, mean, rstd, DX,           \
+                                                             static_cast<const uint4*>(dres));            \
+    else                                                                                                 \
+      ln_bwd_dx_kernel<V><<<grid, kWarps * 32, 0, s>>>(rows, h, DY, X, W, mean, rstd, DX);                \
+    break;
     FCDP_LN_BWD(1) FCDP_LN_BWD(2) FCDP_LN_BWD(3) FCDP_LN_BWD(4) FCDP_LN_BWD(5) FCDP_LN_BWD(6) FCDP_LN_BWD(7)
     FCDP_LN_BWD(8)
 #undef FCDP_LN_BWD

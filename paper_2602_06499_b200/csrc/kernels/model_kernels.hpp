@@ -10,12 +10,15 @@
 namespace fcdp {
 
 bool layernorm_supported(int h);
+// r / s_out (both or neither): normalise the residual sum s = x + r (bf16), written to s_out
 cudaError_t launch_layernorm_fwd(std::int64_t rows, int h, float eps, const void* x, const void* w, const void* b,
-                                 void* y, float* mean, float* rstd, cudaStream_t s);
+                                 void* y, float* mean, float* rstd, cudaStream_t s, const void* r = nullptr,
+                                 void* s_out = nullptr);
 // part: 2 * splits * h floats of scratch (column partials of dgamma, dbeta)
+// dres (nullable): gradient reaching the residual sum from downstream, added to dx
 cudaError_t launch_layernorm_bwd(std::int64_t rows, int h, const void* dy, const void* x, const void* w,
                                  const float* mean, const float* rstd, void* dx, void* dw, void* db, float* part,
-                                 int splits, cudaStream_t s);
+                                 int splits, cudaStream_t s, const void* dres = nullptr);
 
 // bias gradient: out[c] = sum_r dy[r, c] (cols a multiple of 8); part: splits * cols floats
 int colsum_splits(std::int64_t rows, int cols);

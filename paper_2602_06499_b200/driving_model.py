@@ -194,6 +194,68 @@ def _layer_norm(x, w, b, eps=1e-5):
     return _LN.apply(x, w, b, eps)
 
 
+_ALN = None
+
+
+def _add_layer_norm(x, r, w, b, eps=1e-5):
+    """(s, LN(s)) with s = x + r: the residual add fused into libfcdp's LayerNorm
+    (forward) and the residual's gradient folded into its dx (backward)."""
+    global _ALN
+    import torch
+    import torch.nn.functional as F
+    h = x.shape[-1]
+    if not (x.is_cuda and x.dtype == torch.bfloat16 and r.dtype == torch.bfloat16 and h % 256 == 0 and h <= 2048):
+        s = x + r
+        return s, F.layer_norm(s, (h,), w, b, eps)
+    if _ALN is None:
+        _ALN = _make_add_layernorm()
+    return _ALN.apply(x, r, w, b, eps)
+
+
+def _make_add_layernorm():
+    import ctypes as C
+    import torch
+    from ._capi import check, lib
+
+    P = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+
+    class AddLayerNormFn(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, x, r, w, b, eps):
+            xc, rc = x.contiguous(), r.contiguous()
+            h = xc.shape[-1]
+            rows = xc.numel() // h
+            s_ = torch.empty_like(xc)
+            y = torch.empty_like(xc)
+            mean = torch.empty(rows, dtype=torch.float32, device=x.device)
+            rstd = torch.empty_like(mean)
+            st = C.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+            check(lib().fcdp_add_layernorm_fwd(rows, h, eps, P(xc), P(rc), P(w), P(b), P(s_), P(y), P(mean), P(rstd),
+                                               st))
+            ctx.save_for_backward(s_, w, mean, rstd)
+            return s_, y
+
+        @staticmethod
+        def backward(ctx, ds, dy):
+            s_, w, mean, rstd = ctx.saved_tensors
+            h = s_.shape[-1]
+            rows = s_.numel() // h
+            dyc = dy.contiguous() if dy is not None else torch.zeros_like(s_)
+            dsc = ds.contiguous() if ds is not None else None
+            dx = torch.empty_like(s_)
+            want_w = ctx.needs_input_grad[2] or ctx.needs_input_grad[3]
+            dw = torch.empty(h, dtype=w.dtype, device=w.device) if want_w else None
+            db = torch.empty(h, dtype=w.dtype, device=w.device) if want_w else None
+            splits = 64
+            scratch = torch.empty(2 * splits * h, dtype=torch.float32, device=s_.device) if want_w else None
+            st = C.c_void_p(torch.cuda.current_stream(s_.device).cuda_stream)
+            check(lib().fcdp_layernorm_bwd_res(rows, h, P(dyc), P(s_), P(w), P(mean), P(rstd), P(dsc), P(dx), P(dw),
+                                               P(db), P(scratch), splits, st))
+            return dx, dx, dw, db, None
+
+    return AddLayerNormFn
+
+
 def _make_layernorm():
     import ctypes as C
     import torch
@@ -655,8 +717,8 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         # strided copy (tools/attn_layout_probe.py: 0.85 vs 1.29 ms per block fwd+bwd)
         q, k, v = _linear_bias(a, p["qkv_w"], p["qkv_b"]).view(b, s, 3, nh, h // nh).unbind(2)
         o = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), is_causal=True)
-        x = x + _linear_bias(o.transpose(1, 2).reshape(b, s, h), p["proj_w"], p["proj_b"])
-        m = _layer_norm(x, p["ln2_w"], p["ln2_b"])
+        x, m = _add_layer_norm(x, _linear_bias(o.transpose(1, 2).reshape(b, s, h), p["proj_w"], p["proj_b"]),
+                               p["ln2_w"], p["ln2_b"])
         return x + _gpt2_mlp(m, p)
     if ldef.kind == "llama_block":
         b, s, _ = x.shape

@@ -305,3 +305,32 @@ def test_cublaslt_gelu_epilogue_is_tanh_gelu(built):
     match_erf = (act == erf_ref).float().mean().item()
     # measured: 0.935 of the bf16 outputs equal the tanh-GELU rounding, 0.737 the erf one
     assert match_tanh > 0.9 and match_tanh > match_erf + 0.1, (match_tanh, match_erf)
+
+
+@pytest.mark.parametrize("rows,h", [(8192, 2048), (77, 256)])
+def test_add_layernorm_matches_fp32(built, rows, h):
+    """Residual add fused into the LayerNorm (s = x + r, LN(s)) and the residual's
+    gradient folded into its dx, vs fp32 (s feeds a further residual add)."""
+    from paper_2602_06499_b200.driving_model import _add_layer_norm
+    import torch.nn.functional as F
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(rows + h)
+    x, r = ((torch.randn(rows, h, device=dev, generator=g) * 2).to(torch.bfloat16).requires_grad_(True) for _ in range(2))
+    w = (1 + 0.1 * torch.randn(h, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    b = (0.1 * torch.randn(h, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True)
+    ds, dy = (torch.randn(rows, h, device=dev, generator=g).to(torch.bfloat16) for _ in range(2))
+    s_, y = _add_layer_norm(x, r, w, b)
+    torch.autograd.backward((s_, y), (ds, dy))
+    xr, rr, wr, br = (t.detach().float().requires_grad_(True) for t in (x, r, w, b))
+    sr = xr + rr
+    yr = F.layer_norm(sr, (h,), wr, br, 1e-5)
+    torch.autograd.backward((sr, yr), (ds.float(), dy.float()))
+    xt, rt, wt, bt = (t.detach().clone().requires_grad_(True) for t in (x, r, w, b))
+    st_ = xt + rt
+    yt = F.layer_norm(st_, (h,), wt, bt, 1e-5)
+    torch.autograd.backward((st_, yt), (ds, dy))
+    assert torch.equal(s_, st_)  # the same bf16 add
+    for ours, theirs, ref, name in ((y, yt, yr, "y"), (x.grad, xt.grad, xr.grad, "dx"), (r.grad, rt.grad, rr.grad, "dr"),
+                                    (w.grad, wt.grad, wr.grad, "dw"), (b.grad, bt.grad, br.grad, "db")):
+        e_ours, e_torch = _rel(ours, ref), _rel(theirs, ref)
+        assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
