@@ -258,6 +258,15 @@ int fcdp_add_layernorm_fwd(int64_t rows, int32_t h, float eps, const void* x, co
 int fcdp_layernorm_bwd_res(int64_t rows, int32_t h, const void* dy, const void* x, const void* w, const float* mean,
                            const float* rstd, const void* dres, void* dx, void* dw, void* db, float* scratch,
                            int32_t splits, void* stream);
+/* Driving-model Llama RMSNorm (bf16 rows, h a multiple of 1024 and <= 8192, fp32
+ * statistics): y = x * rsqrt(mean(x^2) + eps) * w and per-row rstd; with r and
+ * s_out the input is the residual sum s = x + r (bf16, written to s_out).
+ * Backward: dx (+ dres, nullable) and, if dw != NULL, dgamma through `scratch`
+ * (splits * h floats). */
+int fcdp_rmsnorm_fwd(int64_t rows, int32_t h, float eps, const void* x, const void* r, const void* w, void* s_out,
+                     void* y, float* rstd, void* stream);
+int fcdp_rmsnorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, const void* w, const float* rstd,
+                     const void* dres, void* dx, void* dw, float* scratch, int32_t splits, void* stream);
 /* Driving-model bias gradient (bf16 [rows x cols], cols a multiple of 8 and
  * <= 16384): db[c] = sum_r dy[r, c] in fp32; row-split partials in `scratch`
  * (splits * cols floats; splits from fcdp_colsum_splits), summed in split order

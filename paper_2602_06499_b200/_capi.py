@@ -169,6 +169,8 @@ SIGNATURES = {
     "fcdp_model_kernel_launches": (C.c_uint64, [i32]),
     "fcdp_add_layernorm_fwd": (C.c_int, [i64, i32, C.c_float, P, P, P, P, P, P, P, P, P]),
     "fcdp_layernorm_bwd_res": (C.c_int, [i64, i32, P, P, P, P, P, P, P, P, P, P, i32, P]),
+    "fcdp_rmsnorm_fwd": (C.c_int, [i64, i32, C.c_float, P, P, P, P, P, P, P]),
+    "fcdp_rmsnorm_bwd": (C.c_int, [i64, i32, P, P, P, P, P, P, P, P, i32, P]),
     "fcdp_numa_parse_cpulist": (C.c_int, [C.c_char_p, C.POINTER(i32), i32, C.POINTER(i32)]),
     "fcdp_numa_selftest": (C.c_int, [i32, C.c_uint64, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32),
                                      C.POINTER(i32), C.POINTER(i32)]),

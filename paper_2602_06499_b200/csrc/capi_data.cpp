@@ -194,6 +194,28 @@ int fcdp_layernorm_bwd_res(int64_t rows, int32_t h, const void* dy, const void* 
   });
 }
 
+int fcdp_rmsnorm_fwd(int64_t rows, int32_t h, float eps, const void* x, const void* r, const void* w, void* s_out,
+                     void* y, float* rstd, void* stream) {
+  return guarded([&] {
+    if (!fcdp::rmsnorm_supported(h)) throw shardsim::ConfigError("rmsnorm: h must be a multiple of 1024, <= 8192");
+    if ((r == nullptr) != (s_out == nullptr)) throw shardsim::ConfigError("rmsnorm: r and s_out go together");
+    check_cuda(fcdp::launch_rmsnorm_fwd(rows, h, eps, x, r, w, s_out, y, rstd, static_cast<cudaStream_t>(stream)),
+               "fcdp_rmsnorm_fwd");
+    fcdp::g_model_launches += 1;
+  });
+}
+
+int fcdp_rmsnorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, const void* w, const float* rstd,
+                     const void* dres, void* dx, void* dw, float* scratch, int32_t splits, void* stream) {
+  return guarded([&] {
+    if (!fcdp::rmsnorm_supported(h)) throw shardsim::ConfigError("rmsnorm: h must be a multiple of 1024, <= 8192");
+    check_cuda(fcdp::launch_rmsnorm_bwd(rows, h, dy, x, w, rstd, dres, dx, dw, scratch, splits,
+                                        static_cast<cudaStream_t>(stream)),
+               "fcdp_rmsnorm_bwd");
+    fcdp::g_model_launches += dw ? 2 : 1;
+  });
+}
+
 int fcdp_colsum_splits(int64_t rows, int32_t cols) { return fcdp::colsum_splits(rows, cols); }
 
 int fcdp_bias_grad(int64_t rows, int32_t cols, const void* dy, void* db, float* scratch, int32_t splits,

@@ -369,6 +369,50 @@ __global__ void __launch_bounds__(kColThreads * kRowLanes) colsum_partial_kernel
   if (threadIdx.x == 0) counter[blockIdx.x] = 0;
 }
 
+// RMSNorm dgamma = sum_r dy * x * rstd: column partials + last-block split sum.
+__global__ void __launch_bounds__(kColThreads * kRowLanes) rms_bwd_dw_partial_kernel(
+    std::int64_t rows, int h, int splits, const uint4* __restrict__ dy, const uint4* __restrict__ x,
+    const float* __restrict__ rstd_in, float* __restrict__ part_w, unsigned int* __restrict__ counter,
+    __nv_bfloat16* __restrict__ dw) {
+  __shared__ float red_w[kRowLanes][kColThreads * 8 + 1];
+  const int cv = blockIdx.x * kColThreads + (threadIdx.x % kColThreads);
+  const int rl = threadIdx.x / kColThreads;
+  const std::int64_t per = (rows + splits - 1) / splits;
+  const std::int64_t r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+  float aw[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) aw[e] = 0.f;
+  if (cv < h / 8)
+    for (std::int64_t r = r0 + rl; r < r1; r += kRowLanes) {
+      float xf[8], df[8];
+      unpack8(__ldg(x + r * (h / 8) + cv), xf);
+      unpack8(__ldg(dy + r * (h / 8) + cv), df);
+      const float rstd = __ldg(rstd_in + r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) aw[e] += df[e] * (xf[e] * rstd);
+    }
+  const int c = threadIdx.x % kColThreads;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) red_w[rl][c * 8 + e] = aw[e];
+  __syncthreads();
+  for (int col = threadIdx.x; col < kColThreads * 8; col += blockDim.x) {
+    float sw = 0.f;
+#pragma unroll
+    for (int l = 0; l < kRowLanes; ++l) sw += red_w[l][col];
+    const int gcol = blockIdx.x * kColThreads * 8 + col;
+    if (gcol < h) part_w[static_cast<std::int64_t>(blockIdx.y) * h + gcol] = sw;
+  }
+  if (!last_split_block(counter)) return;
+  for (int col = threadIdx.x; col < kColThreads * 8; col += blockDim.x) {
+    const int gcol = blockIdx.x * kColThreads * 8 + col;
+    if (gcol >= h) continue;
+    float sw = 0.f;
+    for (int k = 0; k < splits; ++k) sw += __ldcg(part_w + static_cast<std::int64_t>(k) * h + gcol);
+    dw[gcol] = __float2bfloat16_rn(sw);
+  }
+  if (threadIdx.x == 0) counter[blockIdx.x] = 0;
+}
+
 // y = gelu(h + b): the MLP's first linear runs without its bias epilogue and the
 // bias add is fused here (one read of h, one write of y).  A thread owns one
 // column vector (its bias loaded once) and walks rows gridDim.y apart, 4 in
@@ -499,6 +543,108 @@ __global__ void __launch_bounds__(kXentThreads) xent_bwd_kernel(int vpr, const u
       a[e] = (p - (static_cast<std::int64_t>(i) * 8 + e == lab ? 1.0f : 0.0f)) * sc;
     }
     __stcs(dr + i, pack8(a));
+  }
+}
+
+// ------------------------------------------------------------- Llama: RMSNorm
+// One block of kRmsThreads threads per row (h = kRmsThreads * 8 * kV, i.e. a
+// multiple of 1024: Llama-7B 4096, 13B 5120), the row in registers, fp32
+// statistics.  kRes: the input is the residual sum s = x + r (bf16, written
+// out) - the Llama block's second norm takes its residual add in the same pass.
+// Backward: dx = rstd * (g - xh * mean(g * xh)) with g = dy * w, xh = x * rstd,
+// (+ dres: the residual's downstream gradient); dw as column partials summed by
+// the last block of each column group (as the LayerNorm's).
+constexpr int kRmsThreads = 128;
+
+__device__ __forceinline__ float block_sum_rms(float v, float* red) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < kRmsThreads / 32; ++i) t += red[i];  // fixed order
+  __syncthreads();
+  return t;
+}
+
+template <int kV, bool kRes>
+__global__ void __launch_bounds__(kRmsThreads) rms_fwd_kernel(int h, float eps, const uint4* __restrict__ x,
+                                                              const uint4* __restrict__ r, const uint4* __restrict__ w,
+                                                              uint4* __restrict__ s_out, uint4* __restrict__ y,
+                                                              float* __restrict__ rstd_out) {
+  __shared__ float red[kRmsThreads / 32];
+  const std::int64_t base = static_cast<std::int64_t>(blockIdx.x) * (h / 8);
+  float v[kV][8];
+#pragma unroll
+  for (int k = 0; k < kV; ++k) unpack8(__ldcs(x + base + k * kRmsThreads + threadIdx.x), v[k]);
+  if constexpr (kRes) {
+#pragma unroll
+    for (int k = 0; k < kV; ++k) {
+      float rf[8];
+      unpack8(__ldcs(r + base + k * kRmsThreads + threadIdx.x), rf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[k][e] += rf[e];
+      const uint4 q = pack8(v[k]);
+      __stcs(s_out + base + k * kRmsThreads + threadIdx.x, q);
+      unpack8(q, v[k]);
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kV; ++k)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ss += v[k][e] * v[k][e];
+  const float rstd = rsqrtf(block_sum_rms(ss, red) / h + eps);
+#pragma unroll
+  for (int k = 0; k < kV; ++k) {
+    float wf[8], o[8];
+    unpack8(__ldg(w + k * kRmsThreads + threadIdx.x), wf);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = v[k][e] * rstd * wf[e];
+    __stcs(y + base + k * kRmsThreads + threadIdx.x, pack8(o));
+  }
+  if (threadIdx.x == 0) rstd_out[blockIdx.x] = rstd;
+}
+
+template <int kV, bool kRes>
+__global__ void __launch_bounds__(kRmsThreads) rms_bwd_dx_kernel(int h, const uint4* __restrict__ dy,
+                                                                 const uint4* __restrict__ x,
+                                                                 const uint4* __restrict__ w,
+                                                                 const float* __restrict__ rstd_in,
+                                                                 const uint4* __restrict__ dres,
+                                                                 uint4* __restrict__ dx) {
+  __shared__ float red[kRmsThreads / 32];
+  const std::int64_t base = static_cast<std::int64_t>(blockIdx.x) * (h / 8);
+  const float rstd = __ldg(rstd_in + blockIdx.x);
+  float xh[kV][8], g[kV][8];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < kV; ++k) {
+    float xf[8], df[8], wf[8];
+    unpack8(__ldg(x + base + k * kRmsThreads + threadIdx.x), xf);
+    unpack8(__ldcs(dy + base + k * kRmsThreads + threadIdx.x), df);
+    unpack8(__ldg(w + k * kRmsThreads + threadIdx.x), wf);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      xh[k][e] = xf[e] * rstd;
+      g[k][e] = df[e] * wf[e];
+      s += g[k][e] * xh[k][e];
+    }
+  }
+  const float c = block_sum_rms(s, red) / h;
+#pragma unroll
+  for (int k = 0; k < kV; ++k) {
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = rstd * (g[k][e] - xh[k][e] * c);
+    if constexpr (kRes) {
+      float rf[8];
+      unpack8(__ldcs(dres + base + k * kRmsThreads + threadIdx.x), rf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] += rf[e];
+    }
+    __stcs(dx + base + k * kRmsThreads + threadIdx.x, pack8(o));
   }
 }
 
@@ -777,6 +923,67 @@ cudaError_t launch_swiglu_bwd(std::int64_t rows, int f, const void* dy, const vo
       rows, f / 8, static_cast<const uint4*>(dy), static_cast<const uint4*>(g), g_stride / 8,
       static_cast<const uint4*>(u), u_stride / 8, static_cast<uint4*>(dg), dg_stride / 8, static_cast<uint4*>(du),
       du_stride / 8);
+  return cudaGetLastError();
+}
+
+bool rmsnorm_supported(int h) { return h % 1024 == 0 && h / 1024 >= 1 && h / 1024 <= 8; }
+
+cudaError_t launch_rmsnorm_fwd(std::int64_t rows, int h, float eps, const void* x, const void* r, const void* w,
+                               void* s_out, void* y, float* rstd, cudaStream_t s) {
+  if (!rmsnorm_supported(h) || rows < 1 || rows > 0x7fffffff || (r == nullptr) != (s_out == nullptr))
+    return cudaErrorInvalidValue;
+  const unsigned grid = static_cast<unsigned>(rows);
+  auto X = static_cast<const uint4*>(x);
+  auto R = static_cast<const uint4*>(r);
+  auto W = static_cast<const uint4*>(w);
+  auto SO = static_cast<uint4*>(s_out);
+  auto Y = static_cast<uint4*>(y);
+  switch (h / 1024) {
+#define FCDP_RMS_FWD(V)                                                                           \
+  case V:                                                                                         \
+    if (r)                                                                                        \
+      rms_fwd_kernel<V, true><<<grid, kRmsThreads, 0, s>>>(h, eps, X, R, W, SO, Y, rstd);         \
+    else                                                                                          \
+      rms_fwd_kernel<V, false><<<grid, kRmsThreads, 0, s>>>(h, eps, X, nullptr, W, nullptr, Y, rstd); \
+    break;
+    FCDP_RMS_FWD(1) FCDP_RMS_FWD(2) FCDP_RMS_FWD(3) FCDP_RMS_FWD(4) FCDP_RMS_FWD(5) FCDP_RMS_FWD(6) FCDP_RMS_FWD(7)
+    FCDP_RMS_FWD(8)
+#undef FCDP_RMS_FWD
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rmsnorm_bwd(std::int64_t rows, int h, const void* dy, const void* x, const void* w,
+                               const float* rstd, const void* dres, void* dx, void* dw, float* part, int splits,
+                               cudaStream_t s) {
+  if (!rmsnorm_supported(h) || rows < 1 || rows > 0x7fffffff || splits < 1) return cudaErrorInvalidValue;
+  const unsigned grid = static_cast<unsigned>(rows);
+  auto DY = static_cast<const uint4*>(dy);
+  auto X = static_cast<const uint4*>(x);
+  auto W = static_cast<const uint4*>(w);
+  auto DR = static_cast<const uint4*>(dres);
+  auto DX = static_cast<uint4*>(dx);
+  switch (h / 1024) {
+#define FCDP_RMS_BWD(V)                                                                       \
+  case V:                                                                                     \
+    if (dres)                                                                                 \
+      rms_bwd_dx_kernel<V, true><<<grid, kRmsThreads, 0, s>>>(h, DY, X, W, rstd, DR, DX);      \
+    else                                                                                      \
+      rms_bwd_dx_kernel<V, false><<<grid, kRmsThreads, 0, s>>>(h, DY, X, W, rstd, nullptr, DX); \
+    break;
+    FCDP_RMS_BWD(1) FCDP_RMS_BWD(2) FCDP_RMS_BWD(3) FCDP_RMS_BWD(4) FCDP_RMS_BWD(5) FCDP_RMS_BWD(6) FCDP_RMS_BWD(7)
+    FCDP_RMS_BWD(8)
+#undef FCDP_RMS_BWD
+    default: return cudaErrorInvalidValue;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || !dw) return e;
+  const dim3 g2((h / 8 + kColThreads - 1) / kColThreads, splits);
+  unsigned int* ctr = counter_slots();
+  if (!ctr || g2.x > kCounterSlots) return cudaErrorInvalidValue;
+  rms_bwd_dw_partial_kernel<<<g2, kColThreads * kRowLanes, 0, s>>>(rows, h, splits, DY, X, rstd, part, ctr,
+                                                                   static_cast<__nv_bfloat16*>(dw));
   return cudaGetLastError();
 }
 

@@ -47,4 +47,12 @@ cudaError_t launch_swiglu_bwd(std::int64_t rows, int f, const void* dy, const vo
                               const void* u, std::int64_t u_stride, void* dg, std::int64_t dg_stride, void* du,
                               std::int64_t du_stride, cudaStream_t s);
 
+// Llama RMSNorm (h a multiple of 1024, <= 8192): y = x * rstd * w (r / s_out: residual sum first)
+bool rmsnorm_supported(int h);
+cudaError_t launch_rmsnorm_fwd(std::int64_t rows, int h, float eps, const void* x, const void* r, const void* w,
+                               void* s_out, void* y, float* rstd, cudaStream_t s);
+cudaError_t launch_rmsnorm_bwd(std::int64_t rows, int h, const void* dy, const void* x, const void* w,
+                               const float* rstd, const void* dres, void* dx, void* dw, float* part, int splits,
+                               cudaStream_t s);
+
 }  // namespace fcdp

@@ -1542,8 +1542,15 @@ void Engine::exec(std::uint32_t event_id) {
       for (shardsim::EventId d : e.deps) flush |= d2h_deferred_id_[d] != 0;
       if (flush) flush_deferred_d2h();
     }
+    // With tracing on, a dependent waits on the dependency's trace-end event
+    // itself (recorded right after its done event on the same stream): the two
+    // records are separate front-end commands, and waiting on the done event let
+    // a dependent's begin timestamp precede the dependency's end timestamp when
+    // the producer's channel was descheduled between them (seen once with two
+    // ranks time-sharing one GPU), which the trace check reads as a violation.
     for (shardsim::EventId d : e.deps)
-      if (stream_of[d] != s) CK(cudaStreamWaitEvent(s, ev_done_[d], 0));
+      if (stream_of[d] != s)
+        CK(cudaStreamWaitEvent(s, trace_ && d < traced_events_ ? trace_end_[d] : ev_done_[d], 0));
     // (the staging side s_agsend_ needs none of the program's deps: its source,
     //  the own shard, is final since the previous iteration joined, and buffer
     //  reuse on it is guarded by the receivers' consumed markers - so the NIC

@@ -256,6 +256,89 @@ def _make_add_layernorm():
     return AddLayerNormFn
 
 
+_RMS = None
+
+
+def _rms_norm(x, w, r=None, eps=1e-5):
+    """RMSNorm of x (or of the residual sum s = x + r, returned as (s, y)) on
+    libfcdp's kernels for bf16 rows with h a multiple of 1024; torch otherwise."""
+    global _RMS
+    import torch
+    import torch.nn.functional as F
+    h = x.shape[-1]
+    if not (x.is_cuda and x.dtype == torch.bfloat16 and h % 1024 == 0 and h <= 8192
+            and (r is None or r.dtype == torch.bfloat16)):
+        if r is None:
+            return F.rms_norm(x, (h,), w, eps=eps)
+        s_ = x + r
+        return s_, F.rms_norm(s_, (h,), w, eps=eps)
+    if _RMS is None:
+        _RMS = _make_rmsnorm()
+    if r is None:
+        return _RMS[0].apply(x, w, eps)
+    return _RMS[1].apply(x, r, w, eps)
+
+
+def _make_rmsnorm():
+    import ctypes as C
+    import torch
+    from ._capi import check, lib
+
+    P = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+    S = lambda dev: C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+    def fwd(x, r, w, eps):
+        xc = x.contiguous()
+        h = xc.shape[-1]
+        rows = xc.numel() // h
+        y = torch.empty_like(xc)
+        s_ = torch.empty_like(xc) if r is not None else None
+        rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
+        rc = r.contiguous() if r is not None else None
+        check(lib().fcdp_rmsnorm_fwd(rows, h, eps, P(xc), P(rc), P(w), P(s_), P(y), P(rstd), S(x.device)))
+        return (s_ if r is not None else xc), y, rstd
+
+    def bwd(ctx, dy, dres, want_w):
+        xin, w, rstd = ctx.saved_tensors
+        h = xin.shape[-1]
+        rows = xin.numel() // h
+        dyc = dy.contiguous() if dy is not None else torch.zeros_like(xin)
+        drc = dres.contiguous() if dres is not None else None
+        dx = torch.empty_like(xin)
+        splits = 64
+        dw = torch.empty(h, dtype=w.dtype, device=w.device) if want_w else None
+        scratch = torch.empty(splits * h, dtype=torch.float32, device=xin.device) if want_w else None
+        check(lib().fcdp_rmsnorm_bwd(rows, h, P(dyc), P(xin), P(w), P(rstd), P(drc), P(dx), P(dw), P(scratch), splits,
+                                     S(xin.device)))
+        return dx, dw
+
+    class RMSNormFn(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, x, w, eps):
+            xin, y, rstd = fwd(x, None, w, eps)
+            ctx.save_for_backward(xin, w, rstd)
+            return y
+
+        @staticmethod
+        def backward(ctx, dy):
+            dx, dw = bwd(ctx, dy, None, ctx.needs_input_grad[1])
+            return dx, dw, None
+
+    class AddRMSNormFn(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, x, r, w, eps):
+            s_, y, rstd = fwd(x, r, w, eps)
+            ctx.save_for_backward(s_, w, rstd)
+            return s_, y
+
+        @staticmethod
+        def backward(ctx, ds, dy):
+            dx, dw = bwd(ctx, dy, ds, ctx.needs_input_grad[2])
+            return dx, dx, dw, None
+
+    return RMSNormFn, AddRMSNormFn
+
+
 def _make_layernorm():
     import ctypes as C
     import torch
@@ -722,7 +805,7 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
         return x + _gpt2_mlp(m, p)
     if ldef.kind == "llama_block":
         b, s, _ = x.shape
-        a = F.rms_norm(x, (h,), p["attn_norm"], eps=1e-5)
+        a = _rms_norm(x, p["attn_norm"])
 
         def proj(name, inp):
             if f"{name}_A" in p and _fused_ok(inp, p[f"{name}_w"]):
@@ -742,14 +825,13 @@ def layer_forward(cfg: ModelConfig, ldef: LayerDef, p, x, tokens=None, labels=No
             k = _rope_fn(proj("k", a).view(b, s, nh, h // nh)).transpose(1, 2)
             v = proj("v", a).view(b, s, nh, h // nh).transpose(1, 2)
         o = F.scaled_dot_product_attention(q, k, v, is_causal=True)
-        x = x + proj("o", o.transpose(1, 2).reshape(b, s, h))
-        m = F.rms_norm(x, (h,), p["mlp_norm"], eps=1e-5)
+        x, m = _rms_norm(x, p["mlp_norm"], r=proj("o", o.transpose(1, 2).reshape(b, s, h)))
         return x + F.linear(_swiglu_mlp(m, p["gate_w"], p["up_w"]), p["down_w"])
     if ldef.kind == "head":
         if "lnf_w" in p:
             a = _layer_norm(x, p["lnf_w"], p["lnf_b"])
         else:
-            a = F.rms_norm(x, (h,), p["norm_w"], eps=1e-5)
+            a = _rms_norm(x, p["norm_w"])
         logits = F.linear(a, p["lm_w"])
         return _cross_entropy(logits, labels)
     raise ValueError(ldef.kind)

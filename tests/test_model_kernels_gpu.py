@@ -334,3 +334,47 @@ def test_add_layernorm_matches_fp32(built, rows, h):
                                     (w.grad, wt.grad, wr.grad, "dw"), (b.grad, bt.grad, br.grad, "db")):
         e_ours, e_torch = _rel(ours, ref), _rel(theirs, ref)
         assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
+
+
+@pytest.mark.parametrize("rows,h,res,train", [(4096, 4096, False, True), (4096, 4096, True, False), (33, 5120, True, True),
+                                              (8, 1024, False, False)])
+def test_rmsnorm_matches_fp32(built, rows, h, res, train):
+    """Llama RMSNorm (and its residual-add variant) vs fp32 torch, incl. dgamma."""
+    from paper_2602_06499_b200.driving_model import _rms_norm
+    import torch.nn.functional as F
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(rows + h + res)
+    x = (torch.randn(rows, h, device=dev, generator=g) * 2).to(torch.bfloat16).requires_grad_(True)
+    r = (torch.randn(rows, h, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(True) if res else None
+    w = (1 + 0.1 * torch.randn(h, device=dev, generator=g)).to(torch.bfloat16).requires_grad_(train)
+    dy, ds = (torch.randn(rows, h, device=dev, generator=g).to(torch.bfloat16) for _ in range(2))
+
+    def run(x_, r_, w_, ref):
+        if res:
+            s_ = x_ + r_
+            y_ = F.rms_norm(s_, (h,), w_, eps=1e-5)
+            torch.autograd.backward((s_, y_), (ds.float() if ref else ds, dy.float() if ref else dy))
+            return s_, y_
+        y_ = F.rms_norm(x_, (h,), w_, eps=1e-5)
+        y_.backward(dy.float() if ref else dy)
+        return None, y_
+
+    out = _rms_norm(x, w, r=r)
+    s_, y = out if res else (None, out)
+    torch.autograd.backward((s_, y) if res else (y,), (ds, dy) if res else (dy,))
+    xr, wr = x.detach().float().requires_grad_(True), w.detach().float().requires_grad_(train)
+    rr = r.detach().float().requires_grad_(True) if res else None
+    _, yr = run(xr, rr, wr, True)
+    xt, wt = x.detach().clone().requires_grad_(True), w.detach().clone().requires_grad_(train)
+    rt = r.detach().clone().requires_grad_(True) if res else None
+    st_, yt = run(xt, rt, wt, False)
+    if res:
+        assert torch.equal(s_, st_)
+    pairs = [(y, yt, yr, "y"), (x.grad, xt.grad, xr.grad, "dx")]
+    if res:
+        pairs.append((r.grad, rt.grad, rr.grad, "dr"))
+    if train:
+        pairs.append((w.grad, wt.grad, wr.grad, "dw"))
+    for ours, theirs, ref, name in pairs:
+        e_ours, e_torch = _rel(ours, ref), _rel(theirs, ref)
+        assert e_ours <= max(1.5 * e_torch, 8e-3), (name, e_ours, e_torch)
