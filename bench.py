@@ -36,7 +36,7 @@ def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="fcdp", choices=["fcdp", "reference"])
     p.add_argument("--preset", default="gpt2-1.3b")
     p.add_argument("--strategy", default="fcdp")
