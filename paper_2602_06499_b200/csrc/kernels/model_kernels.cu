@@ -655,20 +655,20 @@ __global__ void __launch_bounds__(kRmsThreads) rms_bwd_dx_kernel(int h, const ui
 // 16-byte vector (4 pairs) per thread, fp32 arithmetic, one rounding.
 // xs / ys: token strides of x and y in 16-byte vectors (heads * dim / 8 when
 // contiguous; larger for one third of a joint [tokens x 3h] q|k|v projection).
-__global__ void __launch_bounds__(256) rope_kernel(std::int64_t nvec, int seq, int heads, int dim,
+// Grid: x over a token's vectors, y over tokens (a grid-stride loop past 65535):
+// no per-element 64-bit index division (which made the flat version issue-bound).
+__global__ void __launch_bounds__(256) rope_kernel(std::int64_t tokens, int seq, int vrow, int vdim,
                                                    const uint4* __restrict__ x, std::int64_t xs,
                                                    const float* __restrict__ cs, const float* __restrict__ sn,
                                                    float sign, uint4* __restrict__ y, std::int64_t ys) {
-  const std::int64_t step = static_cast<std::int64_t>(gridDim.x) * blockDim.x;
-  const int vrow = heads * dim / 8;  // vectors per token
-  const int vdim = dim / 8;
-  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nvec; i += step) {
-    const std::int64_t tok = i / vrow;
-    const int col = static_cast<int>(i - tok * vrow);
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= vrow) return;
+  const int d0 = (col % vdim) * 4;  // first rotated pair of this vector
+  const int half = vdim * 4;        // dim / 2
+  for (std::int64_t tok = blockIdx.y; tok < tokens; tok += gridDim.y) {
     const int pos = static_cast<int>(tok % seq);
-    const int d0 = (col % vdim) * 4;  // first pair index
-    const float4 c = __ldg(reinterpret_cast<const float4*>(cs + static_cast<std::int64_t>(pos) * (dim / 2) + d0));
-    const float4 s4 = __ldg(reinterpret_cast<const float4*>(sn + static_cast<std::int64_t>(pos) * (dim / 2) + d0));
+    const float4 c = __ldg(reinterpret_cast<const float4*>(cs + static_cast<std::int64_t>(pos) * half + d0));
+    const float4 s4 = __ldg(reinterpret_cast<const float4*>(sn + static_cast<std::int64_t>(pos) * half + d0));
     const float cc[4] = {c.x, c.y, c.z, c.w};
     const float ss[4] = {sign * s4.x, sign * s4.y, sign * s4.z, sign * s4.w};
     float v[8], o[8];
@@ -898,10 +898,11 @@ cudaError_t launch_rope(std::int64_t batch, int seq, int heads, int dim, const v
   if (dim % 8 || batch < 1 || seq < 1 || heads < 1 || x_stride % 8 || y_stride % 8 || x_stride < row ||
       y_stride < row)
     return cudaErrorInvalidValue;
-  const std::int64_t nvec = batch * seq * row / 8;
-  rope_kernel<<<elementwise_grid(nvec), 256, 0, s>>>(nvec, seq, heads, dim, static_cast<const uint4*>(x),
-                                                     x_stride / 8, cs, sn, inverse ? -1.0f : 1.0f,
-                                                     static_cast<uint4*>(y), y_stride / 8);
+  const std::int64_t tokens = batch * seq;
+  const int vrow = static_cast<int>(row / 8);
+  const dim3 grid((vrow + 255) / 256, static_cast<unsigned>(std::min<std::int64_t>(tokens, 65535)));
+  rope_kernel<<<grid, 256, 0, s>>>(tokens, seq, vrow, dim / 8, static_cast<const uint4*>(x), x_stride / 8, cs, sn,
+                                   inverse ? -1.0f : 1.0f, static_cast<uint4*>(y), y_stride / 8);
   return cudaGetLastError();
 }
 

@@ -21,7 +21,8 @@ CLASSES = [("adamw_fused_rs", r"adam_grad_kernel"), ("adamw", r"adam_kernel"), (
            # driving-model kernels (model_kernels.cu): the path's consumer, not the path
            ("model_bias_gelu_fwd", r"bias_gelu_fwd_kernel"), ("model_gelu_bwd_bias_grad", r"colsum_partial_kernel<(true|1)>"),
            ("model_bias_grad", r"colsum_(partial|final)_kernel"), ("model_layernorm", r"ln_(fwd|bwd)"),
-           ("model_xent", r"xent_(fwd|bwd)_kernel"), ("model_rope", r"rope_kernel"), ("model_swiglu", r"swiglu_")]
+           ("model_xent", r"xent_(fwd|bwd)_kernel"), ("model_rope", r"rope_kernel"), ("model_swiglu", r"swiglu_"),
+           ("model_rmsnorm", r"rms_(fwd|bwd)")]
 
 
 def ours(name):
